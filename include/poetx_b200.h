@@ -1,0 +1,221 @@
+/*
+ * poetx_b200.h -- C ABI of the B200-native POET-X hot path.
+ *
+ * The reference (/root/reference/pkg/src/poetx) is a pure-Python package
+ * with no FFI; its "plugin/operator API" for this path is the set of Python
+ * functions cited beside each entry point below.  The Python package
+ * paper_2603_05500_b200 mirrors those functions one-to-one and reaches the
+ * GPU only through this ABI (ctypes).  Any other host
+ * (C, C++, Rust, Go via cgo) can bind the same symbols.
+ *
+ * Conventions
+ *   - every pointer named d_* or passed as `void*` data is DEVICE memory
+ *     unless stated otherwise; matrices are row-major, contiguous;
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default);
+ *     all device work is stream-ordered, nothing synchronises the host;
+ *   - return value: POETX_OK (0) or a positive POETX_E* class code;
+ *     poetx_last_error() returns the thread-local message.  The Python
+ *     wrapper maps codes to the reference's exception classes
+ *     (errors.py:9-42: ShapeError, ConfigError, StateError, NumericsError);
+ *   - the library never allocates persistent device memory; callers pass
+ *     workspaces sized by the *_workspace_bytes queries.
+ */
+#ifndef POETX_B200_H
+#define POETX_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POETX_ABI_VERSION 1
+
+/* element types */
+enum { POETX_F32 = 0, POETX_F64 = 1, POETX_BF16 = 2 };
+/* status codes (errors.py:9-42) */
+enum {
+  POETX_OK = 0,
+  POETX_ESHAPE = 1,    /* ShapeError   */
+  POETX_ECONFIG = 2,   /* ConfigError  */
+  POETX_ESTATE = 3,    /* StateError   */
+  POETX_ENUMERICS = 4, /* NumericsError */
+  POETX_ECUDA = 5      /* CUDA runtime / launch failure */
+};
+/* layer variants (layer.py:68) */
+enum { POETX_FAST = 0, POETX_MEM = 1 };
+
+const char* poetx_last_error(void);
+int poetx_abi_version(void);
+/* number of device kernels this library has launched in this process */
+uint64_t poetx_launch_count(void);
+/* 1 if the tcgen05/TMA GEMM path is compiled in and enabled */
+int poetx_tc_enabled(void);
+void poetx_set_tc_enabled(int on);
+
+/* ---------------------------------------------------------------- H1 RNG --
+ * numpy Generator(Philox) state (the reference draws permutations through
+ * numpy: linalg.py:264-291 Rng, permute.py:79-83 sample_permutation).
+ * HOST memory.  Bit-exact with numpy 2.x: counter pre-increment, 4-word
+ * buffer, low-then-high uint32 halves, masked-rejection bounded ints,
+ * Fisher-Yates for i = n-1 .. 1.                                            */
+typedef struct {
+  uint64_t counter[4];
+  uint64_t key[2];
+  uint64_t buffer[4];
+  int64_t buffer_pos;
+  int64_t has_uint32;
+  uint64_t uinteger;
+} poetx_philox_state;
+
+/* fresh stream: Rng(seed, stream) (linalg.py:276-279) */
+int poetx_philox_seed(poetx_philox_state* st, uint64_t seed, uint64_t stream);
+/* Rng.permutation(n) -> forward map and its inverse (host int32[n] each;
+ * inv may be NULL) (linalg.py:290-291, permute.py:65-76) */
+int poetx_philox_permutation(poetx_philox_state* st, int64_t n, int32_t* fwd, int32_t* inv);
+
+/* ------------------------------------------------------------------ CNP --
+ * cnp.py.  dtype in {F32, F64}: Q, G, caches and grads in that type.
+ * dtype BF16 is not a CNP dtype (parameters stay fp32 master); use F32 and
+ * request a bf16 copy of G through g_bf16.                                 */
+
+/* skew_from_packed (cnp.py:71-78): q[nb,b,b] from packed[nb, b(b-1)/2] */
+int poetx_skew_from_packed(int dtype, int64_t nb, int64_t b, const void* packed, void* q,
+                           void* stream);
+/* packed_grad_from_skew_grad (cnp.py:81-86): g_ij = dq_ij - dq_ji;
+ * accumulate != 0 adds into g */
+int poetx_packed_grad_from_skew_grad(int dtype, int64_t nb, int64_t b, const void* dq,
+                                     void* g, int accumulate, void* stream);
+size_t poetx_cnp_workspace_bytes(int dtype, int64_t nb, int64_t b, int k);
+/* cnp_forward (cnp.py:99-125).  Input: q (full skew stack) if q != NULL,
+ * else packed params (unpacked in-kernel).  Outputs: g (required),
+ * g_bf16 (optional bf16 copy for the tensor-core path), q2 (optional
+ * cache of Q^2, k == 3 only). */
+int poetx_cnp_forward(int dtype, int64_t nb, int64_t b, int k, const void* q,
+                      const void* packed, void* g, void* g_bf16, void* q2, void* ws,
+                      size_t ws_bytes, void* stream);
+/* cnp_backward (cnp.py:128-158), optionally fused with
+ * packed_grad_from_skew_grad (cnp.py:81-86).  q / packed as above;
+ * q2 may be NULL (recomputed).  Writes dq (full stack) if dq != NULL and
+ * the packed gradient if dpacked != NULL (accumulate != 0 adds). */
+int poetx_cnp_backward(int dtype, int64_t nb, int64_t b, int k, const void* q,
+                       const void* packed, const void* q2, const void* dg, void* dq,
+                       void* dpacked, int accumulate, void* ws, size_t ws_bytes, void* stream);
+/* cayley-free orthogonality audit ||G^T G - I||_F over the stack
+ * (blockdiag.py:134-138).  out: DEVICE double[1]. */
+int poetx_orthogonality_error(int dtype, int64_t nb, int64_t b, const void* g, double* out,
+                              void* ws, size_t ws_bytes, void* stream);
+
+/* ----------------------------------------------------- permutations -----
+ * permute.py.  These are exact data movement in any dtype.                */
+/* y[i, j] = x[i, idx[j]]   (permute_cols / permute_features, permute.py:95-110:
+ * 'forward' passes idx = pi.inverse, 'inverse' passes idx = pi.forward) */
+int poetx_permute_cols(int dtype, int64_t rows, int64_t cols, const int32_t* idx,
+                       const void* x, void* y, void* stream);
+/* y[i, :] = x[idx[i], :]   (permute_rows, permute.py:86-92) */
+int poetx_permute_rows(int dtype, int64_t rows, int64_t cols, const int32_t* idx,
+                       const void* x, void* y, void* stream);
+/* y[i, j] = x[ridx[i], cidx[j]]  (premerge_weight, permute.py:113-125;
+ * also the composite re-permutation of merge_and_reinit) */
+int poetx_gather2d(int dtype, int64_t rows, int64_t cols, const int32_t* ridx,
+                   const int32_t* cidx, const void* x, void* y, void* stream);
+
+/* ------------------------------------------------------- block-diagonal --
+ * blockdiag.py.  g is (nb, b, b) in dtype (BF16 activations take a BF16 g). */
+/* apply_to_features (blockdiag.py:58-73): y_s = x_s g[s] (or g[s]^T) */
+int poetx_apply_to_features(int dtype, int64_t T, int64_t nb, int64_t b, const void* g,
+                            int transpose, const void* x, void* y, void* stream);
+/* apply_to_weight_rows (blockdiag.py:76-90): y_s = g[s] w_s (or g[s]^T w_s) */
+int poetx_apply_to_weight_rows(int dtype, int64_t nb, int64_t b, int64_t cols, const void* g,
+                               int transpose, const void* w, void* y, void* stream);
+size_t poetx_segmented_outer_workspace_bytes(int dtype, int64_t T, int64_t nb, int64_t b);
+/* segmented_outer (blockdiag.py:100-121): out[s] = sum_t x_s^T y_s.
+ * out is F64 for F64 inputs and F32 otherwise (BF16 inputs accumulate in
+ * fp32).  Deterministic split-T reduction.  accumulate != 0 adds. */
+int poetx_segmented_outer(int dtype, int64_t T, int64_t nb, int64_t b, const void* x,
+                          const void* y, void* out, int accumulate, void* ws, size_t ws_bytes,
+                          void* stream);
+
+/* ---------------------------------------------------------------- GEMM --
+ * C[M,N] (+)= op(A)[M,K] op(B)[K,N]; lda/ldb/ldc are row strides of the
+ * stored (untransposed) arrays.  linalg.matmul / matmul_abt
+ * (linalg.py:42-83) are (transB = 0 / 1).  BF16 inputs accumulate in fp32
+ * and store BF16; with tc enabled BF16 shapes that tile evenly run on the
+ * tcgen05/TMA kernel. */
+int poetx_matmul(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
+                 int transA, const void* B, int64_t ldb, int transB, void* C, int64_t ldc,
+                 int accumulate, void* stream);
+
+/* ---------------------------------------------------------------- layer --
+ * PoetLinearLayer forward/backward (layer.py:214-256) as one call each.  */
+typedef struct {
+  int dtype;        /* activation / frozen-weight type: F32, F64 or BF16 */
+  int variant;      /* POETX_FAST or POETX_MEM */
+  int neumann_k;
+  int64_t m, n, b;  /* in-features, out-features, block size */
+  const int32_t* perm_in_fwd;  /* device int32[m] */
+  const int32_t* perm_in_inv;
+  const int32_t* perm_out_fwd; /* device int32[n] */
+  const int32_t* perm_out_inv;
+  const void* premerged;       /* device [m, n] = W[pi_in(i), pi_out(j)] */
+} poetx_layer_desc;
+
+/* factor state produced by poetx_layer_factors and consumed by fwd/bwd.
+ * Parameter/factor type: F64 for F64 layers, else F32 (fp32 master). */
+typedef struct {
+  const void* packed_r;  /* [m/b, b(b-1)/2] */
+  const void* packed_p;  /* [n/b, b(b-1)/2] */
+  void* g_r;             /* [m/b, b, b] param type */
+  void* g_p;
+  void* g_r_lowp;        /* BF16 copies (BF16 layers only, else NULL) */
+  void* g_p_lowp;
+  void* q2_r;            /* Q^2 caches (k == 3), may be NULL */
+  void* q2_p;
+} poetx_layer_factors_t;
+
+size_t poetx_layer_workspace_bytes(const poetx_layer_desc* d, int64_t T);
+int poetx_layer_factors(const poetx_layer_desc* d, poetx_layer_factors_t* f, void* ws,
+                        size_t ws_bytes, void* stream);
+/* z[T,n] = layer(x[T,m]); saved_t[T,n] written when non-NULL (fast). */
+int poetx_layer_forward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                        const void* x, void* z, void* saved_t, void* ws, size_t ws_bytes,
+                        void* stream);
+/* grads: dx[T,m] (may be NULL), packed grads (param type; accumulate != 0
+ * adds into them).  saved_t NULL => recompute (mem variant). */
+int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                         const void* x, const void* dz, const void* saved_t, void* dx,
+                         void* dpacked_r, void* dpacked_p, int accumulate, void* ws,
+                         size_t ws_bytes, void* stream);
+/* merge_and_reinit numerics (layer.py:260-314): new premerged
+ * PM'[i,j] = M[inv_in(new_in(i)), inv_out(new_out(j))] with
+ * M = blockdiag(G_R) PM blockdiag(G_P) computed in fp32/fp64 from the
+ * given factors; optional W_out = Psi^T M Psi (materialize_weight). */
+size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d);
+int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_p,
+                      const int32_t* new_in_fwd, const int32_t* new_out_fwd,
+                      void* premerged_out, void* w_out, void* ws, size_t ws_bytes,
+                      void* stream);
+
+/* ------------------------------------------------------------ optimizer --
+ * optim.py.  Multi-tensor: host arrays of device pointers.               */
+/* sum of squares in float64 over all tensors into DEVICE double out[0]
+ * (global_grad_norm, optim.py:77-81, squared); nonfinite (DEVICE int) is
+ * set to 1 if any element is inf/nan. */
+int poetx_sqnorm(int dtype, int ntensors, const void* const* g, const int64_t* numel,
+                 double* out, int* nonfinite, void* ws, size_t ws_bytes, void* stream);
+size_t poetx_sqnorm_workspace_bytes(int ntensors, const int64_t* numel);
+/* fused clip + AdamW (optim.py:84-94 + 127-148), arithmetic in the param
+ * type with the reference's operation order.  If sqnorm != NULL (DEVICE
+ * double) and sqrt(*sqnorm) > clip_threshold, grads are first scaled by
+ * (type)(clip_threshold / norm) -- written back to g when write_back_grads.
+ * bc1 = 1 - beta1^t, bc2 = 1 - beta2^t computed by the caller in double. */
+int poetx_adamw(int dtype, int ntensors, void* const* p, void* const* g, void* const* m,
+                void* const* v, const int64_t* numel, double lr, double beta1, double beta2,
+                double eps, double weight_decay, double bc1, double bc2, const double* sqnorm,
+                double clip_threshold, int write_back_grads, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POETX_B200_H */

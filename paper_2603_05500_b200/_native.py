@@ -1,0 +1,208 @@
+"""ctypes binding of the C ABI (include/poetx_b200.h).
+
+This is the ONLY way the package reaches the GPU.  There is no CPU or
+PyTorch fallback: if libpoetx_b200.so is missing or fails to load, every
+entry point raises immediately.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import numpy as np
+import torch
+
+from .errors import ConfigError, NumericsError, PoetxError, ShapeError, StateError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpoetx_b200.so")
+
+F32, F64, BF16 = 0, 1, 2
+FAST, MEM = 0, 1
+_CODES = {1: ShapeError, 2: ConfigError, 3: StateError, 4: NumericsError, 5: PoetxError}
+
+VP = C.c_void_p
+I64 = C.c_int64
+I32 = C.c_int
+SZ = C.c_size_t
+
+
+class PhiloxState(C.Structure):
+    _fields_ = [
+        ("counter", C.c_uint64 * 4),
+        ("key", C.c_uint64 * 2),
+        ("buffer", C.c_uint64 * 4),
+        ("buffer_pos", C.c_int64),
+        ("has_uint32", C.c_int64),
+        ("uinteger", C.c_uint64),
+    ]
+
+
+class LayerDesc(C.Structure):
+    _fields_ = [
+        ("dtype", C.c_int),
+        ("variant", C.c_int),
+        ("neumann_k", C.c_int),
+        ("m", C.c_int64),
+        ("n", C.c_int64),
+        ("b", C.c_int64),
+        ("perm_in_fwd", VP),
+        ("perm_in_inv", VP),
+        ("perm_out_fwd", VP),
+        ("perm_out_inv", VP),
+        ("premerged", VP),
+    ]
+
+
+class LayerFactors(C.Structure):
+    _fields_ = [
+        ("packed_r", VP),
+        ("packed_p", VP),
+        ("g_r", VP),
+        ("g_p", VP),
+        ("g_r_lowp", VP),
+        ("g_p_lowp", VP),
+        ("q2_r", VP),
+        ("q2_p", VP),
+    ]
+
+
+_SIGS = {
+    "poetx_last_error": (C.c_char_p, []),
+    "poetx_abi_version": (I32, []),
+    "poetx_launch_count": (C.c_uint64, []),
+    "poetx_tc_enabled": (I32, []),
+    "poetx_set_tc_enabled": (None, [I32]),
+    "poetx_philox_seed": (I32, [C.POINTER(PhiloxState), C.c_uint64, C.c_uint64]),
+    "poetx_philox_permutation": (I32, [C.POINTER(PhiloxState), I64, VP, VP]),
+    "poetx_skew_from_packed": (I32, [I32, I64, I64, VP, VP, VP]),
+    "poetx_packed_grad_from_skew_grad": (I32, [I32, I64, I64, VP, VP, I32, VP]),
+    "poetx_cnp_workspace_bytes": (SZ, [I32, I64, I64, I32]),
+    "poetx_cnp_forward": (I32, [I32, I64, I64, I32, VP, VP, VP, VP, VP, VP, SZ, VP]),
+    "poetx_cnp_backward": (I32, [I32, I64, I64, I32, VP, VP, VP, VP, VP, VP, I32, VP, SZ, VP]),
+    "poetx_orthogonality_error": (I32, [I32, I64, I64, VP, VP, VP, SZ, VP]),
+    "poetx_permute_cols": (I32, [I32, I64, I64, VP, VP, VP, VP]),
+    "poetx_permute_rows": (I32, [I32, I64, I64, VP, VP, VP, VP]),
+    "poetx_gather2d": (I32, [I32, I64, I64, VP, VP, VP, VP, VP]),
+    "poetx_apply_to_features": (I32, [I32, I64, I64, I64, VP, I32, VP, VP, VP]),
+    "poetx_apply_to_weight_rows": (I32, [I32, I64, I64, I64, VP, I32, VP, VP, VP]),
+    "poetx_segmented_outer_workspace_bytes": (SZ, [I32, I64, I64, I64]),
+    "poetx_segmented_outer": (I32, [I32, I64, I64, I64, VP, VP, VP, I32, VP, SZ, VP]),
+    "poetx_matmul": (I32, [I32, I64, I64, I64, VP, I64, I32, VP, I64, I32, VP, I64, I32, VP]),
+    "poetx_layer_workspace_bytes": (SZ, [C.POINTER(LayerDesc), I64]),
+    "poetx_layer_factors": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), VP, SZ, VP]),
+    "poetx_layer_forward": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I64, VP, VP, VP,
+                                  VP, SZ, VP]),
+    "poetx_layer_backward": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I64, VP, VP, VP,
+                                   VP, VP, VP, I32, VP, SZ, VP]),
+    "poetx_merge_workspace_bytes": (SZ, [C.POINTER(LayerDesc)]),
+    "poetx_layer_merge": (I32, [C.POINTER(LayerDesc), VP, VP, VP, VP, VP, VP, VP, SZ, VP]),
+    "poetx_sqnorm_workspace_bytes": (SZ, [I32, VP]),
+    "poetx_sqnorm": (I32, [I32, I32, VP, VP, VP, VP, VP, SZ, VP]),
+    "poetx_adamw": (I32, [I32, I32, VP, VP, VP, VP, VP, C.c_double, C.c_double, C.c_double,
+                          C.c_double, C.c_double, C.c_double, C.c_double, VP, C.c_double, I32, VP]),
+}
+
+EXPORTED_SYMBOLS = tuple(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def lib():
+    """Load libpoetx_b200.so once; fail loudly if it is missing."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(LIB_PATH):
+                raise RuntimeError(
+                    f"{LIB_PATH} is missing: build it with `python -m paper_2603_05500_b200.build` "
+                    "(there is no CPU fallback)"
+                )
+            handle = C.CDLL(LIB_PATH)
+            for name, (res, args) in _SIGS.items():
+                fn = getattr(handle, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = handle
+    return _lib
+
+
+def check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().poetx_last_error().decode("utf-8", "replace")
+        raise _CODES.get(rc, PoetxError)(msg)
+
+
+def call(name: str, *args) -> None:
+    check(getattr(lib(), name)(*args))
+
+
+def launch_count() -> int:
+    return int(lib().poetx_launch_count())
+
+
+# -------------------------------------------------------------- tensors ------
+
+_TORCH_CODE = {torch.float32: F32, torch.float64: F64, torch.bfloat16: BF16}
+
+
+def dtype_code(dt: torch.dtype) -> int:
+    try:
+        return _TORCH_CODE[dt]
+    except KeyError:
+        raise ShapeError(f"unsupported dtype {dt}") from None
+
+
+def ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def stream_ptr(device=None) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def require_cuda(t: torch.Tensor, what: str) -> None:
+    if not t.is_cuda:
+        raise ShapeError(f"{what} must be a CUDA tensor (no CPU fallback)")
+    if not t.is_contiguous():
+        raise ShapeError(f"{what} must be contiguous")
+
+
+class _WorkspacePool:
+    """One growable scratch buffer per (device, stream).  Kernels are
+    stream-ordered, so reuse on the same stream is race-free."""
+
+    def __init__(self):
+        self._bufs = {}
+
+    def get(self, nbytes: int, device=None) -> torch.Tensor:
+        dev = torch.device("cuda", torch.cuda.current_device() if device is None else device.index)
+        key = (dev.index, stream_ptr(dev))
+        buf = self._bufs.get(key)
+        if buf is None or buf.numel() < nbytes:
+            nbytes = max(nbytes, 1 << 20)
+            if buf is not None:
+                nbytes = max(nbytes, int(buf.numel() * 1.5))
+            buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+            self._bufs[key] = buf
+        return buf
+
+    def clear(self):
+        self._bufs.clear()
+
+
+WORKSPACE = _WorkspacePool()
+
+
+def workspace(nbytes: int, device=None):
+    buf = WORKSPACE.get(int(nbytes), device)
+    return buf.data_ptr(), buf.numel()
+
+
+def np_int32_ptr(a: np.ndarray) -> int:
+    assert a.dtype == np.int32 and a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data

@@ -1,0 +1,148 @@
+"""Cayley-Neumann parameterization on the GPU (reference cnp.py).
+
+Packed strict-upper-triangle skew parameters (row-major pair order,
+cnp.py:66-68) unpack to Q; the factor is G = (I + Q)(I + sum_{i<=k} Q^i),
+for k = 3 regrouped as G = 2(Q + Q^2 + Q^2 Q) + Q^2 Q^2 + I (three block
+products, Q^2 cached) with the six-product closed-form backward
+(cnp.py:128-145).  All arithmetic runs in libpoetx_b200 kernels; numpy
+inputs are accepted for drop-in use and come back as numpy.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import ConfigError, ShapeError
+
+
+def num_pairs(block_dim: int) -> int:
+    return block_dim * (block_dim - 1) // 2
+
+
+def _to_dev(a, dtype=None):
+    if isinstance(a, np.ndarray):
+        t = torch.from_numpy(np.ascontiguousarray(a)).cuda()
+        return (t if dtype is None else t.to(dtype)), True
+    return a, False
+
+
+def _out(t, was_np):
+    return t.cpu().numpy() if was_np else t
+
+
+@dataclass
+class SkewParams:
+    """Packed skew-symmetric parameters for a stack of blocks (cnp.py:42-59).
+    ``packed`` is a device tensor (num_blocks, b(b-1)/2)."""
+
+    num_blocks: int
+    block_dim: int
+    packed: torch.Tensor
+
+    def __post_init__(self):
+        if isinstance(self.packed, np.ndarray):
+            self.packed = torch.from_numpy(np.ascontiguousarray(self.packed)).cuda()
+        want = (self.num_blocks, num_pairs(self.block_dim))
+        if tuple(self.packed.shape) != want:
+            raise ShapeError(f"packed shape {tuple(self.packed.shape)}, expected {want}")
+
+    @classmethod
+    def zeros(cls, num_blocks: int, block_dim: int, dtype=torch.float64, device="cuda") -> "SkewParams":
+        if num_blocks < 1 or block_dim < 1:
+            raise ShapeError(f"bad block layout ({num_blocks}, {block_dim})")
+        return cls(num_blocks, block_dim,
+                   torch.zeros((num_blocks, num_pairs(block_dim)), dtype=dtype, device=device))
+
+
+def _pdtype(t: torch.Tensor) -> int:
+    if t.dtype not in (torch.float32, torch.float64):
+        raise ShapeError(f"CNP dtype must be float32 or float64, got {t.dtype}")
+    return N.dtype_code(t.dtype)
+
+
+def skew_from_packed(params: SkewParams):
+    """Unpack to a (num_blocks, b, b) skew-symmetric stack (cnp.py:71-78)."""
+    p = params.packed
+    b = params.block_dim
+    q = torch.empty((params.num_blocks, b, b), dtype=p.dtype, device=p.device)
+    N.call("poetx_skew_from_packed", _pdtype(p), params.num_blocks, b, p.data_ptr(), q.data_ptr(),
+           N.stream_ptr(p.device))
+    return q
+
+
+def packed_grad_from_skew_grad(dq):
+    """g_ij = dQ_ij - dQ_ji (cnp.py:81-86)."""
+    dq, was_np = _to_dev(dq)
+    if dq.ndim != 3 or dq.shape[1] != dq.shape[2]:
+        raise ShapeError(f"expected a square block stack, got {tuple(dq.shape)}")
+    nb, b, _ = dq.shape
+    g = torch.empty((nb, num_pairs(b)), dtype=dq.dtype, device=dq.device)
+    N.call("poetx_packed_grad_from_skew_grad", _pdtype(dq), nb, b, dq.contiguous().data_ptr(),
+           g.data_ptr(), 0, N.stream_ptr(dq.device))
+    return _out(g, was_np)
+
+
+@dataclass
+class CnpCache:
+    """Saved operands for the backward pass (cnp.py:89-96)."""
+
+    k: int
+    q: torch.Tensor
+    qsq: torch.Tensor | None  # k == 3 fast path
+    powers: list | None = None  # generic path: recomputed on device from q
+
+
+def cnp_forward(q, neumann_k: int = 3):
+    """Blockwise truncated Cayley transform -> (g, cache) (cnp.py:99-125)."""
+    q, was_np = _to_dev(q)
+    if q.ndim != 3 or q.shape[1] != q.shape[2]:
+        raise ShapeError(f"expected a square block stack, got {tuple(q.shape)}")
+    if neumann_k < 1:
+        raise ConfigError(f"neumann_k must be >= 1, got {neumann_k}")
+    q = q.contiguous()
+    nb, b, _ = q.shape
+    dt = _pdtype(q)
+    g = torch.empty_like(q)
+    qsq = torch.empty_like(q) if neumann_k == 3 else None
+    ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(dt, nb, b, neumann_k), q.device)
+    N.call("poetx_cnp_forward", dt, nb, b, neumann_k, q.data_ptr(), None, g.data_ptr(), None,
+           N.ptr(qsq), ws, wsb, N.stream_ptr(q.device))
+    cache = CnpCache(k=neumann_k, q=q, qsq=qsq)
+    if was_np:
+        return g.cpu().numpy(), cache
+    return g, cache
+
+
+def cnp_backward(cache: CnpCache, dg):
+    """Adjoint w.r.t. the full Q stack (cnp.py:128-158); project with
+    packed_grad_from_skew_grad."""
+    dg, was_np = _to_dev(dg)
+    if tuple(dg.shape) != tuple(cache.q.shape):
+        raise ShapeError(f"cotangent shape {tuple(dg.shape)} does not match Q {tuple(cache.q.shape)}")
+    q = cache.q
+    nb, b, _ = q.shape
+    dt = _pdtype(q)
+    dg = dg.to(q.dtype).contiguous()
+    dq = torch.empty_like(q)
+    ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(dt, nb, b, cache.k), q.device)
+    N.call("poetx_cnp_backward", dt, nb, b, cache.k, q.data_ptr(), None, N.ptr(cache.qsq),
+           dg.data_ptr(), dq.data_ptr(), None, 0, ws, wsb, N.stream_ptr(q.device))
+    return _out(dq, was_np)
+
+
+def cayley_exact(q):
+    """Exact Cayley transform (I + Q)(I - Q)^{-1}, blockwise, solved in float64
+    (cnp.py:161-176).  Audit / merge-hook only: uses torch.linalg.solve."""
+    q, was_np = _to_dev(q)
+    if q.ndim != 3 or q.shape[1] != q.shape[2]:
+        raise ShapeError(f"expected a square block stack, got {tuple(q.shape)}")
+    q64 = q.to(torch.float64)
+    eye = torch.eye(q.shape[1], dtype=torch.float64, device=q.device).expand_as(q64)
+    lhs = (eye - q64).transpose(1, 2)
+    rhs = (eye + q64).transpose(1, 2)
+    sol = torch.linalg.solve(lhs, rhs).transpose(1, 2).contiguous().to(q.dtype)
+    return _out(sol, was_np)

@@ -1,0 +1,265 @@
+// PoetLinearLayer orchestration (layer.py:181-314) behind the C ABI:
+// factors (CNP on both sides), forward chain, backward chain, merge.
+// Kernels are stream-ordered; nothing here synchronises the host.
+#include "common.cuh"
+#include "simt_gemm.cuh"
+
+namespace poetx {
+int gemm(int dt, int out_dt, const GemmDesc& d, cudaStream_t st);
+int gather2d(int dt, int64_t rows, int64_t cols, const int32_t* ridx, const int32_t* cidx,
+             const void* x, void* y, cudaStream_t st);
+int apply_features(int dt, int64_t T, int64_t nb, int64_t b, const void* g, int transpose,
+                   const void* x, void* y, cudaStream_t st);
+int apply_weight_rows(int dt, int64_t nb, int64_t b, int64_t cols, const void* g, int transpose,
+                      const void* w, void* y, cudaStream_t st);
+int segmented_outer(int dt, int64_t T, int64_t nb, int64_t b, const void* x, const void* y,
+                    void* out, int accumulate, Workspace& ws, cudaStream_t st);
+size_t cnp_ws_bytes(int dt, int64_t nb, int64_t b, int k);
+size_t outer_ws_bytes(int dt, int64_t T, int64_t nb, int64_t b);
+}  // namespace poetx
+
+using namespace poetx;
+
+namespace {
+
+int check_desc(const poetx_layer_desc* d) {
+  POETX_REQUIRE(d != nullptr, POETX_ESHAPE, "layer: null descriptor");
+  POETX_REQUIRE(valid_dtype(d->dtype), POETX_ESHAPE, "layer: unsupported dtype %d", d->dtype);
+  POETX_REQUIRE(d->b >= 1, POETX_ECONFIG, "block_size must be >= 1, got %lld", (long long)d->b);
+  POETX_REQUIRE(d->m % d->b == 0 && d->n % d->b == 0, POETX_ECONFIG,
+                "layer dims (%lld, %lld) must both be divisible by block_size %lld",
+                (long long)d->m, (long long)d->n, (long long)d->b);
+  POETX_REQUIRE(d->variant == POETX_FAST || d->variant == POETX_MEM, POETX_ECONFIG,
+                "variant must be fast or mem");
+  POETX_REQUIRE(d->neumann_k >= 1, POETX_ECONFIG, "neumann_k must be >= 1, got %d", d->neumann_k);
+  return POETX_OK;
+}
+
+// G used by the activation path: the bf16 copy for BF16 layers
+const void* act_g(const poetx_layer_desc* d, const void* g, const void* g16) {
+  return d->dtype == POETX_BF16 ? g16 : g;
+}
+
+size_t cnp_bwd_ws(const poetx_layer_desc* d) {
+  int pdt = param_dtype(d->dtype);
+  size_t r = cnp_ws_bytes(pdt, d->m / d->b, d->b, d->neumann_k);
+  size_t p = cnp_ws_bytes(pdt, d->n / d->b, d->b, d->neumann_k);
+  return r > p ? r : p;
+}
+
+template <typename Tin, typename Tout>
+__global__ void gather_convert_kernel(int64_t rows, int64_t cols, const int32_t* __restrict__ ridx,
+                                      const int32_t* __restrict__ cidx, const Tin* __restrict__ x,
+                                      Tout* __restrict__ y) {
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const Tin* xr = x + static_cast<int64_t>(ridx ? ridx[r] : r) * cols;
+    Tout* yr = y + r * cols;
+    for (int64_t j = threadIdx.x; j < cols; j += blockDim.x)
+      yr[j] = cvt<Tin, Tout>(xr[cidx ? cidx[j] : j]);
+  }
+}
+
+__global__ void compose_kernel(int64_t n, const int32_t* __restrict__ inv_old,
+                               const int32_t* __restrict__ fwd_new, int32_t* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = inv_old[fwd_new[i]];
+}
+
+template <typename Tin, typename Tout>
+int gather_convert(int64_t rows, int64_t cols, const int32_t* ridx, const int32_t* cidx,
+                   const void* x, void* y, cudaStream_t st) {
+  unsigned grid = static_cast<unsigned>(rows < 148 * 16 ? rows : 148 * 16);
+  gather_convert_kernel<Tin, Tout><<<grid, 256, 0, st>>>(rows, cols, ridx, cidx,
+                                                         static_cast<const Tin*>(x),
+                                                         static_cast<Tout*>(y));
+  POETX_LAUNCHED("gather_convert");
+  return POETX_OK;
+}
+
+int gather_to(int src_dt, int dst_dt, int64_t rows, int64_t cols, const int32_t* ridx,
+              const int32_t* cidx, const void* x, void* y, cudaStream_t st) {
+  if (src_dt == dst_dt) return gather2d(src_dt, rows, cols, ridx, cidx, x, y, st);
+  if (src_dt == POETX_F32 && dst_dt == POETX_BF16)
+    return gather_convert<float, __nv_bfloat16>(rows, cols, ridx, cidx, x, y, st);
+  if (src_dt == POETX_BF16 && dst_dt == POETX_F32)
+    return gather_convert<__nv_bfloat16, float>(rows, cols, ridx, cidx, x, y, st);
+  set_error("gather_to: unsupported conversion %d -> %d", src_dt, dst_dt);
+  return POETX_ESHAPE;
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t poetx_layer_workspace_bytes(const poetx_layer_desc* d, int64_t T) {
+  if (check_desc(d) != POETX_OK) return 0;
+  const size_t e = elt_size(d->dtype), acc = elt_size(param_dtype(d->dtype));
+  const int64_t w = d->m > d->n ? d->m : d->n;
+  size_t act = align_up(static_cast<size_t>(T) * w * e);
+  size_t grads = align_up(static_cast<size_t>(d->m * d->b) * acc) +
+                 align_up(static_cast<size_t>(d->n * d->b) * acc);
+  size_t outer = outer_ws_bytes(d->dtype, T, d->m / d->b, d->b);
+  size_t outer2 = outer_ws_bytes(d->dtype, T, d->n / d->b, d->b);
+  if (outer2 > outer) outer = outer2;
+  size_t cnp = cnp_bwd_ws(d);
+  return 4 * act + grads + (outer > cnp ? outer : cnp) + 8192;
+}
+
+int poetx_layer_factors(const poetx_layer_desc* d, poetx_layer_factors_t* f, void* ws,
+                        size_t ws_bytes, void* stream) {
+  POETX_TRY(check_desc(d));
+  POETX_REQUIRE(f && f->packed_r && f->packed_p && f->g_r && f->g_p, POETX_ESHAPE,
+                "layer_factors: missing factor buffers");
+  if (d->dtype == POETX_BF16)
+    POETX_REQUIRE(f->g_r_lowp && f->g_p_lowp, POETX_ESHAPE, "layer_factors: bf16 layer needs lowp G");
+  const int pdt = param_dtype(d->dtype);
+  const int k = d->neumann_k;
+  void* q2r = k == 3 ? f->q2_r : nullptr;
+  void* q2p = k == 3 ? f->q2_p : nullptr;
+  POETX_TRY(poetx_cnp_forward(pdt, d->m / d->b, d->b, k, nullptr, f->packed_r, f->g_r,
+                              d->dtype == POETX_BF16 ? f->g_r_lowp : nullptr, q2r, ws, ws_bytes,
+                              stream));
+  POETX_TRY(poetx_cnp_forward(pdt, d->n / d->b, d->b, k, nullptr, f->packed_p, f->g_p,
+                              d->dtype == POETX_BF16 ? f->g_p_lowp : nullptr, q2p, ws, ws_bytes,
+                              stream));
+  return POETX_OK;
+}
+
+int poetx_layer_forward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                        const void* x, void* z, void* saved_t, void* ws, size_t ws_bytes,
+                        void* stream) {
+  POETX_TRY(check_desc(d));
+  POETX_REQUIRE(T >= 0 && x && z && f, POETX_ESHAPE, "layer_forward: bad arguments");
+  if (T == 0) return POETX_OK;
+  cudaStream_t st = as_stream(stream);
+  const int dt = d->dtype;
+  const int64_t w = d->m > d->n ? d->m : d->n;
+  const size_t e = elt_size(dt);
+  Workspace wsp(ws, ws_bytes);
+  void* b1 = wsp.take_bytes(T * w * e);
+  void* b2 = wsp.take_bytes(T * w * e);
+  void* b3 = wsp.take_bytes(T * w * e);
+  POETX_REQUIRE(b1 && b2 && b3, POETX_ESHAPE, "layer_forward: workspace too small");
+  void* t = saved_t ? saved_t : b3;
+  // u = x[:, pi_in]  (permute_features 'inverse', layer.py:220)
+  POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b1, st));
+  // a = u blockdiag(G_R)  (mm1, layer.py:221)
+  POETX_TRY(apply_features(dt, T, d->m / d->b, d->b, act_g(d, f->g_r, f->g_r_lowp), 0, b1, b2, st));
+  // t = a PM  (mm2, layer.py:222)
+  POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b2, d->m, 0, d->premerged, d->n, 0, t, d->n, 0, stream));
+  // v = t blockdiag(G_P)  (mm3, layer.py:223)
+  POETX_TRY(apply_features(dt, T, d->n / d->b, d->b, act_g(d, f->g_p, f->g_p_lowp), 0, t, b1, st));
+  // z = v[:, pi_out^-1]  (permute_features 'forward', layer.py:224)
+  POETX_TRY(gather2d(dt, T, d->n, nullptr, d->perm_out_inv, b1, z, st));
+  return POETX_OK;
+}
+
+int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                         const void* x, const void* dz, const void* saved_t, void* dx,
+                         void* dpacked_r, void* dpacked_p, int accumulate, void* ws,
+                         size_t ws_bytes, void* stream) {
+  POETX_TRY(check_desc(d));
+  POETX_REQUIRE(T >= 0 && x && dz && f && dpacked_r && dpacked_p, POETX_ESHAPE,
+                "layer_backward: bad arguments");
+  cudaStream_t st = as_stream(stream);
+  const int dt = d->dtype, pdt = param_dtype(dt);
+  const int64_t w = d->m > d->n ? d->m : d->n, b = d->b, nbr = d->m / b, nbp = d->n / b;
+  const size_t e = elt_size(dt), acc = elt_size(pdt);
+  Workspace wsp(ws, ws_bytes);
+  void* b1 = wsp.take_bytes(T * w * e);
+  void* b2 = wsp.take_bytes(T * w * e);
+  void* b3 = wsp.take_bytes(T * w * e);
+  void* b4 = wsp.take_bytes(T * w * e);
+  void* dgr = wsp.take_bytes(nbr * b * b * acc);
+  void* dgp = wsp.take_bytes(nbp * b * b * acc);
+  POETX_REQUIRE(b1 && b2 && b3 && b4 && dgr && dgp, POETX_ESHAPE,
+                "layer_backward: workspace too small");
+  Workspace tail(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
+  const void* gr = act_g(d, f->g_r, f->g_r_lowp);
+  const void* gp = act_g(d, f->g_p, f->g_p_lowp);
+  // dv = dz[:, pi_out]  (layer.py:238)
+  POETX_TRY(gather2d(dt, T, d->n, nullptr, d->perm_out_fwd, dz, b1, st));
+  const void* t = saved_t;
+  if (!t) {
+    // mem variant: recompute u, a, t with the forward's kernels (bitwise equal)
+    POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b2, st));
+    POETX_TRY(apply_features(dt, T, nbr, b, gr, 0, b2, b3, st));
+    POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b3, d->m, 0, d->premerged, d->n, 0, b4, d->n, 0, stream));
+    t = b4;
+  }
+  // dG_P = segmented_outer(t, dv)  (layer.py:247)
+  POETX_TRY(segmented_outer(dt, T, nbp, b, t, b1, dgp, 0, tail, st));
+  // dt = dv blockdiag(G_P)^T  (layer.py:248)
+  POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, b1, b2, st));
+  // da = dt PM^T  (layer.py:249)
+  POETX_TRY(poetx_matmul(dt, T, d->m, d->n, b2, d->n, 0, d->premerged, d->n, 1, b3, d->m, 0, stream));
+  // u = x[:, pi_in]  (layer.py:250)
+  POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b1, st));
+  // dG_R = segmented_outer(u, da)  (layer.py:251)
+  Workspace tail2(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
+  POETX_TRY(segmented_outer(dt, T, nbr, b, b1, b3, dgr, 0, tail2, st));
+  if (dx) {
+    // du = da blockdiag(G_R)^T ; dx = du[:, pi_in^-1]  (layer.py:252-253)
+    POETX_TRY(apply_features(dt, T, nbr, b, gr, 1, b3, b2, st));
+    POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_inv, b2, dx, st));
+  }
+  // packed grads = P(cnp_backward(.))  (layer.py:254-255)
+  void* cws = static_cast<char*>(ws) + wsp.used;
+  size_t cwsb = ws_bytes - wsp.used;
+  const int k = d->neumann_k;
+  POETX_TRY(poetx_cnp_backward(pdt, nbr, b, k, nullptr, f->packed_r, k == 3 ? f->q2_r : nullptr,
+                               dgr, nullptr, dpacked_r, accumulate, cws, cwsb, stream));
+  POETX_TRY(poetx_cnp_backward(pdt, nbp, b, k, nullptr, f->packed_p, k == 3 ? f->q2_p : nullptr,
+                               dgp, nullptr, dpacked_p, accumulate, cws, cwsb, stream));
+  return POETX_OK;
+}
+
+size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d) {
+  if (check_desc(d) != POETX_OK) return 0;
+  size_t acc = elt_size(param_dtype(d->dtype));
+  return 3 * align_up(static_cast<size_t>(d->m * d->n) * acc) +
+         align_up(static_cast<size_t>(d->m + d->n) * 4) + 4096;
+}
+
+int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_p,
+                      const int32_t* new_in_fwd, const int32_t* new_out_fwd, void* premerged_out,
+                      void* w_out, void* ws, size_t ws_bytes, void* stream) {
+  POETX_TRY(check_desc(d));
+  POETX_REQUIRE(g_r && g_p, POETX_ESHAPE, "layer_merge: missing factors");
+  cudaStream_t st = as_stream(stream);
+  const int dt = d->dtype, pdt = param_dtype(dt);
+  const int64_t m = d->m, n = d->n, b = d->b;
+  const size_t acc = elt_size(pdt);
+  Workspace wsp(ws, ws_bytes);
+  void* pm = wsp.take_bytes(m * n * acc);
+  void* mid1 = wsp.take_bytes(m * n * acc);
+  void* mid2 = wsp.take_bytes(m * n * acc);
+  int32_t* ridx = wsp.take<int32_t>(m);
+  int32_t* cidx = wsp.take<int32_t>(n);
+  POETX_REQUIRE(pm && mid1 && mid2 && ridx && cidx, POETX_ESHAPE, "layer_merge: workspace too small");
+  // mid = blockdiag(G_R) PM blockdiag(G_P) in the parameter type (layer.py:269-271)
+  const void* pm_src = d->premerged;
+  if (dt == POETX_BF16) {
+    POETX_TRY(gather_to(POETX_BF16, POETX_F32, m, n, nullptr, nullptr, d->premerged, pm, st));
+    pm_src = pm;
+  }
+  POETX_TRY(apply_weight_rows(pdt, m / b, b, n, g_r, 0, pm_src, mid1, st));
+  POETX_TRY(apply_features(pdt, m, n / b, b, g_p, 0, mid1, mid2, st));
+  if (w_out) {
+    // W = Psi_m^T mid Psi_n : W[r, c] = mid[inv_in(r), inv_out(c)]  (layer.py:272-273)
+    POETX_TRY(gather_to(pdt, dt, m, n, d->perm_in_inv, d->perm_out_inv, mid2, w_out, st));
+  }
+  if (premerged_out) {
+    POETX_REQUIRE(new_in_fwd && new_out_fwd, POETX_ESHAPE, "layer_merge: missing new permutations");
+    // PM'[i, j] = W[new_in(i), new_out(j)] = mid[inv_in(new_in(i)), inv_out(new_out(j))]
+    compose_kernel<<<grid_for(m, 256), 256, 0, st>>>(m, d->perm_in_inv, new_in_fwd, ridx);
+    POETX_LAUNCHED("compose");
+    compose_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, d->perm_out_inv, new_out_fwd, cidx);
+    POETX_LAUNCHED("compose");
+    POETX_TRY(gather_to(pdt, dt, m, n, ridx, cidx, mid2, premerged_out, st));
+  }
+  return POETX_OK;
+}
+
+}  // extern "C"

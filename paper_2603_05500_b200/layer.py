@@ -1,0 +1,351 @@
+"""POET-X linear layer on the GPU -- drop-in for the reference's
+``poetx.layer`` (layer.py:1-344).
+
+The layer owns a frozen weight stored ONLY in its premerged form
+PM = Psi_m W Psi_n^T (PM[i, j] = W[pi_in(i), pi_out(j)], layer.py:161-167)
+on the device; ``base`` is recomputed from it on demand (exact gather).
+Two packed skew stacks ``q_r`` (m/b blocks) and ``q_p`` (n/b blocks)
+are the trainable state.  Forward (layer.py:214-229)
+
+    u = x[:, pi_in] ; a = u blockdiag(G_R) ; t = a PM ; v = t blockdiag(G_P) ;
+    z = v[:, pi_out^-1]
+
+and the hand-written backward (layer.py:231-256) run as one C-ABI call
+each (csrc/layer.cu).  ``fast`` saves t, ``mem`` recomputes it with the
+same deterministic kernels, so both variants give bitwise-equal grads.
+
+dtypes: float32 / float64 (parity path, CUDA-core FFMA/DFMA) and
+bfloat16 (performance path: tcgen05 tensor cores, fp32 accumulation,
+fp32 master parameters).  numpy inputs are accepted and returned as numpy.
+"""
+
+from __future__ import annotations
+
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .blockdiag import orthogonality_error
+from .cnp import SkewParams, cayley_exact, num_pairs
+from .errors import ConfigError, ShapeError, StateError
+from .permute import PermutationMap, sample_permutation
+from .rng import Rng
+
+VARIANTS = ("fast", "mem")
+
+_NP_TO_TORCH = {np.dtype(np.float32): torch.float32, np.dtype(np.float64): torch.float64}
+
+
+def _torch_dtype(dt) -> torch.dtype:
+    if isinstance(dt, torch.dtype):
+        return dt
+    try:
+        return _NP_TO_TORCH[np.dtype(dt)]
+    except (KeyError, TypeError):
+        raise ShapeError(f"unsupported dtype {dt}") from None
+
+
+def param_dtype(dt: torch.dtype) -> torch.dtype:
+    return torch.float64 if dt == torch.float64 else torch.float32
+
+
+@dataclass
+class LayerCache:
+    """Operands one forward saves for its backward (layer.py:71-81)."""
+
+    x: torch.Tensor
+    g_r: torch.Tensor
+    g_p: torch.Tensor
+    factors: "Factors"
+    saved_mm2: torch.Tensor | None  # fast variant only
+    was_numpy: bool = False
+    consumed: bool = False
+
+
+@dataclass
+class LayerGrads:
+    q_r: torch.Tensor  # packed, same shape as the parameters
+    q_p: torch.Tensor
+    x: torch.Tensor  # cotangent for the layer input
+
+
+@dataclass
+class MergeAudit:
+    merge_index: int
+    orth_err_r: float
+    orth_err_p: float
+    sv_drift: float = float("nan")
+
+
+class Factors:
+    """Device factor state for one forward: G (param dtype), bf16 copies,
+    Q^2 caches and the packed parameters they were computed from."""
+
+    def __init__(self, layer: "PoetLinearLayer", packed_r: torch.Tensor, packed_p: torch.Tensor):
+        dev, pdt = layer.device, layer.param_dtype
+        b, k = layer.block_size, layer.neumann_k
+        nbr, nbp = layer.m // b, layer.n // b
+        self.packed_r, self.packed_p = packed_r, packed_p
+        self.g_r = torch.empty((nbr, b, b), dtype=pdt, device=dev)
+        self.g_p = torch.empty((nbp, b, b), dtype=pdt, device=dev)
+        low = layer.dtype == torch.bfloat16
+        self.g_r_lowp = torch.empty((nbr, b, b), dtype=torch.bfloat16, device=dev) if low else None
+        self.g_p_lowp = torch.empty((nbp, b, b), dtype=torch.bfloat16, device=dev) if low else None
+        self.q2_r = torch.empty((nbr, b, b), dtype=pdt, device=dev) if k == 3 else None
+        self.q2_p = torch.empty((nbp, b, b), dtype=pdt, device=dev) if k == 3 else None
+        self.struct = N.LayerFactors(
+            packed_r.data_ptr(), packed_p.data_ptr(), self.g_r.data_ptr(), self.g_p.data_ptr(),
+            N.ptr(self.g_r_lowp), N.ptr(self.g_p_lowp), N.ptr(self.q2_r), N.ptr(self.q2_p))
+
+
+class PoetLinearLayer:
+    def __init__(self, base_weight, block_size: int, rng: Rng, *, name: str = "poet",
+                 variant: str = "fast", neumann_k: int = 3, device=None):
+        if isinstance(base_weight, np.ndarray):
+            if base_weight.dtype not in (np.float32, np.float64):
+                raise ShapeError(f"unsupported dtype {base_weight.dtype}")
+            base_weight = torch.from_numpy(np.ascontiguousarray(base_weight))
+        if base_weight.ndim != 2:
+            raise ShapeError(f"base weight must be 2-D, got {tuple(base_weight.shape)}")
+        m, n = base_weight.shape
+        if block_size < 1:
+            raise ConfigError(f"block_size must be >= 1, got {block_size}")
+        if m % block_size or n % block_size:
+            raise ConfigError(
+                f"layer dims ({m}, {n}) must both be divisible by block_size {block_size}")
+        if variant not in VARIANTS:
+            raise ConfigError(f"variant must be one of {VARIANTS}, got {variant!r}")
+        if neumann_k < 1:
+            raise ConfigError(f"neumann_k must be >= 1, got {neumann_k}")
+        if base_weight.dtype not in (torch.float32, torch.float64, torch.bfloat16):
+            raise ShapeError(f"unsupported dtype {base_weight.dtype}")
+        if num_pairs(block_size) == 0:
+            warnings.warn("block_size 1 leaves no trainable rotation parameters", stacklevel=2)
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        self.name = name
+        self.m, self.n = int(m), int(n)
+        self.block_size = int(block_size)
+        self.variant = variant
+        self.neumann_k = int(neumann_k)
+        self.dtype = base_weight.dtype
+        self.param_dtype = param_dtype(self.dtype)
+        self.q_r = SkewParams.zeros(self.m // block_size, block_size, dtype=self.param_dtype, device=self.device)
+        self.q_p = SkewParams.zeros(self.n // block_size, block_size, dtype=self.param_dtype, device=self.device)
+        self.merge_count = 0
+        self.perm_in = sample_permutation(self.m, rng)
+        self.perm_out = sample_permutation(self.n, rng)
+        w = base_weight.to(self.device).contiguous()
+        self.premerged = self._premerge(w, self.perm_in, self.perm_out)
+
+    # -- construction helpers ----------------------------------------------------
+
+    @property
+    def quantized(self) -> bool:
+        return False
+
+    def trainable_param_count(self) -> int:
+        return int(self.q_r.packed.numel() + self.q_p.packed.numel())
+
+    def _stream(self) -> int:
+        return N.stream_ptr(self.device)
+
+    def _premerge(self, w: torch.Tensor, pin: PermutationMap, pout: PermutationMap) -> torch.Tensor:
+        out = torch.empty((self.m, self.n), dtype=self.dtype, device=self.device)
+        rf, _ = pin.device(self.device)
+        cf, _ = pout.device(self.device)
+        N.call("poetx_gather2d", N.dtype_code(self.dtype), self.m, self.n, rf.data_ptr(),
+               cf.data_ptr(), w.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    @property
+    def base(self) -> torch.Tensor:
+        """Frozen weight W recovered from the premerged copy:
+        W[r, c] = PM[pi_in^-1(r), pi_out^-1(c)] (exact)."""
+        _, ri = self.perm_in.device(self.device)
+        _, ci = self.perm_out.device(self.device)
+        out = torch.empty((self.m, self.n), dtype=self.dtype, device=self.device)
+        N.call("poetx_gather2d", N.dtype_code(self.dtype), self.m, self.n, ri.data_ptr(),
+               ci.data_ptr(), self.premerged.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    @base.setter
+    def base(self, w) -> None:
+        if isinstance(w, np.ndarray):
+            w = torch.from_numpy(np.ascontiguousarray(w))
+        if tuple(w.shape) != (self.m, self.n):
+            raise ShapeError(f"base weight shape {tuple(w.shape)}, expected ({self.m}, {self.n})")
+        self.premerged = self._premerge(w.to(self.device, self.dtype).contiguous(), self.perm_in, self.perm_out)
+
+    def set_permutations(self, perm_in: PermutationMap, perm_out: PermutationMap) -> None:
+        """Install explicit permutations keeping W fixed (layer.py:153-159)."""
+        if perm_in.n != self.m or perm_out.n != self.n:
+            raise ShapeError("permutation sizes do not match layer dims")
+        w = self.base
+        self.perm_in, self.perm_out = perm_in, perm_out
+        self.premerged = self._premerge(w, perm_in, perm_out)
+
+    def quantize_base(self) -> None:
+        """int8 base (POET-XQ) -- mem variant only (layer.py:169-177)."""
+        if self.variant != "mem":
+            raise ConfigError("quantized base requires the mem variant")
+        raise ConfigError("int8 premerged base (POET-XQ) is not built in this round")
+
+    # -- descriptor ----------------------------------------------------------------
+
+    def _desc(self) -> N.LayerDesc:
+        fi, ii = self.perm_in.device(self.device)
+        fo, io = self.perm_out.device(self.device)
+        d = N.LayerDesc()
+        d.dtype = N.dtype_code(self.dtype)
+        d.variant = N.FAST if self.variant == "fast" else N.MEM
+        d.neumann_k = self.neumann_k
+        d.m, d.n, d.b = self.m, self.n, self.block_size
+        d.perm_in_fwd, d.perm_in_inv = fi.data_ptr(), ii.data_ptr()
+        d.perm_out_fwd, d.perm_out_inv = fo.data_ptr(), io.data_ptr()
+        d.premerged = self.premerged.data_ptr()
+        return d
+
+    def compute_factors(self, packed_r=None, packed_p=None) -> Factors:
+        f = Factors(self, self.q_r.packed if packed_r is None else packed_r,
+                    self.q_p.packed if packed_p is None else packed_p)
+        d = self._desc()
+        ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(
+            N.dtype_code(self.param_dtype), max(self.m, self.n) // self.block_size,
+            self.block_size, self.neumann_k), self.device)
+        N.call("poetx_layer_factors", d, f.struct, ws, wsb, self._stream())
+        return f
+
+    # -- forward / backward ----------------------------------------------------------
+
+    def _input(self, x, what):
+        was_np = isinstance(x, np.ndarray)
+        if was_np:
+            if _NP_TO_TORCH.get(x.dtype) != self.dtype:
+                raise ShapeError(f"{what} dtype {x.dtype} does not match layer dtype {self.dtype}")
+            x = torch.from_numpy(np.ascontiguousarray(x)).to(self.device)
+        elif x.dtype != self.dtype:
+            raise ShapeError(f"{what} dtype {x.dtype} does not match layer dtype {self.dtype}")
+        if not x.is_cuda:
+            x = x.to(self.device)
+        return x.contiguous(), was_np
+
+    def forward(self, x, ledger=None):
+        if x.ndim != 2 or x.shape[1] != self.m:
+            raise ShapeError(f"input shape {tuple(x.shape)} does not match layer ({self.m}, {self.n})")
+        x, was_np = self._input(x, "input")
+        T = x.shape[0]
+        # snapshot the parameters so backward differentiates this forward's factors
+        f = self.compute_factors(self.q_r.packed.clone(), self.q_p.packed.clone())
+        z = torch.empty((T, self.n), dtype=self.dtype, device=self.device)
+        saved = torch.empty((T, self.n), dtype=self.dtype, device=self.device) if self.variant == "fast" else None
+        d = self._desc()
+        ws, wsb = N.workspace(N.lib().poetx_layer_workspace_bytes(d, T), self.device)
+        N.call("poetx_layer_forward", d, f.struct, T, x.data_ptr(), z.data_ptr(), N.ptr(saved), ws, wsb,
+               self._stream())
+        if saved is not None and ledger is not None:
+            ledger.save_activation(self.name, saved.numel() * saved.element_size())
+        cache = LayerCache(x=x, g_r=f.g_r, g_p=f.g_p, factors=f, saved_mm2=saved, was_numpy=was_np)
+        return (z.cpu().numpy() if was_np else z), cache
+
+    def backward(self, cache: LayerCache, dz) -> LayerGrads:
+        if cache.consumed:
+            raise StateError("layer cache already consumed by a previous backward")
+        if tuple(dz.shape) != (cache.x.shape[0], self.n):
+            raise ShapeError(f"cotangent shape {tuple(dz.shape)} does not match output")
+        dz, _ = self._input(dz, "cotangent")
+        cache.consumed = True
+        T = cache.x.shape[0]
+        dx = torch.empty((T, self.m), dtype=self.dtype, device=self.device)
+        gr = torch.empty_like(self.q_r.packed)
+        gp = torch.empty_like(self.q_p.packed)
+        d = self._desc()
+        ws, wsb = N.workspace(N.lib().poetx_layer_workspace_bytes(d, T), self.device)
+        N.call("poetx_layer_backward", d, cache.factors.struct, T, cache.x.data_ptr(), dz.data_ptr(),
+               N.ptr(cache.saved_mm2), dx.data_ptr(), gr.data_ptr(), gp.data_ptr(), 0, ws, wsb,
+               self._stream())
+        if cache.was_numpy:
+            return LayerGrads(q_r=gr.cpu().numpy(), q_p=gp.cpu().numpy(), x=dx.cpu().numpy())
+        return LayerGrads(q_r=gr, q_p=gp, x=dx)
+
+    # -- merge -------------------------------------------------------------------------
+
+    def _merge_factors(self, use_exact_cayley: bool):
+        f = self.compute_factors()
+        if not use_exact_cayley:
+            return f.g_r, f.g_p
+        from .cnp import skew_from_packed
+        return cayley_exact(skew_from_packed(self.q_r)), cayley_exact(skew_from_packed(self.q_p))
+
+    def _merge_call(self, g_r, g_p, new_in=None, new_out=None, want_w=False):
+        d = self._desc()
+        ws, wsb = N.workspace(N.lib().poetx_merge_workspace_bytes(d), self.device)
+        pm_new = w = None
+        ni = no = None
+        if new_in is not None:
+            pm_new = torch.empty_like(self.premerged)
+            ni = new_in.device(self.device)[0]
+            no = new_out.device(self.device)[0]
+        if want_w:
+            w = torch.empty_like(self.premerged)
+        N.call("poetx_layer_merge", d, g_r.contiguous().data_ptr(), g_p.contiguous().data_ptr(),
+               N.ptr(ni), N.ptr(no), N.ptr(pm_new), N.ptr(w), ws, wsb, self._stream())
+        return pm_new, w
+
+    def _transformed_base(self, use_exact_cayley: bool) -> torch.Tensor:
+        """Psi_m^T (G_R PM G_P) Psi_n (layer.py:260-273)."""
+        g_r, g_p = self._merge_factors(use_exact_cayley)
+        return self._merge_call(g_r, g_p, want_w=True)[1]
+
+    def materialize_weight(self):
+        """Dense effective weight R W P (layer.py:275-277)."""
+        return self._transformed_base(use_exact_cayley=False)
+
+    def merge_and_reinit(self, rng: Rng, *, use_exact_cayley: bool = False,
+                         compute_sv_drift: bool = False) -> MergeAudit:
+        """Fold the factors into the frozen weight, zero the packed parameters in
+        place, resample both permutations, rebuild PM (layer.py:279-314)."""
+        g_r, g_p = self._merge_factors(use_exact_cayley)
+        err_r = orthogonality_error(g_r)
+        err_p = orthogonality_error(g_p)
+        new_in = sample_permutation(self.m, rng)
+        new_out = sample_permutation(self.n, rng)
+        drift = float("nan")
+        old_base = self.base if compute_sv_drift else None
+        pm_new, w_new = self._merge_call(g_r, g_p, new_in, new_out, want_w=compute_sv_drift)
+        if compute_sv_drift:
+            sv_old = torch.linalg.svdvals(old_base.double())
+            sv_new = torch.linalg.svdvals(w_new.double())
+            denom = torch.clamp(sv_old, min=np.finfo(np.float64).tiny)
+            drift = float(torch.max(torch.abs(sv_new - sv_old) / denom))
+        self.premerged = pm_new
+        self.q_r.packed.zero_()
+        self.q_p.packed.zero_()
+        self.perm_in, self.perm_out = new_in, new_out
+        self.merge_count += 1
+        return MergeAudit(self.merge_count, float(err_r), float(err_p), drift)
+
+
+def init_layer(m: int, n: int, block_size: int, rng: Rng, *, name: str = "poet",
+               variant: str = "fast", neumann_k: int = 3, dtype=np.float32,
+               weight_std: float | None = None, base_weight=None, device=None) -> PoetLinearLayer:
+    """Layer with a Gaussian (or given) frozen base weight (layer.py:317-344).
+    Draw order off ``rng``: weight, then pi_in, then pi_out."""
+    tdt = _torch_dtype(dtype) if not (isinstance(dtype, torch.dtype)) else dtype
+    if base_weight is None:
+        std = (1.0 / np.sqrt(m)) if weight_std is None else float(weight_std)
+        draw = rng.normal((m, n)) * std
+        if tdt == torch.bfloat16:
+            base_weight = torch.from_numpy(draw.astype(np.float32)).to(torch.bfloat16)
+        else:
+            base_weight = torch.from_numpy(draw.astype(np.float32 if tdt == torch.float32 else np.float64))
+    else:
+        if tuple(base_weight.shape) != (m, n):
+            raise ShapeError(f"base weight shape {tuple(base_weight.shape)}, expected ({m}, {n})")
+        if isinstance(base_weight, np.ndarray):
+            base_weight = torch.from_numpy(np.ascontiguousarray(base_weight))
+        base_weight = base_weight.to(tdt)
+    return PoetLinearLayer(base_weight, block_size, rng, name=name, variant=variant,
+                           neumann_k=neumann_k, device=device)
