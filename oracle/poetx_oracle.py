@@ -485,3 +485,24 @@ def philox_permutation_py(gen: PhiloxPy, n):
         j = gen.interval(i)
         arr[i], arr[j] = arr[j], arr[i]
     return np.array(arr, dtype=np.int32)
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs[0] inputs (tests/golden/make_golden.py draws them through the reference)
+# ---------------------------------------------------------------------------
+
+
+def cfg1_inputs(seed=2603, m=512, n=512, b=64, T=1024, dt=np.float32, scale=0.01):
+    """Regenerate BASELINE configs[0] inputs exactly as make_golden.py drew them
+    through the reference (init_layer draw order: W, then pi_in, then pi_out)."""
+    r = numpy_rng(seed, keyed_stream("layer"))
+    base = (r.standard_normal((m, n)) * (1.0 / np.sqrt(m))).astype(dt)
+    fwd_in = r.permutation(m).astype(np.int32)
+    fwd_out = r.permutation(n).astype(np.int32)
+    p = numpy_rng(seed, keyed_stream("packed"))
+    q_r = (scale * p.standard_normal((m // b, b * (b - 1) // 2))).astype(dt)
+    q_p = (scale * p.standard_normal((n // b, b * (b - 1) // 2))).astype(dt)
+    dd = numpy_rng(seed, keyed_stream("data"))
+    x = dd.standard_normal((T, m)).astype(dt)
+    dz = dd.standard_normal((T, n)).astype(dt)
+    return base, fwd_in, fwd_out, q_r, q_p, x, dz

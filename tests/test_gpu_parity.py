@@ -214,9 +214,7 @@ def test_layer_golden(P, tag, variant):
 
 def test_cfg1_layer_vs_oracle(P):
     """BASELINE configs[0]: 512x512, b=64, k=3, fp32, 1024 tokens."""
-    from tests.test_oracle_golden import cfg1_inputs
-
-    base, fi, fo, q_r, q_p, x, dz = cfg1_inputs()
+    base, fi, fo, q_r, q_p, x, dz = O.cfg1_inputs()
     ref = O.OracleLayer(base, 64, fi, fo)
     ref.q_r[...] = q_r
     ref.q_p[...] = q_p

@@ -103,20 +103,7 @@ def test_layer_bitwise(tag, variant):
     assert np.array_equal(z2, d[f"{tag}/z_after_merge"])
 
 
-def cfg1_inputs(seed=2603, m=512, n=512, b=64, T=1024, dt=np.float32, scale=0.01):
-    """Regenerate BASELINE configs[0] inputs exactly as make_golden.py drew them
-    through the reference (init_layer draw order: W, then pi_in, then pi_out)."""
-    r = keyed(seed, "layer")
-    base = (r.standard_normal((m, n)) * (1.0 / np.sqrt(m))).astype(dt)
-    fwd_in = r.permutation(m).astype(np.int32)
-    fwd_out = r.permutation(n).astype(np.int32)
-    p = keyed(seed, "packed")
-    q_r = (scale * p.standard_normal((m // b, b * (b - 1) // 2))).astype(dt)
-    q_p = (scale * p.standard_normal((n // b, b * (b - 1) // 2))).astype(dt)
-    dd = keyed(seed, "data")
-    x = dd.standard_normal((T, m)).astype(dt)
-    dz = dd.standard_normal((T, n)).astype(dt)
-    return base, fwd_in, fwd_out, q_r, q_p, x, dz
+cfg1_inputs = O.cfg1_inputs
 
 
 def test_cfg1_checksums():
