@@ -53,6 +53,12 @@ uint64_t poetx_launch_count(void);
 /* 1 if the tcgen05/TMA GEMM path is compiled in and enabled */
 int poetx_tc_enabled(void);
 void poetx_set_tc_enabled(int on);
+/* device timing hooks: while enabled, tensor-core kernel launches are
+ * bracketed by CUDA events on their stream; query sums durations (ms),
+ * launch count and algorithmic FLOPs per kernel name ("tc_gemm", ...). */
+void poetx_prof_enable(int on);
+void poetx_prof_reset(void);
+int poetx_prof_query(const char* name, double* total_ms, int64_t* count, double* flops);
 
 /* ---------------------------------------------------------------- H1 RNG --
  * numpy Generator(Philox) state (the reference draws permutations through

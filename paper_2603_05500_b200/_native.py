@@ -74,6 +74,10 @@ _SIGS = {
     "poetx_launch_count": (C.c_uint64, []),
     "poetx_tc_enabled": (I32, []),
     "poetx_set_tc_enabled": (None, [I32]),
+    "poetx_prof_enable": (None, [I32]),
+    "poetx_prof_reset": (None, []),
+    "poetx_prof_query": (I32, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
+                               C.POINTER(C.c_double)]),
     "poetx_philox_seed": (I32, [C.POINTER(PhiloxState), C.c_uint64, C.c_uint64]),
     "poetx_philox_permutation": (I32, [C.POINTER(PhiloxState), I64, VP, VP]),
     "poetx_skew_from_packed": (I32, [I32, I64, I64, VP, VP, VP]),

@@ -1,0 +1,102 @@
+// Per-kernel device timing hooks: when enabled, selected launches are
+// bracketed by CUDA events recorded on the launching stream, so bench.py
+// can report a kernel's average device duration inside a real step.
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace poetx {
+
+struct ProfRec {
+  cudaEvent_t start, stop;
+  double flops;
+};
+struct ProfState {
+  std::mutex mu;
+  bool on = false;
+  std::unordered_map<std::string, std::vector<ProfRec>> recs;
+  std::vector<cudaEvent_t> pool;
+};
+static ProfState& prof() {
+  static ProfState s;
+  return s;
+}
+bool prof_on() { return prof().on; }
+
+static cudaEvent_t take_event() {
+  auto& s = prof();
+  if (!s.pool.empty()) {
+    cudaEvent_t e = s.pool.back();
+    s.pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// returns an opaque token; call prof_end after the launch
+void* prof_begin(cudaStream_t st) {
+  auto& s = prof();
+  std::lock_guard<std::mutex> g(s.mu);
+  if (!s.on) return nullptr;
+  cudaEvent_t e = take_event();
+  cudaEventRecord(e, st);
+  return reinterpret_cast<void*>(e);
+}
+void prof_end(void* token, const char* name, double flops, cudaStream_t st) {
+  if (!token) return;
+  auto& s = prof();
+  std::lock_guard<std::mutex> g(s.mu);
+  cudaEvent_t e = take_event();
+  cudaEventRecord(e, st);
+  s.recs[name].push_back({reinterpret_cast<cudaEvent_t>(token), e, flops});
+}
+
+}  // namespace poetx
+
+using namespace poetx;
+
+extern "C" {
+void poetx_prof_enable(int on) {
+  std::lock_guard<std::mutex> g(prof().mu);
+  prof().on = on != 0;
+}
+void poetx_prof_reset(void) {
+  auto& s = prof();
+  std::lock_guard<std::mutex> g(s.mu);
+  for (auto& kv : s.recs)
+    for (auto& r : kv.second) {
+      s.pool.push_back(r.start);
+      s.pool.push_back(r.stop);
+    }
+  s.recs.clear();
+}
+int poetx_prof_query(const char* name, double* total_ms, int64_t* count, double* flops) {
+  auto& s = prof();
+  std::lock_guard<std::mutex> g(s.mu);
+  double ms = 0, fl = 0;
+  int64_t n = 0;
+  auto it = s.recs.find(name ? name : "");
+  if (it != s.recs.end()) {
+    for (auto& r : it->second) {
+      if (cudaEventSynchronize(r.stop) != cudaSuccess) {
+        set_error("prof_query: event sync failed");
+        return POETX_ECUDA;
+      }
+      float e = 0;
+      cudaEventElapsedTime(&e, r.start, r.stop);
+      ms += e;
+      fl += r.flops;
+      ++n;
+    }
+  }
+  if (total_ms) *total_ms = ms;
+  if (count) *count = n;
+  if (flops) *flops = fl;
+  return POETX_OK;
+}
+}

@@ -27,6 +27,9 @@
 
 namespace poetx {
 
+void* prof_begin(cudaStream_t st);
+void prof_end(void* token, const char* name, double flops, cudaStream_t st);
+
 static int g_tc_on = 1;
 bool tc_enabled() { return g_tc_on != 0; }
 
@@ -347,7 +350,9 @@ int launch(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cuda
   }
   int tiles = a.m_tiles * a.n_tiles;
   int grid = tiles < num_sms() ? tiles : num_sms();
+  void* tok = prof_begin(st);
   tc_gemm_kernel<MN><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, a);
+  prof_end(tok, "tc_gemm", 2.0 * a.M * a.N * a.K, st);
   POETX_LAUNCHED("tc_gemm");
   return POETX_OK;
 }

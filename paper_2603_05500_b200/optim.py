@@ -219,12 +219,12 @@ def adamw_step(params: dict, grads: dict, state: AdamWState, lr: float, sched: S
     _adamw_launch(ps, gs, ms, vs, lr, sched, state.t)
 
 
-def fused_clip_adamw(groups, threshold: float, sched: ScheduleConfig, t: int):
+def fused_clip_adamw(groups, threshold: float, sched: ScheduleConfig):
     """Trainer path: one device norm over every group's grads, then per group
-    (params, grads, m, v, lr) the clip-scaled AdamW update -- no host sync.
+    (params, grads, m, v, lr, t) the clip-scaled AdamW update -- no host sync.
     Returns (sqnorm tensor, nonfinite tensor) for lazy inspection."""
     allg = [g for grp in groups for g in grp[1]]
     sq, bad = device_sqnorm(allg)
-    for ps, gs, ms, vs, lr in groups:
+    for ps, gs, ms, vs, lr, t in groups:
         _adamw_launch(ps, gs, ms, vs, lr, sched, t, sqnorm=sq, threshold=threshold, write_back=0)
     return sq, bad

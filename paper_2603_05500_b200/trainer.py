@@ -1,0 +1,382 @@
+"""GPU-resident POET-X training step around the hot path:
+a Llama decoder whose seven projections per block are POET-X layers, the
+reference trainer's step logic (runner.py:279-327: clip threshold ramp,
+global clip, AdamW on POET and dense groups with the POET lr scale,
+merge-then-reinitialize every ``merge_gap`` steps with moment reset) and
+token-batch data parallelism over NCCL.
+
+This is the *caller* of the path, used by bench.py; the reference has no
+Llama (its models are toy MLPs, models.py), so model shapes follow the
+paper.  Attention, RMSNorm, embedding, lm_head
+and the loss are plain PyTorch (cuDNN/flash SDPA); every POET-X operation
+is a libpoetx_b200 kernel.
+
+Memory layout (B200-first): all packed skew parameters of the model live
+in ONE flat fp32 buffer (and their grads, AdamW m and v in three more), so
+the global norm, the fused clip+AdamW update and the data-parallel
+all-reduce are one launch each over contiguous HBM.  Dense trainables
+(embedding, lm_head, RMSNorm gains) share a second flat fp32 group.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.nn.functional as F
+
+from . import _native as N
+from .cnp import num_pairs
+from .optim import ScheduleConfig, clip_threshold_at, fused_clip_adamw, lr_at
+from .permute import PermutationMap, sample_permutation
+from .rng import Rng
+
+
+@dataclass
+class LlamaConfig:
+    name: str
+    d: int
+    f: int
+    layers: int
+    heads: int
+    block: int
+    vocab: int = 32000
+    seq: int = 256
+    variant: str = "fast"
+    neumann_k: int = 3
+
+    @property
+    def head_dim(self) -> int:
+        return self.d // self.heads
+
+
+# FFN widths are the LLaMA multiple_of rounding of 8d/3 made
+# divisible by b; these reproduce the paper's Llama-3B parameter counts.
+CONFIGS = {
+    "llama-60m": dict(d=512, f=1408, layers=8, heads=8, block=64),
+    "llama-350m": dict(d=1024, f=2816, layers=24, heads=16, block=256),
+    "llama-1b": dict(d=2048, f=5632, layers=24, heads=32, block=256),
+    "llama-8b": dict(d=4096, f=14336, layers=32, heads=32, block=256, seq=1024),
+}
+
+
+def llama_config(name: str, **over) -> LlamaConfig:
+    kw = dict(CONFIGS[name])
+    kw.update(over)
+    return LlamaConfig(name=name, **kw)
+
+
+# --------------------------------------------------------------------------
+# flat parameter groups
+# --------------------------------------------------------------------------
+
+
+class FlatGroup:
+    """Contiguous fp32 param / grad / m / v buffers with named views."""
+
+    def __init__(self, sizes: dict, device):
+        self.offsets = {}
+        off = 0
+        for name, n in sizes.items():
+            self.offsets[name] = (off, n)
+            off += n
+        self.numel = off
+        self.param = torch.zeros(off, dtype=torch.float32, device=device)
+        self.grad = torch.zeros(off, dtype=torch.float32, device=device)
+        self.m = torch.zeros(off, dtype=torch.float32, device=device)
+        self.v = torch.zeros(off, dtype=torch.float32, device=device)
+        self.t = 0
+
+    def view(self, buf: torch.Tensor, name: str, shape) -> torch.Tensor:
+        off, n = self.offsets[name]
+        return buf[off:off + n].view(*shape)
+
+    def reset_moments(self):
+        self.m.zero_()
+        self.v.zero_()
+        self.t = 0
+
+
+# --------------------------------------------------------------------------
+# POET-X linear as an autograd op
+# --------------------------------------------------------------------------
+
+
+class _PoetFn(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, x, mod):
+        T = x.shape[0]
+        f = mod.factors()
+        z = torch.empty((T, mod.n), dtype=torch.bfloat16, device=x.device)
+        saved = torch.empty((T, mod.n), dtype=torch.bfloat16, device=x.device) if mod.variant == "fast" else None
+        d = mod.desc
+        ws, wsb = N.workspace(mod.ws_bytes(T), x.device)
+        N.call("poetx_layer_forward", d, f, T, x.data_ptr(), z.data_ptr(), N.ptr(saved), ws, wsb,
+               N.stream_ptr(x.device))
+        ctx.mod = mod
+        ctx.save_for_backward(x, saved) if saved is not None else ctx.save_for_backward(x)
+        return z
+
+    @staticmethod
+    def backward(ctx, dz):
+        mod = ctx.mod
+        saved = ctx.saved_tensors
+        x = saved[0]
+        t = saved[1] if len(saved) > 1 else None
+        dz = dz.contiguous()
+        T = x.shape[0]
+        dx = torch.empty_like(x)
+        ws, wsb = N.workspace(mod.ws_bytes(T), x.device)
+        N.call("poetx_layer_backward", mod.desc, mod.factors(), T, x.data_ptr(), dz.data_ptr(),
+               N.ptr(t), dx.data_ptr(), mod.grad_r.data_ptr(), mod.grad_p.data_ptr(), 1, ws, wsb,
+               N.stream_ptr(x.device))
+        return dx, None
+
+
+class PoetLinear(torch.nn.Module):
+    """m -> n POET-X projection with bf16 frozen premerged weight and fp32
+    packed parameters living in a FlatGroup."""
+
+    def __init__(self, name, m, n, b, group: FlatGroup, rng: Rng, *, variant="fast", neumann_k=3,
+                 std=None, device="cuda"):
+        super().__init__()
+        self.name, self.m, self.n, self.b = name, m, n, b
+        self.variant, self.k = variant, neumann_k
+        self.device = torch.device(device)
+        nbr, nbp, pairs = m // b, n // b, num_pairs(b)
+        self.packed_r = group.view(group.param, name + ".r", (nbr, pairs))
+        self.packed_p = group.view(group.param, name + ".p", (nbp, pairs))
+        self.grad_r = group.view(group.grad, name + ".r", (nbr, pairs))
+        self.grad_p = group.view(group.grad, name + ".p", (nbp, pairs))
+        # draw order as init_layer (layer.py:335-340): W, then pi_in, then pi_out.
+        # Synthetic-weight runs draw W on the device (seeded) instead of host numpy.
+        std = (1.0 / math.sqrt(m)) if std is None else std
+        gen = torch.Generator(device=self.device).manual_seed(int(rng.integers(0, 2**62)))
+        w = (torch.randn((m, n), generator=gen, device=self.device, dtype=torch.float32) * std).to(torch.bfloat16)
+        self.perm_in = sample_permutation(m, rng)
+        self.perm_out = sample_permutation(n, rng)
+        self.premerged = torch.empty((m, n), dtype=torch.bfloat16, device=self.device)
+        self._install(w)
+        self.g_r = torch.empty((nbr, b, b), dtype=torch.float32, device=self.device)
+        self.g_p = torch.empty((nbp, b, b), dtype=torch.float32, device=self.device)
+        self.g_r16 = torch.empty((nbr, b, b), dtype=torch.bfloat16, device=self.device)
+        self.g_p16 = torch.empty((nbp, b, b), dtype=torch.bfloat16, device=self.device)
+        self.q2_r = torch.empty((nbr, b, b), dtype=torch.float32, device=self.device) if neumann_k == 3 else None
+        self.q2_p = torch.empty((nbp, b, b), dtype=torch.float32, device=self.device) if neumann_k == 3 else None
+        self._factors = N.LayerFactors(
+            self.packed_r.data_ptr(), self.packed_p.data_ptr(), self.g_r.data_ptr(), self.g_p.data_ptr(),
+            self.g_r16.data_ptr(), self.g_p16.data_ptr(), N.ptr(self.q2_r), N.ptr(self.q2_p))
+        self._fresh = False
+        self.merge_count = 0
+
+    def _install(self, w: torch.Tensor):
+        rf, _ = self.perm_in.device(self.device)
+        cf, _ = self.perm_out.device(self.device)
+        N.call("poetx_gather2d", N.BF16, self.m, self.n, rf.data_ptr(), cf.data_ptr(), w.data_ptr(),
+               self.premerged.data_ptr(), N.stream_ptr(self.device))
+        self._set_desc()
+
+    def _set_desc(self):
+        fi, ii = self.perm_in.device(self.device)
+        fo, io = self.perm_out.device(self.device)
+        d = N.LayerDesc()
+        d.dtype, d.variant, d.neumann_k = N.BF16, (N.FAST if self.variant == "fast" else N.MEM), self.k
+        d.m, d.n, d.b = self.m, self.n, self.b
+        d.perm_in_fwd, d.perm_in_inv = fi.data_ptr(), ii.data_ptr()
+        d.perm_out_fwd, d.perm_out_inv = fo.data_ptr(), io.data_ptr()
+        d.premerged = self.premerged.data_ptr()
+        self.desc = d
+
+    def ws_bytes(self, T: int) -> int:
+        return int(N.lib().poetx_layer_workspace_bytes(self.desc, T))
+
+    def invalidate(self):
+        self._fresh = False
+
+    def factors(self) -> N.LayerFactors:
+        """CNP of the current packed parameters, computed once per step."""
+        if not self._fresh:
+            ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(N.F32, max(self.m, self.n) // self.b,
+                                                                    self.b, self.k), self.device)
+            N.call("poetx_layer_factors", self.desc, self._factors, ws, wsb, N.stream_ptr(self.device))
+            self._fresh = True
+        return self._factors
+
+    def forward(self, x):
+        shp = x.shape
+        z = _PoetFn.apply(x.reshape(-1, self.m).contiguous(), self)
+        return z.view(*shp[:-1], self.n)
+
+    def merge_and_reinit(self, rng: Rng):
+        """layer.py:279-314 on the device: fold, resample perms, zero packed."""
+        self.factors()
+        new_in = sample_permutation(self.m, rng)
+        new_out = sample_permutation(self.n, rng)
+        ws, wsb = N.workspace(N.lib().poetx_merge_workspace_bytes(self.desc), self.device)
+        pm_new = torch.empty_like(self.premerged)
+        N.call("poetx_layer_merge", self.desc, self.g_r.data_ptr(), self.g_p.data_ptr(),
+               new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
+               pm_new.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
+        self.premerged.copy_(pm_new)
+        self.perm_in, self.perm_out = new_in, new_out
+        self.packed_r.zero_()
+        self.packed_p.zero_()
+        self._set_desc()
+        self._fresh = False
+        self.merge_count += 1
+
+
+# --------------------------------------------------------------------------
+# Llama
+# --------------------------------------------------------------------------
+
+
+def _rope(x, cos, sin):
+    x1, x2 = x[..., : x.shape[-1] // 2], x[..., x.shape[-1] // 2:]
+    return torch.cat((x1 * cos - x2 * sin, x2 * cos + x1 * sin), dim=-1)
+
+
+class PoetLlama(torch.nn.Module):
+    PROJ = ("q", "k", "v", "o", "gate", "up", "down")
+
+    def __init__(self, cfg: LlamaConfig, seed: int = 0, device="cuda"):
+        super().__init__()
+        self.cfg = cfg
+        dev = torch.device(device)
+        d, f, b = cfg.d, cfg.f, cfg.block
+        shapes = {"q": (d, d), "k": (d, d), "v": (d, d), "o": (d, d), "gate": (d, f), "up": (d, f), "down": (f, d)}
+        sizes = {}
+        for i in range(cfg.layers):
+            for p in self.PROJ:
+                m, n = shapes[p]
+                sizes[f"{i}.{p}.r"] = (m // b) * num_pairs(b)
+                sizes[f"{i}.{p}.p"] = (n // b) * num_pairs(b)
+        self.poet = FlatGroup(sizes, dev)
+        dense_sizes = {"embed": cfg.vocab * d, "head": cfg.vocab * d, "norm_f": d}
+        for i in range(cfg.layers):
+            dense_sizes[f"{i}.norm1"] = d
+            dense_sizes[f"{i}.norm2"] = d
+        self.dense = FlatGroup(dense_sizes, dev)
+        g = torch.Generator(device=dev).manual_seed(seed)
+        self.dense.view(self.dense.param, "embed", (cfg.vocab, d)).normal_(0, 1.0 / math.sqrt(d), generator=g)
+        self.dense.view(self.dense.param, "head", (cfg.vocab, d)).normal_(0, 1.0 / math.sqrt(d), generator=g)
+        for name in dense_sizes:
+            if "norm" in name:
+                self.dense.view(self.dense.param, name, (d,)).fill_(1.0)
+        self.layers = []
+        for i in range(cfg.layers):
+            mods = {}
+            for p in self.PROJ:
+                m, n = shapes[p]
+                mods[p] = PoetLinear(f"{i}.{p}", m, n, b, self.poet, Rng.keyed(seed, "init", i, p),
+                                     variant=cfg.variant, neumann_k=cfg.neumann_k, device=dev)
+            self.layers.append(mods)
+        hd = cfg.head_dim
+        inv = 1.0 / (10000 ** (torch.arange(0, hd, 2, device=dev, dtype=torch.float32) / hd))
+        ang = torch.outer(torch.arange(cfg.seq, device=dev, dtype=torch.float32), inv)
+        self.cos = ang.cos().to(torch.bfloat16)
+        self.sin = ang.sin().to(torch.bfloat16)
+
+    def poet_layers(self):
+        return [mods[p] for mods in self.layers for p in self.PROJ]
+
+    def dense_param(self, name, shape):
+        return self.dense.view(self.dense.param, name, shape)
+
+    def forward(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        cfg = self.cfg
+        B, S = tokens.shape
+        d, H, hd = cfg.d, cfg.heads, cfg.head_dim
+        embed = self.dense_param("embed", (cfg.vocab, d)).detach().requires_grad_(True)
+        h = F.embedding(tokens.reshape(-1), embed).to(torch.bfloat16)
+        cos, sin = self.cos[:S].view(1, S, 1, hd // 2), self.sin[:S].view(1, S, 1, hd // 2)
+        leaves = [embed]
+        for i, mods in enumerate(self.layers):
+            n1 = self.dense_param(f"{i}.norm1", (d,)).detach().requires_grad_(True)
+            n2 = self.dense_param(f"{i}.norm2", (d,)).detach().requires_grad_(True)
+            leaves += [n1, n2]
+            x = F.rms_norm(h, (d,), n1.to(torch.bfloat16), 1e-6)
+            q = mods["q"](x).view(B, S, H, hd)
+            k = mods["k"](x).view(B, S, H, hd)
+            v = mods["v"](x).view(B, S, H, hd)
+            q, k = _rope(q, cos, sin), _rope(k, cos, sin)
+            a = F.scaled_dot_product_attention(q.transpose(1, 2), k.transpose(1, 2), v.transpose(1, 2),
+                                               is_causal=True)
+            h = h + mods["o"](a.transpose(1, 2).reshape(B * S, d))
+            x = F.rms_norm(h, (d,), n2.to(torch.bfloat16), 1e-6)
+            h = h + mods["down"](F.silu(mods["gate"](x)) * mods["up"](x))
+        nf = self.dense_param("norm_f", (d,)).detach().requires_grad_(True)
+        head = self.dense_param("head", (cfg.vocab, d)).detach().requires_grad_(True)
+        leaves += [nf, head]
+        h = F.rms_norm(h, (d,), nf.to(torch.bfloat16), 1e-6)
+        logits = F.linear(h, head.to(torch.bfloat16))
+        loss = F.cross_entropy(logits.float(), targets.reshape(-1))
+        self._leaves = leaves
+        return loss
+
+    def backward_dense_grads(self, loss):
+        """Backprop; dense grads land in the flat dense grad buffer."""
+        names = ["embed"] + [f"{i}.norm{j}" for i in range(self.cfg.layers) for j in (1, 2)] + ["norm_f", "head"]
+        grads = torch.autograd.grad(loss, self._leaves)
+        for name, g in zip(names, grads):
+            self.dense.view(self.dense.grad, name, g.shape).add_(g)
+
+
+class Trainer:
+    """One training step = forward, backward, (all-reduce), clip+AdamW, merge."""
+
+    def __init__(self, cfg: LlamaConfig, micro_batch: int, seed: int = 0, merge_gap: int = 400,
+                 total_steps: int = 10_000, base_lr: float = 1e-3, device="cuda", pg=None):
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.model = PoetLlama(cfg, seed=seed, device=self.device)
+        self.micro_batch = micro_batch
+        self.seed = seed
+        self.merge_gap = merge_gap
+        self.sched = ScheduleConfig(base_lr=base_lr, total_steps=total_steps, warmup_steps=0)
+        self.step_idx = 0
+        self.since_merge = None
+        self.pg = pg
+        self.last_sq = None
+        self.last_bad = None
+
+    def tokens_per_step(self) -> int:
+        return self.micro_batch * self.cfg.seq
+
+    def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        model = self.model
+        model.poet.grad.zero_()
+        model.dense.grad.zero_()
+        for lay in model.poet_layers():
+            lay.invalidate()
+        loss = model(tokens, targets)
+        model.backward_dense_grads(loss)
+        if self.pg is not None:
+            import torch.distributed as dist
+
+            dist.all_reduce(model.poet.grad, op=dist.ReduceOp.AVG, group=self.pg)
+            dist.all_reduce(model.dense.grad, op=dist.ReduceOp.AVG, group=self.pg)
+        s = self.sched
+        thr = clip_threshold_at(self.step_idx, self.since_merge, s)
+        model.poet.t += 1
+        model.dense.t += 1
+        self.last_sq, self.last_bad = fused_clip_adamw(
+            [([model.poet.param], [model.poet.grad], [model.poet.m], [model.poet.v],
+              lr_at(self.step_idx, s, poet=True), model.poet.t),
+             ([model.dense.param], [model.dense.grad], [model.dense.m], [model.dense.v],
+              lr_at(self.step_idx, s), model.dense.t)],
+            thr, s)
+        self.step_idx += 1
+        if self.since_merge is not None:
+            self.since_merge += 1
+        if self.merge_gap and self.step_idx % self.merge_gap == 0:
+            self.merge()
+        return loss.detach()
+
+    def merge(self):
+        for idx, lay in enumerate(self.model.poet_layers()):
+            lay.merge_and_reinit(Rng.keyed(self.seed, "merge", self.step_idx, idx))
+        self.model.poet.reset_moments()
+        self.since_merge = 0

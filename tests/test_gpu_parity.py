@@ -384,5 +384,5 @@ def test_fused_clip_adamw_matches_two_step(P):
     P.adamw_step({"w": pa}, {"w": ga}, st, 0.01, s)
     pb, gb = dev(p0), dev(g0)
     mb, vb = torch.zeros_like(pb), torch.zeros_like(pb)
-    P.fused_clip_adamw([([pb], [gb], [mb], [vb], 0.01)], 0.5, s, 1)
+    P.fused_clip_adamw([([pb], [gb], [mb], [vb], 0.01, 1)], 0.5, s)
     assert torch.equal(pa, pb)

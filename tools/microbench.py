@@ -1,0 +1,83 @@
+"""Kernel microbenchmarks on one GPU (CUDA-event timing, warm L2 noted).
+
+    python tools/microbench.py [gemm|layer|all]
+"""
+import os
+import sys
+import time
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch
+
+from paper_2603_05500_b200 import _native as N
+
+
+def timeit(fn, iters=20, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    s.record()
+    for _ in range(iters):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / iters
+
+
+def gemm():
+    print("== tcgen05 GEMM vs cuBLAS (bf16) ==")
+    for M, Nn, K in [(8192, 2048, 2048), (8192, 5632, 2048), (8192, 2048, 5632), (16384, 4096, 4096)]:
+        for tb in (0, 1):
+            a = torch.randn((M, K), device="cuda").bfloat16()
+            b = torch.randn((Nn, K) if tb else (K, Nn), device="cuda").bfloat16()
+            c = torch.empty((M, Nn), device="cuda", dtype=torch.bfloat16)
+
+            def ours():
+                N.call("poetx_matmul", N.BF16, M, Nn, K, a.data_ptr(), K, 0, b.data_ptr(), b.shape[1], tb,
+                       c.data_ptr(), Nn, 0, N.stream_ptr())
+            ms = timeit(ours)
+            bt = b.t() if tb else b
+            ms_cublas = timeit(lambda: torch.matmul(a, bt))
+            fl = 2.0 * M * Nn * K
+            print(f"M={M} N={Nn} K={K} transB={tb}: ours {ms:.3f} ms {fl / ms / 1e9:.0f} TF/s | "
+                  f"cuBLAS {ms_cublas:.3f} ms {fl / ms_cublas / 1e9:.0f} TF/s")
+
+
+def layer():
+    import paper_2603_05500_b200 as P
+    from paper_2603_05500_b200.trainer import FlatGroup, PoetLinear
+    print("== POET-X layer (bf16, b=256, T=8192) ==")
+    T = 8192
+    for m, n in [(2048, 2048), (2048, 5632), (5632, 2048)]:
+        b = 256
+        g = FlatGroup({"x.r": (m // b) * b * (b - 1) // 2, "x.p": (n // b) * b * (b - 1) // 2}, "cuda")
+        lay = PoetLinear("x", m, n, b, g, P.Rng(0))
+        x = torch.randn((T, m), device="cuda").bfloat16().requires_grad_(True)
+        dz = torch.randn((T, n), device="cuda").bfloat16()
+
+        def fact():
+            lay.invalidate(); lay.factors()
+
+        def fwd():
+            return lay(x)
+
+        def fwdbwd():
+            z = lay(x)
+            z.backward(dz)
+        t_f = timeit(fact, 5, 1)
+        t_fw = timeit(fwd, 5, 1)
+        t_fb = timeit(fwdbwd, 5, 1)
+        gemm_ms = 2 * 2.0 * T * m * n / 1.4e15 * 1e3
+        print(f"{m}->{n}: factors {t_f:.3f} ms, fwd {t_fw:.3f} ms, fwd+bwd {t_fb:.3f} ms "
+              f"(2 GEMMs at 1.4 PF would be {gemm_ms:.3f} ms)")
+    N.lib().poetx_prof_enable(0)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1] if len(sys.argv) > 1 else "all"
+    if what in ("gemm", "all"):
+        gemm()
+    if what in ("layer", "all"):
+        layer()
