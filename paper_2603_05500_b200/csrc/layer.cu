@@ -16,6 +16,7 @@ int segmented_outer(int dt, int64_t T, int64_t nb, int64_t b, const void* x, con
                     void* out, int accumulate, Workspace& ws, cudaStream_t st);
 size_t cnp_ws_bytes(int dt, int64_t nb, int64_t b, int k);
 size_t outer_ws_bytes(int dt, int64_t T, int64_t nb, int64_t b);
+size_t tc_outer_ws_bytes(int64_t T, int64_t nb, int64_t b);
 }  // namespace poetx
 
 using namespace poetx;
@@ -102,6 +103,11 @@ size_t poetx_layer_workspace_bytes(const poetx_layer_desc* d, int64_t T) {
   size_t outer = outer_ws_bytes(d->dtype, T, d->m / d->b, d->b);
   size_t outer2 = outer_ws_bytes(d->dtype, T, d->n / d->b, d->b);
   if (outer2 > outer) outer = outer2;
+  if (d->dtype == POETX_BF16) {
+    size_t t1 = tc_outer_ws_bytes(T, d->m / d->b, d->b), t2 = tc_outer_ws_bytes(T, d->n / d->b, d->b);
+    if (t1 > outer) outer = t1;
+    if (t2 > outer) outer = t2;
+  }
   size_t cnp = cnp_bwd_ws(d);
   return 4 * act + grads + (outer > cnp ? outer : cnp) + 8192;
 }

@@ -476,9 +476,33 @@ int segmented_outer(int dt, int64_t T, int64_t nb, int64_t b, const void* x, con
   const int out_dt = dt == POETX_F64 ? POETX_F64 : POETX_F32;
   const size_t acc_sz = out_dt == POETX_F64 ? 8 : 4;
   if (nb <= 0 || b <= 0) return POETX_OK;
-  if (dt == POETX_BF16 && tc_enabled() && !accumulate) {
-    int rc = tc_segmented_outer(T, nb, b, x, y, static_cast<float*>(out), ws, st);
-    if (rc != POETX_ENOTSUPPORTED) return rc;
+  if (dt == POETX_BF16 && tc_enabled() && b % 64 == 0 && dim % 8 == 0 && T > 0) {
+    // tcgen05: both operands MN-major (tokens are the contraction index),
+    // deterministic split-T partials reduced in fixed order
+    const int s = tc_outer_splits(T, nb, b);
+    float* tgt = static_cast<float*>(out);
+    if (s > 1 || accumulate) {
+      tgt = static_cast<float*>(ws.take_bytes(static_cast<size_t>(s) * total * 4));
+      POETX_REQUIRE(tgt, POETX_ESHAPE, "segmented_outer: workspace too small");
+    }
+    TcOperand xa{x, T, dim, dim, true};
+    TcOperand yb{y, T, dim, dim, true};
+    TcProblem p{};
+    p.M = b; p.N = b; p.K = T; p.groups = static_cast<int>(nb); p.splits = s;
+    p.bn = static_cast<int>(b < 256 ? b : 256);
+    p.a_g0 = static_cast<int>(b); p.b_g0 = static_cast<int>(b);
+    p.C = tgt; p.ldc = b; p.c_goff = b * b; p.c_soff = total; p.out_f32 = 1; p.alpha = 1.0f;
+    p.name = "tc_outer";
+    int rc = tc_grouped(xa, yb, p, st);
+    if (rc != POETX_ENOTSUPPORTED) {
+      POETX_TRY(rc);
+      if (tgt != out) {
+        reduce_splits_kernel<float><<<grid_for(total, 256), 256, 0, st>>>(
+            total, s, tgt, static_cast<float*>(out), accumulate);
+        POETX_LAUNCHED("reduce_splits");
+      }
+      return POETX_OK;
+    }
   }
   int splits = outer_splits(T, nb, b);
   int64_t chunk = (T + splits - 1) / splits;

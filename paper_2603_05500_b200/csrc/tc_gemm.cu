@@ -1,23 +1,31 @@
-// tcgen05 / TMEM / TMA tensor-core GEMM for the BF16 path (sm_100a).
+// tcgen05 / TMEM / TMA tensor-core kernels for the BF16 path (sm_100a).
 //
-//   C[M,N] = A[M,K] . op(B)[K,N]     BF16 operands, FP32 accumulation in TMEM
+// One warp-specialised, persistent kernel serves every tensor-core product
+// on the POET-X path as a *grouped* GEMM
 //
-// used for the layer's one dense product t = a PM (mm2, layer.py:222) and
-// its adjoint da = dt PM^T (layer.py:249).  A is K-major (row-major
-// activations); B is MN-major for mm2 (PM row-major [K=m, N=n]) and
-// K-major for the adjoint (PM read as [N=m, K=n]), selected by the UMMA
-// instruction descriptor -- PM is stored once.
+//   for g in groups, s in k-splits:   C[g, s][M, N] = A[g][M, K_s] . B[g][K_s, N]
 //
-// Structure (one CTA per SM, persistent over 128x256 output tiles):
-//   warp 0      TMA producer: 4-stage ring of {A 128x64, B 256x64} tiles
-//               (SWIZZLE_128B), mbarrier full/empty handshake;
-//   warp 1      MMA issuer: one elected lane issues tcgen05.mma
-//               (M=128, N=256, K=16) into a double-buffered TMEM
-//               accumulator (2 x 256 fp32 columns), tcgen05.commit frees
-//               smem stages and publishes finished accumulators;
-//   warp 2      TMEM allocator (512 columns);
-//   warps 4..7  epilogue: tcgen05.ld 32x32b -> bf16 -> global, then release
-//               the accumulator so the next tile's MMAs overlap the store.
+// with BF16 operands addressed through 2-D TMA tensor maps (each group adds
+// a fixed coordinate offset, so block-diagonal segments, stacks of b x b
+// blocks and split-K slices are all views of one tensor, never copies),
+// either operand K-major or MN-major (a transposed operand is just the
+// other major in the UMMA instruction descriptor), and FP32 accumulation
+// in TMEM written out as BF16 or FP32:
+//
+//   mm2 t = a PM / adjoint da = dt PM^T    (layer.py:222, 249)   1 group
+//   apply_to_features y_s = x_s G[s]       (blockdiag.py:58-73)  nb groups
+//   segmented_outer dG[s] = x_s^T y_s      (blockdiag.py:100-121) nb groups x splits
+//   CNP products Q^2, Q^2 Q, ...           (cnp.py:99-145)       nb groups
+//
+// Roles (one CTA per SM, 256 threads):
+//   warp 0      TMA producer: STAGES-deep ring of {A 128x64, B BNx64}
+//               SWIZZLE_128B tiles, mbarrier full/empty handshake;
+//   warp 1      MMA issuer: one lane issues tcgen05.mma (M=128, N=BN, K=16)
+//               into a double-buffered TMEM accumulator; tcgen05.commit
+//               releases smem stages / publishes finished accumulators;
+//   warp 2      TMEM allocator;
+//   warps 4..7  epilogue: tcgen05.ld 32x32b -> BF16/FP32 -> global, then
+//               release the accumulator (next tile's MMAs overlap the store).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -35,13 +43,16 @@ bool tc_enabled() { return g_tc_on != 0; }
 
 namespace tc {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;             // 16 KB
-constexpr int B_BYTES = BN * BK * 2;             // 32 KB
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;   // 48 KB
-constexpr int TMEM_COLS = 512;                   // 2 accumulators x 256 fp32 columns
-constexpr int THREADS = 256;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int BM = 128, BK = 64, THREADS = 256;
+constexpr int A_BYTES = BM * BK * 2;  // 16 KB
+
+template <int BN> struct Cfg {
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+};
 
 // ------------------------------------------------------------ PTX helpers --
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -116,10 +127,21 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= static_cast<uint64_t>(2) << 61;
   return d;
 }
-// instruction descriptor kind::f16: D fp32, A/B bf16, A K-major, B major per flag
-__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool b_mn_major) {
-  return (1u << 4) | (1u << 7) | (1u << 10) | ((b_mn_major ? 1u : 0u) << 16) |
-         (static_cast<uint32_t>(N >> 3) << 17) | (static_cast<uint32_t>(M >> 4) << 24);
+// K-major SW128: rows of 128 B, 8-row groups 1024 B apart; a K=16 step is +32 B.
+// MN-major SW128: 64-element MN atoms of BK rows (LBO = BK*128 B apart), 8-row
+// K groups 1024 B apart (SBO); a K=16 step is +16 rows = +2048 B.
+template <bool MN>
+__device__ __forceinline__ uint64_t operand_desc(uint32_t base, int kstep) {
+  if constexpr (MN)
+    return sdesc(base + kstep * 2048, BK * 128, 1024);
+  else
+    return sdesc(base + kstep * 32, 16, 1024);
+}
+// instruction descriptor kind::f16: D fp32, A/B bf16, majors, N, M
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((a_mn ? 1u : 0u) << 15) |
+         ((b_mn ? 1u : 0u) << 16) | (static_cast<uint32_t>(N >> 3) << 17) |
+         (static_cast<uint32_t>(M >> 4) << 24);
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
@@ -141,30 +163,36 @@ __device__ __forceinline__ uint32_t pack_bf16(uint32_t lo, uint32_t hi) {
   return *reinterpret_cast<uint32_t*>(&v);
 }
 
-struct GemmArgs {
-  int M, N, K;
-  __nv_bfloat16* C;
-  int64_t ldc;
+struct Args {
+  int M, N, K;             // per group; K is split into `splits` chunks of kps
+  int groups, splits, kps;
   int m_tiles, n_tiles;
+  int a_g0, a_g1, b_g0, b_g1;  // per-group TMA coordinate offsets (c0, c1)
+  void* C;
+  int64_t ldc, c_goff, c_soff;  // element strides: row, group, split
+  int out_f32;
+  float alpha;
 };
 
 // ------------------------------------------------------------------ kernel --
-template <bool B_MN_MAJOR>
+template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(THREADS, 1)
-    tc_gemm_kernel(const __grid_constant__ CUtensorMap map_a,
-                   const __grid_constant__ CUtensorMap map_b, GemmArgs args) {
+    tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+              Args args) {
+  using CF = Cfg<BN>;
+  constexpr int STAGES = CF::STAGES;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;   // [2]
-  uint64_t* tempty = tfull + 2;       // [2]
+  uint64_t* tfull = empty + STAGES;  // [2]
+  uint64_t* tempty = tfull + 2;      // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int num_tiles = args.m_tiles * args.n_tiles;
-  const int k_blocks = (args.K + BK - 1) / BK;
+  const int tiles_per_split = args.m_tiles * args.n_tiles;
+  const int num_tiles = tiles_per_split * args.splits * args.groups;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
@@ -181,7 +209,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == 2) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS)
+                 "r"(CF::TMEM_COLS)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -189,6 +217,19 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+
+  auto decode = [&](int tile, int& g, int& s, int& m0, int& n0, int& kb0, int& kbn) {
+    g = tile / (tiles_per_split * args.splits);
+    int r = tile % (tiles_per_split * args.splits);
+    s = r / tiles_per_split;
+    r %= tiles_per_split;
+    m0 = (r / args.n_tiles) * BM;
+    n0 = (r % args.n_tiles) * BN;
+    int k0 = s * args.kps;
+    int k1 = k0 + args.kps < args.K ? k0 + args.kps : args.K;
+    kb0 = k0 / BK;
+    kbn = (k1 - k0 + BK - 1) / BK;
+  };
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -198,20 +239,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-        const int m0 = (tile / args.n_tiles) * BM, n0 = (tile % args.n_tiles) * BN;
-        for (int kb = 0; kb < k_blocks; ++kb) {
+        int g, s, m0, n0, kb0, kbn;
+        decode(tile, g, s, m0, n0, kb0, kbn);
+        const int ag0 = args.a_g0 * g, ag1 = args.a_g1 * g;
+        const int bg0 = args.b_g0 * g, bg1 = args.b_g1 * g;
+        for (int kb = kb0; kb < kb0 + kbn; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = smem + stage * STAGE_BYTES;
+          uint8_t* sa = smem + stage * CF::STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
-          mbar_expect_tx(&full[stage], STAGE_BYTES);
-          tma_load_2d(sa, &map_a, &full[stage], kb * BK, m0);
-          if constexpr (B_MN_MAJOR) {
-            // four 64-wide N atoms, each BK K-rows of 128 B
+          const int k = kb * BK;
+          mbar_expect_tx(&full[stage], CF::STAGE_BYTES);
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int j = 0; j < BM / 64; ++j)
+              tma_load_2d(sa + j * (BK * 128), &map_a, &full[stage], ag0 + m0 + j * 64, ag1 + k);
+          } else {
+            tma_load_2d(sa, &map_a, &full[stage], ag0 + k, ag1 + m0);
+          }
+          if constexpr (B_MN) {
 #pragma unroll
             for (int j = 0; j < BN / 64; ++j)
-              tma_load_2d(sb + j * (BK * 128), &map_b, &full[stage], n0 + j * 64, kb * BK);
+              tma_load_2d(sb + j * (BK * 128), &map_b, &full[stage], bg0 + n0 + j * 64, bg1 + k);
           } else {
-            tma_load_2d(sb, &map_b, &full[stage], kb * BK, n0);
+            tma_load_2d(sb, &map_b, &full[stage], bg0 + k, bg1 + n0);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -219,38 +269,35 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
-    constexpr uint32_t idesc = idesc_bf16(BM, BN, B_MN_MAJOR);
+    constexpr uint32_t idesc = idesc_bf16(BM, BN, A_MN, B_MN);
     int stage = 0;
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+      int g, s, m0, n0, kb0, kbn;
+      decode(tile, g, s, m0, n0, kb0, kbn);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       fence_after();
       const uint32_t tmem_d = tmem_base + acc * BN;
-      for (int kb = 0; kb < k_blocks; ++kb) {
+      for (int kb = 0; kb < kbn; ++kb) {
         mbar_wait(&full[stage], phase);
         fence_after();
         if (lane == 0) {
-          const uint32_t a_addr = smem_u32(smem + stage * STAGE_BYTES);
+          const uint32_t a_addr = smem_u32(smem + stage * CF::STAGE_BYTES);
           const uint32_t b_addr = a_addr + A_BYTES;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // K-major SW128: advance 16 elements = 32 B inside the 128 B swizzle row
-            const uint64_t ad = sdesc(a_addr + k * 32, 16, 1024);
-            uint64_t bd;
-            if constexpr (B_MN_MAJOR)
-              bd = sdesc(b_addr + k * 16 * 128, BK * 128, 1024);  // 16 K-rows per step
-            else
-              bd = sdesc(b_addr + k * 32, 16, 1024);
-            umma_bf16(tmem_d, ad, bd, idesc, (kb | k) != 0);
-          }
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16(tmem_d, operand_desc<A_MN>(a_addr, k), operand_desc<B_MN>(b_addr, k), idesc,
+                      (kb | k) != 0);
           umma_commit(&empty[stage]);  // smem stage free once these MMAs retire
-          if (kb == k_blocks - 1) umma_commit(&tfull[acc]);
+          if (kb == kbn - 1) umma_commit(&tfull[acc]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (kbn == 0 && lane == 0) umma_commit(&tfull[acc]);  // empty K range
+      __syncwarp();
       if (++acc == 2) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
@@ -259,25 +306,43 @@ __global__ void __launch_bounds__(THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-      const int m0 = (tile / args.n_tiles) * BM, n0 = (tile % args.n_tiles) * BN;
+      int g, s, m0, n0, kb0, kbn;
+      decode(tile, g, s, m0, n0, kb0, kbn);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
       const int row = m0 + ew * 32 + lane;
-      __nv_bfloat16* crow = args.C + static_cast<int64_t>(row) * args.ldc;
+      const int64_t base = g * args.c_goff + s * args.c_soff + static_cast<int64_t>(row) * args.ldc;
+      const bool row_ok = row < args.M;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];
         tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c, r);
-        if (row < args.M && n0 + c < args.N) {
-          uint4* dst = reinterpret_cast<uint4*>(crow + n0 + c);
+        if (kbn == 0) {
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            uint4 v;
-            v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
-            v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
-            v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
-            v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
-            dst[q] = v;
+          for (int q = 0; q < 32; ++q) r[q] = 0u;
+        }
+        if (args.alpha != 1.0f) {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * args.alpha);
+        }
+        if (row_ok && n0 + c < args.N) {
+          if (args.out_f32) {
+            uint4* dst = reinterpret_cast<uint4*>(static_cast<float*>(args.C) + base + n0 + c);
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              dst[q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+          } else {
+            uint4* dst =
+                reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + base + n0 + c);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              uint4 v;
+              v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
+              v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
+              v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
+              v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
+              dst[q] = v;
+            }
           }
         }
       }
@@ -293,7 +358,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   fence_after();
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
-                 "r"(TMEM_COLS)
+                 "r"(CF::TMEM_COLS)
                  : "memory");
   }
 }
@@ -313,14 +378,14 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
-// 2-D bf16 tensor map: dims {inner, outer}, row pitch in elements, box {bi, bo}
-int make_map(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t pitch,
-             uint32_t box_inner, uint32_t box_outer) {
+// 2-D bf16 tensor map over a row-major [rows, cols] view with row pitch
+int make_map(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
+             uint32_t box_cols, uint32_t box_rows) {
   auto fn = encode_fn();
   POETX_REQUIRE(fn != nullptr, POETX_ECUDA, "cuTensorMapEncodeTiled unavailable");
-  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {pitch * 2};
-  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides,
                   box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -340,55 +405,122 @@ int num_sms() {
   return n;
 }
 
-template <bool MN>
-int launch(const CUtensorMap& ma, const CUtensorMap& mb, const GemmArgs& a, cudaStream_t st) {
+template <int BN, bool A_MN, bool B_MN>
+int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Args& a, const char* name,
+             cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tc_gemm_kernel<MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         SMEM_BYTES);
+    cudaFuncSetAttribute(tc_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<BN>::SMEM_BYTES);
     attr_set = true;
   }
-  int tiles = a.m_tiles * a.n_tiles;
-  int grid = tiles < num_sms() ? tiles : num_sms();
+  int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles * a.splits * a.groups;
+  int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
+  if (grid <= 0) return POETX_OK;
   void* tok = prof_begin(st);
-  tc_gemm_kernel<MN><<<grid, THREADS, SMEM_BYTES, st>>>(ma, mb, a);
-  prof_end(tok, "tc_gemm", 2.0 * a.M * a.N * a.K, st);
-  POETX_LAUNCHED("tc_gemm");
+  tc_kernel<BN, A_MN, B_MN><<<grid, THREADS, Cfg<BN>::SMEM_BYTES, st>>>(ma, mb, a);
+  prof_end(tok, name, 2.0 * a.M * a.N * static_cast<double>(a.K) * a.groups, st);
+  POETX_LAUNCHED(name);
   return POETX_OK;
+}
+
+template <int BN>
+int launch_bn(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const Args& a,
+              const char* name, cudaStream_t st) {
+  if (!a_mn && !b_mn) return launch_t<BN, false, false>(ma, mb, a, name, st);
+  if (!a_mn && b_mn) return launch_t<BN, false, true>(ma, mb, a, name, st);
+  if (a_mn && !b_mn) return launch_t<BN, true, false>(ma, mb, a, name, st);
+  return launch_t<BN, true, true>(ma, mb, a, name, st);
 }
 
 }  // namespace tc
 
-int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
-              const void* B, int64_t ldb, int transB, void* C, int64_t ldc, cudaStream_t st) {
+// An operand is a row-major [rows, cols] bf16 view with a row pitch.
+// K-major: the contraction index runs along cols; MN-major: along rows.
+int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaStream_t st) {
   using namespace tc;
-  if (transA) return POETX_ENOTSUPPORTED;
-  if (M <= 0 || N <= 0) return POETX_OK;
-  if (K <= 0 || N % 32 || K % 8 || lda % 8 || ldb % 8 || ldc % 8) return POETX_ENOTSUPPORTED;
-  if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) |
-       reinterpret_cast<uintptr_t>(C)) & 15)
-    return POETX_ENOTSUPPORTED;
-  if (M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return POETX_ENOTSUPPORTED;
-  CUtensorMap ma, mb;
-  POETX_TRY(make_map(&ma, A, K, M, lda, BK, BM));
-  GemmArgs a{static_cast<int>(M), static_cast<int>(N), static_cast<int>(K),
-             static_cast<__nv_bfloat16*>(C), ldc, static_cast<int>((M + BM - 1) / BM),
-             static_cast<int>((N + BN - 1) / BN)};
-  if (transB) {
-    // B stored [N, K] row-major: K-major operand
-    POETX_TRY(make_map(&mb, B, K, N, ldb, BK, BN));
-    return launch<false>(ma, mb, a, st);
+  const int BN = p.bn;
+  POETX_REQUIRE(BN == 64 || BN == 128 || BN == 256, POETX_ESHAPE, "tc: bad BN %d", BN);
+  if (p.M <= 0 || p.N <= 0 || p.groups <= 0) return POETX_OK;
+  for (const TcOperand* o : {&A, &B}) {
+    if ((reinterpret_cast<uintptr_t>(o->ptr) & 15) || (o->pitch % 8)) return POETX_ENOTSUPPORTED;
   }
-  // B stored [K, N] row-major: MN-major operand, 64-wide N atoms
-  POETX_TRY(make_map(&mb, B, N, K, ldb, 64, BK));
-  return launch<true>(ma, mb, a, st);
+  if ((reinterpret_cast<uintptr_t>(p.C) & 15) || (p.ldc % 8) || (p.c_goff % 8) || (p.c_soff % 8))
+    return POETX_ENOTSUPPORTED;
+  if (p.N % 32) return POETX_ENOTSUPPORTED;
+  CUtensorMap ma, mb;
+  POETX_TRY(make_map(&ma, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : BM));
+  POETX_TRY(make_map(&mb, B.ptr, B.cols, B.rows, B.pitch, 64, B.mn_major ? BK : BN));
+  Args a{};
+  a.M = static_cast<int>(p.M);
+  a.N = static_cast<int>(p.N);
+  a.K = static_cast<int>(p.K);
+  a.groups = p.groups;
+  a.splits = p.splits < 1 ? 1 : p.splits;
+  int64_t kps = (p.K + a.splits - 1) / a.splits;
+  kps = (kps + BK - 1) / BK * BK;
+  a.kps = static_cast<int>(kps > 0 ? kps : BK);
+  a.m_tiles = static_cast<int>((p.M + BM - 1) / BM);
+  a.n_tiles = static_cast<int>((p.N + BN - 1) / BN);
+  a.a_g0 = p.a_g0; a.a_g1 = p.a_g1; a.b_g0 = p.b_g0; a.b_g1 = p.b_g1;
+  a.C = p.C;
+  a.ldc = p.ldc; a.c_goff = p.c_goff; a.c_soff = p.c_soff;
+  a.out_f32 = p.out_f32;
+  a.alpha = p.alpha;
+  const char* name = p.name ? p.name : "tc_gemm";
+  if (BN == 256) return launch_bn<256>(A.mn_major, B.mn_major, ma, mb, a, name, st);
+  if (BN == 128) return launch_bn<128>(A.mn_major, B.mn_major, ma, mb, a, name, st);
+  return launch_bn<64>(A.mn_major, B.mn_major, ma, mb, a, name, st);
 }
 
-int tc_blockdiag(const GemmDesc&, cudaStream_t) { return POETX_ENOTSUPPORTED; }
-size_t tc_outer_ws_bytes(int64_t, int64_t, int64_t) { return 0; }
-int tc_segmented_outer(int64_t, int64_t, int64_t, const void*, const void*, float*, Workspace&,
-                       cudaStream_t) {
-  return POETX_ENOTSUPPORTED;
+int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
+              const void* B, int64_t ldb, int transB, void* C, int64_t ldc, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return POETX_OK;
+  if (K <= 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return POETX_ENOTSUPPORTED;
+  // op(A)[M,K]: stored [M,K] (K-major) or [K,M] (MN-major)
+  TcOperand a{A, transA ? K : M, transA ? M : K, lda, transA != 0};
+  // op(B)[K,N]: stored [K,N] (MN-major) or [N,K] (K-major)
+  TcOperand b{B, transB ? N : K, transB ? K : N, ldb, transB == 0};
+  TcProblem p{};
+  p.M = M; p.N = N; p.K = K; p.groups = 1; p.splits = 1; p.bn = 256;
+  p.C = C; p.ldc = ldc; p.alpha = 1.0f; p.name = "tc_gemm";
+  return tc_grouped(a, b, p, st);
+}
+
+int tc_blockdiag(const GemmDesc& d, cudaStream_t st) {
+  // apply_to_features: A = x [T, dim] K-major with group column offset b;
+  // B = G stack [nb*b, b] (MN-major for G, K-major for G^T) with row offset b
+  const int64_t b = d.K, nb = d.batch, dim = d.sAm, T = d.M;
+  if (b % 64 || b > 256 || d.N != b || d.sAk != 1 || d.sAb != b || d.sCm != dim ||
+      d.sCb != b || d.sCn != 1 || d.sBb != b * b)
+    return POETX_ENOTSUPPORTED;
+  const bool trans = d.sBk == 1;
+  TcOperand x{d.A, T, dim, dim, false};
+  TcOperand g{d.B, nb * b, b, b, !trans};
+  TcProblem p{};
+  p.M = T; p.N = b; p.K = b; p.groups = static_cast<int>(nb); p.splits = 1;
+  p.bn = static_cast<int>(b);
+  p.a_g0 = static_cast<int>(b);
+  p.b_g1 = static_cast<int>(b);
+  p.C = d.C; p.ldc = dim; p.c_goff = b;
+  p.alpha = 1.0f; p.name = "tc_blockdiag";
+  return tc_grouped(x, g, p, st);
+}
+
+size_t tc_outer_ws_bytes(int64_t T, int64_t nb, int64_t b) {
+  int s = tc_outer_splits(T, nb, b);
+  return s > 1 ? align_up(static_cast<size_t>(s) * nb * b * b * 4) : 0;
+}
+
+int tc_outer_splits(int64_t T, int64_t nb, int64_t b) {
+  int64_t bn = b < 256 ? b : 256;
+  int64_t tiles = nb * ((b + 127) / 128) * ((b + bn - 1) / bn);
+  int64_t want = (2 * 148 + tiles - 1) / tiles;
+  int64_t maxs = (T + 255) / 256;
+  if (want > maxs) want = maxs;
+  if (want < 1) want = 1;
+  if (want > 64) want = 64;
+  return static_cast<int>(want);
 }
 
 }  // namespace poetx

@@ -12,6 +12,31 @@ constexpr int POETX_ENOTSUPPORTED = -100;  // internal: "use another kernel"
 
 bool tc_enabled();
 
+// A bf16 operand: row-major [rows, cols] view with a row pitch (elements).
+// K-major: the contraction index runs along cols; MN-major: along rows.
+struct TcOperand {
+  const void* ptr;
+  int64_t rows, cols, pitch;
+  bool mn_major;
+};
+
+// Grouped/split-K problem: for g < groups, s < splits,
+//   C[g*c_goff + s*c_soff + m*ldc + n] = alpha * sum_{k in split s} A_g[m,k] B_g[k,n]
+// where group g shifts the operand TMA coordinates (col, row) by
+// (a_g0*g, a_g1*g) and (b_g0*g, b_g1*g).  BF16 or FP32 output.
+struct TcProblem {
+  int64_t M, N, K;
+  int groups, splits, bn;
+  int a_g0, a_g1, b_g0, b_g1;
+  void* C;
+  int64_t ldc, c_goff, c_soff;
+  int out_f32;
+  float alpha;
+  const char* name;
+};
+
+int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaStream_t st);
+
 // C[M,N] = op(A) op(B), BF16 in, fp32 accumulate (TMEM), BF16 out.
 int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
               const void* B, int64_t ldb, int transB, void* C, int64_t ldc, cudaStream_t st);
@@ -19,9 +44,8 @@ int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int t
 // y_s = x_s g[s] (or g[s]^T) for every length-b segment s; BF16.
 int tc_blockdiag(const GemmDesc& d, cudaStream_t st);
 
-// out[s] = sum_t x_s^T y_s, BF16 in, fp32 out (overwrites out).
+// split-K factor used by the tensor-core segmented outer product
+int tc_outer_splits(int64_t T, int64_t nb, int64_t b);
 size_t tc_outer_ws_bytes(int64_t T, int64_t nb, int64_t b);
-int tc_segmented_outer(int64_t T, int64_t nb, int64_t b, const void* x, const void* y, float* out,
-                       Workspace& ws, cudaStream_t st);
 
 }  // namespace poetx
