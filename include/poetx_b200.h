@@ -108,6 +108,19 @@ int poetx_cnp_forward(int dtype, int64_t nb, int64_t b, int k, const void* q,
 int poetx_cnp_backward(int dtype, int64_t nb, int64_t b, int k, const void* q,
                        const void* packed, const void* q2, const void* dg, void* dq,
                        void* dpacked, int accumulate, void* ws, size_t ws_bytes, void* stream);
+/* Tensor-core CNP for the BF16 path, k = 3, b in {64, 128, 256}, over a
+ * stack of nb blocks (e.g. every block of a model: the packed parameters
+ * are one flat buffer).  Forward: packed fp32 [nb, b(b-1)/2] ->
+ * qq2 = [Q | Q^2] bf16 [nb, b, 2b] (the backward's cache) and
+ * G = I + 2(Q+Q^2+Q^3) + Q^4 as bf16 and/or fp32 [nb, b, b]
+ * (cnp.py:99-116).  Backward: dG fp32 [nb, b, b] -> packed fp32 gradient
+ * via dQ = 2(N1+N2) + (2Q+Q^2)^T N2 + (2N1+N2)(Q^2)^T, N2 = -(N1 Q + Q N1)
+ * (cnp.py:128-145 regrouped) and g_ij = dQ_ij - dQ_ji. */
+size_t poetx_cnp_tc_workspace_bytes(int64_t nb, int64_t b);
+int poetx_cnp_forward_tc(int64_t nb, int64_t b, const float* packed, void* qq2, void* g_bf16,
+                         float* g_f32, void* ws, size_t ws_bytes, void* stream);
+int poetx_cnp_backward_tc(int64_t nb, int64_t b, const void* qq2, const float* dg, float* dpacked,
+                          int accumulate, void* ws, size_t ws_bytes, void* stream);
 /* cayley-free orthogonality audit ||G^T G - I||_F over the stack
  * (blockdiag.py:134-138).  out: DEVICE double[1]. */
 int poetx_orthogonality_error(int dtype, int64_t nb, int64_t b, const void* g, double* out,
@@ -193,6 +206,14 @@ int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t*
                          const void* x, const void* dz, const void* saved_t, void* dx,
                          void* dpacked_r, void* dpacked_p, int accumulate, void* ws,
                          size_t ws_bytes, void* stream);
+/* Same chain, but instead of running the CNP backward per layer it leaves
+ * the block-factor cotangents dG_R [m/b,b,b], dG_P [n/b,b,b] (fp32; F64 for
+ * F64 layers) in caller buffers (accumulate != 0 adds) so one batched
+ * poetx_cnp_backward_tc can serve every layer of a model. */
+int poetx_layer_backward_dg(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                            const void* x, const void* dz, const void* saved_t, void* dx,
+                            void* dg_r, void* dg_p, int accumulate, void* ws, size_t ws_bytes,
+                            void* stream);
 /* merge_and_reinit numerics (layer.py:260-314): new premerged
  * PM'[i,j] = M[inv_in(new_in(i)), inv_out(new_out(j))] with
  * M = blockdiag(G_R) PM blockdiag(G_P) computed in fp32/fp64 from the

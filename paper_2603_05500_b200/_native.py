@@ -85,6 +85,11 @@ _SIGS = {
     "poetx_cnp_workspace_bytes": (SZ, [I32, I64, I64, I32]),
     "poetx_cnp_forward": (I32, [I32, I64, I64, I32, VP, VP, VP, VP, VP, VP, SZ, VP]),
     "poetx_cnp_backward": (I32, [I32, I64, I64, I32, VP, VP, VP, VP, VP, VP, I32, VP, SZ, VP]),
+    "poetx_cnp_tc_workspace_bytes": (SZ, [I64, I64]),
+    "poetx_cnp_forward_tc": (I32, [I64, I64, VP, VP, VP, VP, VP, SZ, VP]),
+    "poetx_cnp_backward_tc": (I32, [I64, I64, VP, VP, VP, I32, VP, SZ, VP]),
+    "poetx_layer_backward_dg": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I64, VP, VP, VP,
+                                      VP, VP, VP, I32, VP, SZ, VP]),
     "poetx_orthogonality_error": (I32, [I32, I64, I64, VP, VP, VP, SZ, VP]),
     "poetx_permute_cols": (I32, [I32, I64, I64, VP, VP, VP, VP]),
     "poetx_permute_rows": (I32, [I32, I64, I64, VP, VP, VP, VP]),

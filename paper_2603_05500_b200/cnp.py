@@ -146,3 +146,38 @@ def cayley_exact(q):
     rhs = (eye + q64).transpose(1, 2)
     sol = torch.linalg.solve(lhs, rhs).transpose(1, 2).contiguous().to(q.dtype)
     return _out(sol, was_np)
+
+
+# ----------------------------------------------------- BF16 tensor-core path --
+
+
+def cnp_forward_tc(packed: torch.Tensor, block_dim: int, want_fp32: bool = False):
+    """Tensor-core CNP (k = 3) for the BF16 path over a whole stack of blocks:
+    packed fp32 (nb, b(b-1)/2) -> (G bf16 (nb, b, b), cache [Q | Q^2] bf16,
+    G fp32 or None).  Same algebra as cnp_forward (cnp.py:109-116)."""
+    if packed.dtype != torch.float32 or packed.ndim != 2 or packed.shape[1] != num_pairs(block_dim):
+        raise ShapeError(f"packed must be float32 (nb, {num_pairs(block_dim)}), got {tuple(packed.shape)}")
+    nb, b = packed.shape[0], block_dim
+    dev = packed.device
+    qq2 = torch.empty((nb, b, 2 * b), dtype=torch.bfloat16, device=dev)
+    g16 = torch.empty((nb, b, b), dtype=torch.bfloat16, device=dev)
+    g32 = torch.empty((nb, b, b), dtype=torch.float32, device=dev) if want_fp32 else None
+    ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(nb, b), dev)
+    N.call("poetx_cnp_forward_tc", nb, b, packed.contiguous().data_ptr(), qq2.data_ptr(), g16.data_ptr(),
+           N.ptr(g32), ws, wsb, N.stream_ptr(dev))
+    return g16, qq2, g32
+
+
+def cnp_backward_tc(qq2: torch.Tensor, dg: torch.Tensor, out: torch.Tensor | None = None,
+                    accumulate: bool = False) -> torch.Tensor:
+    """Tensor-core closed-form backward (cnp.py:136-145 regrouped) fused with
+    the packed projection (cnp.py:81-86): dG fp32 (nb, b, b) -> packed grad."""
+    nb, b, _ = qq2.shape
+    if tuple(dg.shape) != (nb, b, b) or dg.dtype != torch.float32:
+        raise ShapeError(f"dG must be float32 {(nb, b, b)}, got {tuple(dg.shape)} {dg.dtype}")
+    if out is None:
+        out = torch.empty((nb, num_pairs(b)), dtype=torch.float32, device=qq2.device)
+    ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(nb, b), qq2.device)
+    N.call("poetx_cnp_backward_tc", nb, b, qq2.data_ptr(), dg.contiguous().data_ptr(), out.data_ptr(),
+           int(accumulate), ws, wsb, N.stream_ptr(qq2.device))
+    return out

@@ -161,26 +161,26 @@ int poetx_layer_forward(const poetx_layer_desc* d, const poetx_layer_factors_t* 
   return POETX_OK;
 }
 
-int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
-                         const void* x, const void* dz, const void* saved_t, void* dx,
-                         void* dpacked_r, void* dpacked_p, int accumulate, void* ws,
-                         size_t ws_bytes, void* stream) {
-  POETX_TRY(check_desc(d));
-  POETX_REQUIRE(T >= 0 && x && dz && f && dpacked_r && dpacked_p, POETX_ESHAPE,
-                "layer_backward: bad arguments");
+static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_factors_t* f,
+                               int64_t T, const void* x, const void* dz, const void* saved_t,
+                               void* dx, void* dpacked_r, void* dpacked_p, void* dg_r_out,
+                               void* dg_p_out, int accumulate, void* ws, size_t ws_bytes,
+                               void* stream) {
   cudaStream_t st = as_stream(stream);
   const int dt = d->dtype, pdt = param_dtype(dt);
   const int64_t w = d->m > d->n ? d->m : d->n, b = d->b, nbr = d->m / b, nbp = d->n / b;
   const size_t e = elt_size(dt), acc = elt_size(pdt);
+  const bool dg_mode = dg_r_out != nullptr;
   Workspace wsp(ws, ws_bytes);
   void* b1 = wsp.take_bytes(T * w * e);
   void* b2 = wsp.take_bytes(T * w * e);
   void* b3 = wsp.take_bytes(T * w * e);
   void* b4 = wsp.take_bytes(T * w * e);
-  void* dgr = wsp.take_bytes(nbr * b * b * acc);
-  void* dgp = wsp.take_bytes(nbp * b * b * acc);
+  void* dgr = dg_mode ? dg_r_out : wsp.take_bytes(nbr * b * b * acc);
+  void* dgp = dg_mode ? dg_p_out : wsp.take_bytes(nbp * b * b * acc);
   POETX_REQUIRE(b1 && b2 && b3 && b4 && dgr && dgp, POETX_ESHAPE,
                 "layer_backward: workspace too small");
+  const int dg_acc = dg_mode ? accumulate : 0;
   Workspace tail(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
   const void* gr = act_g(d, f->g_r, f->g_r_lowp);
   const void* gp = act_g(d, f->g_p, f->g_p_lowp);
@@ -195,7 +195,7 @@ int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t*
     t = b4;
   }
   // dG_P = segmented_outer(t, dv)  (layer.py:247)
-  POETX_TRY(segmented_outer(dt, T, nbp, b, t, b1, dgp, 0, tail, st));
+  POETX_TRY(segmented_outer(dt, T, nbp, b, t, b1, dgp, dg_acc, tail, st));
   // dt = dv blockdiag(G_P)^T  (layer.py:248)
   POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, b1, b2, st));
   // da = dt PM^T  (layer.py:249)
@@ -204,12 +204,13 @@ int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t*
   POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b1, st));
   // dG_R = segmented_outer(u, da)  (layer.py:251)
   Workspace tail2(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
-  POETX_TRY(segmented_outer(dt, T, nbr, b, b1, b3, dgr, 0, tail2, st));
+  POETX_TRY(segmented_outer(dt, T, nbr, b, b1, b3, dgr, dg_acc, tail2, st));
   if (dx) {
     // du = da blockdiag(G_R)^T ; dx = du[:, pi_in^-1]  (layer.py:252-253)
     POETX_TRY(apply_features(dt, T, nbr, b, gr, 1, b3, b2, st));
     POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_inv, b2, dx, st));
   }
+  if (dg_mode) return POETX_OK;
   // packed grads = P(cnp_backward(.))  (layer.py:254-255)
   void* cws = static_cast<char*>(ws) + wsp.used;
   size_t cwsb = ws_bytes - wsp.used;
@@ -219,6 +220,28 @@ int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t*
   POETX_TRY(poetx_cnp_backward(pdt, nbp, b, k, nullptr, f->packed_p, k == 3 ? f->q2_p : nullptr,
                                dgp, nullptr, dpacked_p, accumulate, cws, cwsb, stream));
   return POETX_OK;
+}
+
+int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                         const void* x, const void* dz, const void* saved_t, void* dx,
+                         void* dpacked_r, void* dpacked_p, int accumulate, void* ws,
+                         size_t ws_bytes, void* stream) {
+  POETX_TRY(check_desc(d));
+  POETX_REQUIRE(T >= 0 && x && dz && f && dpacked_r && dpacked_p, POETX_ESHAPE,
+                "layer_backward: bad arguments");
+  return layer_backward_impl(d, f, T, x, dz, saved_t, dx, dpacked_r, dpacked_p, nullptr, nullptr,
+                             accumulate, ws, ws_bytes, stream);
+}
+
+int poetx_layer_backward_dg(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                            const void* x, const void* dz, const void* saved_t, void* dx,
+                            void* dg_r, void* dg_p, int accumulate, void* ws, size_t ws_bytes,
+                            void* stream) {
+  POETX_TRY(check_desc(d));
+  POETX_REQUIRE(T >= 0 && x && dz && f && dg_r && dg_p, POETX_ESHAPE,
+                "layer_backward_dg: bad arguments");
+  return layer_backward_impl(d, f, T, x, dz, saved_t, dx, nullptr, nullptr, dg_r, dg_p,
+                             accumulate, ws, ws_bytes, stream);
 }
 
 size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d) {

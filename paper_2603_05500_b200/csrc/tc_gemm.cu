@@ -171,6 +171,7 @@ struct Args {
   void* C;
   int64_t ldc, c_goff, c_soff;  // element strides: row, group, split
   int out_f32;
+  int accumulate;  // fp32 output only: C += alpha * AB
   float alpha;
 };
 
@@ -327,10 +328,17 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         if (row_ok && n0 + c < args.N) {
           if (args.out_f32) {
-            uint4* dst = reinterpret_cast<uint4*>(static_cast<float*>(args.C) + base + n0 + c);
+            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.C) + base + n0 + c);
 #pragma unroll
-            for (int q = 0; q < 8; ++q)
-              dst[q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+            for (int q = 0; q < 8; ++q) {
+              float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+              if (args.accumulate) {
+                const float4 o = dst[q];
+                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              }
+              dst[q] = v;
+            }
           } else {
             uint4* dst =
                 reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + base + n0 + c);
@@ -466,6 +474,8 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
   a.C = p.C;
   a.ldc = p.ldc; a.c_goff = p.c_goff; a.c_soff = p.c_soff;
   a.out_f32 = p.out_f32;
+  a.accumulate = p.accumulate;
+  if (p.accumulate && !p.out_f32) return POETX_ENOTSUPPORTED;
   a.alpha = p.alpha;
   const char* name = p.name ? p.name : "tc_gemm";
   if (BN == 256) return launch_bn<256>(A.mn_major, B.mn_major, ma, mb, a, name, st);

@@ -31,6 +31,7 @@ struct TcProblem {
   void* C;
   int64_t ldc, c_goff, c_soff;
   int out_f32;
+  int accumulate;  // fp32 output only: C += alpha * AB
   float alpha;
   const char* name;
 };

@@ -72,3 +72,64 @@ def test_tc_segmented_outer(N, b, nb, T):
     assert err <= 1e-3 * max(1.0, ref.abs().max().item()), err
     # deterministic: bitwise identical on repeat
     assert torch.equal(out, P.segmented_outer(x, y, b))
+
+
+@pytest.mark.parametrize("b,nb,scale", [(256, 12, 0.01), (128, 5, 0.02), (64, 9, 0.03)])
+def test_tc_cnp_vs_oracle(N, b, nb, scale):
+    """BF16 tensor-core CNP (forward G and packed backward) against the float64
+    oracle restatement of cnp.py, at the bf16 tolerance 2e-2."""
+    import numpy as np
+
+    import paper_2603_05500_b200 as P
+    from oracle import poetx_oracle as O
+
+    r = np.random.default_rng(b + nb)
+    packed = scale * r.standard_normal((nb, b * (b - 1) // 2))
+    dg = r.standard_normal((nb, b, b))
+    q = O.skew_from_packed(packed, b)
+    g_ref, cache = O.cnp_forward(q, 3)
+    dp_ref = O.packed_grad_from_skew_grad(O.cnp_backward(cache, dg, 3))
+    g16, qq2, g32 = P.cnp_forward_tc(torch.from_numpy(packed).float().cuda(), b, want_fp32=True)
+    for g in (g16, g32):
+        err = np.abs(g.double().cpu().numpy() - g_ref).max()
+        assert err <= 2e-2 * max(1.0, np.abs(g_ref).max()), err
+    # fp32 G keeps the fine structure: G - I against the oracle
+    d_err = np.abs((g32.double().cpu().numpy() - g_ref)).max() / np.abs(g_ref - np.eye(b)).max()
+    assert d_err <= 2e-2, d_err
+    dp = P.cnp_backward_tc(qq2, torch.from_numpy(dg).float().cuda())
+    err = np.abs(dp.double().cpu().numpy() - dp_ref).max()
+    assert err <= 2e-2 * max(1.0, np.abs(dp_ref).max()), err
+    acc = P.cnp_backward_tc(qq2, torch.from_numpy(dg).float().cuda(), out=dp.clone(), accumulate=True)
+    assert torch.allclose(acc, 2 * dp, rtol=1e-6, atol=1e-6)
+
+
+def test_layer_backward_dg_matches_packed(N):
+    """poetx_layer_backward_dg + batched TC CNP backward == per-layer backward."""
+    import paper_2603_05500_b200 as P
+
+    m, n, b, T = 512, 768, 256, 640
+    base = torch.randn((m, n), device="cuda").div(m ** 0.5).bfloat16()
+    layer = P.PoetLinearLayer(base, b, P.Rng(3))
+    layer.q_r.packed.normal_(0, 0.01)
+    layer.q_p.packed.normal_(0, 0.01)
+    x = torch.randn((T, m), device="cuda").bfloat16()
+    dz = torch.randn((T, n), device="cuda").bfloat16()
+    z, cache = layer.forward(x)
+    g_ref = layer.backward(cache, dz)
+    # dG path
+    f = cache.factors
+    dgr = torch.empty((m // b, b, b), device="cuda")
+    dgp = torch.empty((n // b, b, b), device="cuda")
+    dx = torch.empty_like(x)
+    d = layer._desc()
+    ws, wsb = N.workspace(N.lib().poetx_layer_workspace_bytes(d, T))
+    N.call("poetx_layer_backward_dg", d, f.struct, T, x.data_ptr(), dz.data_ptr(), cache.saved_mm2.data_ptr(),
+           dx.data_ptr(), dgr.data_ptr(), dgp.data_ptr(), 0, ws, wsb, N.stream_ptr())
+    assert torch.equal(dx, g_ref.x)
+    _, qq2r, _ = P.cnp_forward_tc(f.packed_r, b)
+    _, qq2p, _ = P.cnp_forward_tc(f.packed_p, b)
+    gr = P.cnp_backward_tc(qq2r, dgr)
+    gp = P.cnp_backward_tc(qq2p, dgp)
+    for got, want in ((gr, g_ref.q_r), (gp, g_ref.q_p)):
+        err = (got - want).abs().max().item()
+        assert err <= 2e-2 * max(1.0, want.abs().max().item()), err
