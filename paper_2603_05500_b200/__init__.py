@@ -22,6 +22,8 @@ from .cnp import (
     SkewParams,
     cayley_exact,
     cnp_backward,
+    cnp_backward_tc,
+    cnp_forward_tc,
     cnp_forward,
     num_pairs,
     packed_grad_from_skew_grad,
