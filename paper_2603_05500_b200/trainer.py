@@ -99,6 +99,39 @@ class FlatGroup:
         self.t = 0
 
 
+class PoetStack:
+    """Every POET-X block of a model in one place.  The packed parameters
+    of all layers form one flat FlatGroup (block order = layer order), so
+    the Cayley-Neumann forward and backward run as ONE batched tensor-core
+    call each per step over all blocks (csrc/cnp_tc.cu) instead of one
+    small call per layer, and each layer's G / dG are views into stacks."""
+
+    def __init__(self, entries, b, device):
+        self.b = b
+        self.pairs = num_pairs(b)
+        self.group = FlatGroup({name: nb * self.pairs for name, nb in entries}, device)
+        self.nb = self.group.numel // self.pairs
+        self.block_off = {name: off // self.pairs for name, (off, _) in self.group.offsets.items()}
+        self.g16 = torch.empty((self.nb, b, b), dtype=torch.bfloat16, device=device)
+        self.qq2 = torch.empty((self.nb, b, 2 * b), dtype=torch.bfloat16, device=device)
+        self.dg = torch.zeros((self.nb, b, b), dtype=torch.float32, device=device)
+        self.device = device
+
+    def blocks(self, buf, name, nb):
+        o = self.block_off[name]
+        return buf[o:o + nb]
+
+    def forward_factors(self):
+        ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(self.nb, self.b), self.device)
+        N.call("poetx_cnp_forward_tc", self.nb, self.b, self.group.param.data_ptr(), self.qq2.data_ptr(),
+               self.g16.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
+
+    def backward_factors(self):
+        ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(self.nb, self.b), self.device)
+        N.call("poetx_cnp_backward_tc", self.nb, self.b, self.qq2.data_ptr(), self.dg.data_ptr(),
+               self.group.grad.data_ptr(), 0, ws, wsb, N.stream_ptr(self.device))
+
+
 # --------------------------------------------------------------------------
 # POET-X linear as an autograd op
 # --------------------------------------------------------------------------
@@ -108,13 +141,11 @@ class _PoetFn(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, mod):
         T = x.shape[0]
-        f = mod.factors()
         z = torch.empty((T, mod.n), dtype=torch.bfloat16, device=x.device)
         saved = torch.empty((T, mod.n), dtype=torch.bfloat16, device=x.device) if mod.variant == "fast" else None
-        d = mod.desc
         ws, wsb = N.workspace(mod.ws_bytes(T), x.device)
-        N.call("poetx_layer_forward", d, f, T, x.data_ptr(), z.data_ptr(), N.ptr(saved), ws, wsb,
-               N.stream_ptr(x.device))
+        N.call("poetx_layer_forward", mod.desc, mod.fstruct, T, x.data_ptr(), z.data_ptr(), N.ptr(saved),
+               ws, wsb, N.stream_ptr(x.device))
         ctx.mod = mod
         ctx.save_for_backward(x, saved) if saved is not None else ctx.save_for_backward(x)
         return z
@@ -129,27 +160,34 @@ class _PoetFn(torch.autograd.Function):
         T = x.shape[0]
         dx = torch.empty_like(x)
         ws, wsb = N.workspace(mod.ws_bytes(T), x.device)
-        N.call("poetx_layer_backward", mod.desc, mod.factors(), T, x.data_ptr(), dz.data_ptr(),
-               N.ptr(t), dx.data_ptr(), mod.grad_r.data_ptr(), mod.grad_p.data_ptr(), 1, ws, wsb,
+        # leaves dG_R / dG_P in the model's dG stack; the CNP backward of all
+        # layers runs afterwards in one batched call (PoetStack.backward_factors)
+        N.call("poetx_layer_backward_dg", mod.desc, mod.fstruct, T, x.data_ptr(), dz.data_ptr(),
+               N.ptr(t), dx.data_ptr(), mod.dg_r.data_ptr(), mod.dg_p.data_ptr(), 0, ws, wsb,
                N.stream_ptr(x.device))
         return dx, None
 
 
 class PoetLinear(torch.nn.Module):
-    """m -> n POET-X projection with bf16 frozen premerged weight and fp32
-    packed parameters living in a FlatGroup."""
+    """m -> n POET-X projection: bf16 frozen premerged weight, fp32 packed
+    parameters and its factor/cotangent blocks living in a PoetStack."""
 
-    def __init__(self, name, m, n, b, group: FlatGroup, rng: Rng, *, variant="fast", neumann_k=3,
+    def __init__(self, name, m, n, stack: PoetStack, rng: Rng, *, variant="fast", neumann_k=3,
                  std=None, device="cuda"):
         super().__init__()
+        b = stack.b
         self.name, self.m, self.n, self.b = name, m, n, b
         self.variant, self.k = variant, neumann_k
         self.device = torch.device(device)
+        self.stack = stack
         nbr, nbp, pairs = m // b, n // b, num_pairs(b)
-        self.packed_r = group.view(group.param, name + ".r", (nbr, pairs))
-        self.packed_p = group.view(group.param, name + ".p", (nbp, pairs))
-        self.grad_r = group.view(group.grad, name + ".r", (nbr, pairs))
-        self.grad_p = group.view(group.grad, name + ".p", (nbp, pairs))
+        grp = stack.group
+        self.packed_r = grp.view(grp.param, name + ".r", (nbr, pairs))
+        self.packed_p = grp.view(grp.param, name + ".p", (nbp, pairs))
+        self.g_r16 = stack.blocks(stack.g16, name + ".r", nbr)
+        self.g_p16 = stack.blocks(stack.g16, name + ".p", nbp)
+        self.dg_r = stack.blocks(stack.dg, name + ".r", nbr)
+        self.dg_p = stack.blocks(stack.dg, name + ".p", nbp)
         # draw order as init_layer (layer.py:335-340): W, then pi_in, then pi_out.
         # Synthetic-weight runs draw W on the device (seeded) instead of host numpy.
         std = (1.0 / math.sqrt(m)) if std is None else std
@@ -159,16 +197,9 @@ class PoetLinear(torch.nn.Module):
         self.perm_out = sample_permutation(n, rng)
         self.premerged = torch.empty((m, n), dtype=torch.bfloat16, device=self.device)
         self._install(w)
-        self.g_r = torch.empty((nbr, b, b), dtype=torch.float32, device=self.device)
-        self.g_p = torch.empty((nbp, b, b), dtype=torch.float32, device=self.device)
-        self.g_r16 = torch.empty((nbr, b, b), dtype=torch.bfloat16, device=self.device)
-        self.g_p16 = torch.empty((nbp, b, b), dtype=torch.bfloat16, device=self.device)
-        self.q2_r = torch.empty((nbr, b, b), dtype=torch.float32, device=self.device) if neumann_k == 3 else None
-        self.q2_p = torch.empty((nbp, b, b), dtype=torch.float32, device=self.device) if neumann_k == 3 else None
-        self._factors = N.LayerFactors(
-            self.packed_r.data_ptr(), self.packed_p.data_ptr(), self.g_r.data_ptr(), self.g_p.data_ptr(),
-            self.g_r16.data_ptr(), self.g_p16.data_ptr(), N.ptr(self.q2_r), N.ptr(self.q2_p))
-        self._fresh = False
+        del w
+        self.fstruct = N.LayerFactors(self.packed_r.data_ptr(), self.packed_p.data_ptr(), None, None,
+                                      self.g_r16.data_ptr(), self.g_p16.data_ptr(), None, None)
         self.merge_count = 0
 
     def _install(self, w: torch.Tensor):
@@ -192,31 +223,27 @@ class PoetLinear(torch.nn.Module):
     def ws_bytes(self, T: int) -> int:
         return int(N.lib().poetx_layer_workspace_bytes(self.desc, T))
 
-    def invalidate(self):
-        self._fresh = False
-
-    def factors(self) -> N.LayerFactors:
-        """CNP of the current packed parameters, computed once per step."""
-        if not self._fresh:
-            ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(N.F32, max(self.m, self.n) // self.b,
-                                                                    self.b, self.k), self.device)
-            N.call("poetx_layer_factors", self.desc, self._factors, ws, wsb, N.stream_ptr(self.device))
-            self._fresh = True
-        return self._factors
-
     def forward(self, x):
         shp = x.shape
         z = _PoetFn.apply(x.reshape(-1, self.m).contiguous(), self)
         return z.view(*shp[:-1], self.n)
 
     def merge_and_reinit(self, rng: Rng):
-        """layer.py:279-314 on the device: fold, resample perms, zero packed."""
-        self.factors()
+        """layer.py:279-314 on the device: fold G_R PM G_P (fp32 factors from the
+        CUDA-core CNP for merge accuracy), resample perms, zero packed in place."""
+        b = self.b
+        g_r = torch.empty((self.m // b, b, b), dtype=torch.float32, device=self.device)
+        g_p = torch.empty((self.n // b, b, b), dtype=torch.float32, device=self.device)
+        f = N.LayerFactors(self.packed_r.data_ptr(), self.packed_p.data_ptr(), g_r.data_ptr(), g_p.data_ptr(),
+                           self.g_r16.data_ptr(), self.g_p16.data_ptr(), None, None)
+        ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(N.F32, max(self.m, self.n) // b, b, self.k),
+                              self.device)
+        N.call("poetx_layer_factors", self.desc, f, ws, wsb, N.stream_ptr(self.device))
         new_in = sample_permutation(self.m, rng)
         new_out = sample_permutation(self.n, rng)
         ws, wsb = N.workspace(N.lib().poetx_merge_workspace_bytes(self.desc), self.device)
         pm_new = torch.empty_like(self.premerged)
-        N.call("poetx_layer_merge", self.desc, self.g_r.data_ptr(), self.g_p.data_ptr(),
+        N.call("poetx_layer_merge", self.desc, g_r.data_ptr(), g_p.data_ptr(),
                new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
                pm_new.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
         self.premerged.copy_(pm_new)
@@ -224,7 +251,6 @@ class PoetLinear(torch.nn.Module):
         self.packed_r.zero_()
         self.packed_p.zero_()
         self._set_desc()
-        self._fresh = False
         self.merge_count += 1
 
 
@@ -247,13 +273,13 @@ class PoetLlama(torch.nn.Module):
         dev = torch.device(device)
         d, f, b = cfg.d, cfg.f, cfg.block
         shapes = {"q": (d, d), "k": (d, d), "v": (d, d), "o": (d, d), "gate": (d, f), "up": (d, f), "down": (f, d)}
-        sizes = {}
+        entries = []
         for i in range(cfg.layers):
             for p in self.PROJ:
                 m, n = shapes[p]
-                sizes[f"{i}.{p}.r"] = (m // b) * num_pairs(b)
-                sizes[f"{i}.{p}.p"] = (n // b) * num_pairs(b)
-        self.poet = FlatGroup(sizes, dev)
+                entries += [(f"{i}.{p}.r", m // b), (f"{i}.{p}.p", n // b)]
+        self.stack = PoetStack(entries, b, dev)
+        self.poet = self.stack.group
         dense_sizes = {"embed": cfg.vocab * d, "head": cfg.vocab * d, "norm_f": d}
         for i in range(cfg.layers):
             dense_sizes[f"{i}.norm1"] = d
@@ -270,7 +296,7 @@ class PoetLlama(torch.nn.Module):
             mods = {}
             for p in self.PROJ:
                 m, n = shapes[p]
-                mods[p] = PoetLinear(f"{i}.{p}", m, n, b, self.poet, Rng.keyed(seed, "init", i, p),
+                mods[p] = PoetLinear(f"{i}.{p}", m, n, self.stack, Rng.keyed(seed, "init", i, p),
                                      variant=cfg.variant, neumann_k=cfg.neumann_k, device=dev)
             self.layers.append(mods)
         hd = cfg.head_dim
@@ -347,12 +373,11 @@ class Trainer:
 
     def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         model = self.model
-        model.poet.grad.zero_()
         model.dense.grad.zero_()
-        for lay in model.poet_layers():
-            lay.invalidate()
+        model.stack.forward_factors()          # CNP of every block, one batched call
         loss = model(tokens, targets)
-        model.backward_dense_grads(loss)
+        model.backward_dense_grads(loss)       # layers leave dG in model.stack.dg
+        model.stack.backward_factors()         # batched CNP backward -> packed grads
         if self.pg is not None:
             import torch.distributed as dist
 

@@ -47,18 +47,15 @@ def gemm():
 
 def layer():
     import paper_2603_05500_b200 as P
-    from paper_2603_05500_b200.trainer import FlatGroup, PoetLinear
+    from paper_2603_05500_b200.trainer import PoetLinear, PoetStack
     print("== POET-X layer (bf16, b=256, T=8192) ==")
     T = 8192
     for m, n in [(2048, 2048), (2048, 5632), (5632, 2048)]:
         b = 256
-        g = FlatGroup({"x.r": (m // b) * b * (b - 1) // 2, "x.p": (n // b) * b * (b - 1) // 2}, "cuda")
-        lay = PoetLinear("x", m, n, b, g, P.Rng(0))
+        st = PoetStack([("x.r", m // b), ("x.p", n // b)], b, torch.device("cuda"))
+        lay = PoetLinear("x", m, n, st, P.Rng(0))
         x = torch.randn((T, m), device="cuda").bfloat16().requires_grad_(True)
         dz = torch.randn((T, n), device="cuda").bfloat16()
-
-        def fact():
-            lay.invalidate(); lay.factors()
 
         def fwd():
             return lay(x)
@@ -66,13 +63,21 @@ def layer():
         def fwdbwd():
             z = lay(x)
             z.backward(dz)
-        t_f = timeit(fact, 5, 1)
+        t_cf = timeit(st.forward_factors, 5, 1)
+        t_cb = timeit(st.backward_factors, 5, 1)
         t_fw = timeit(fwd, 5, 1)
         t_fb = timeit(fwdbwd, 5, 1)
         gemm_ms = 2 * 2.0 * T * m * n / 1.4e15 * 1e3
-        print(f"{m}->{n}: factors {t_f:.3f} ms, fwd {t_fw:.3f} ms, fwd+bwd {t_fb:.3f} ms "
-              f"(2 GEMMs at 1.4 PF would be {gemm_ms:.3f} ms)")
-    N.lib().poetx_prof_enable(0)
+        print(f"{m}->{n}: cnp fwd {t_cf:.3f} ms, cnp bwd {t_cb:.3f} ms, layer fwd {t_fw:.3f} ms, "
+              f"fwd+bwd {t_fb:.3f} ms (2 GEMMs at 1.4 PF would be {gemm_ms:.3f} ms)")
+    print("== model-batched CNP, Llama-1B (3696 blocks of 256) ==")
+    nb, b = 3696, 256
+    st = PoetStack([("all", nb)], b, torch.device("cuda"))
+    st.group.param.normal_(0, 0.01)
+    t_cf = timeit(st.forward_factors, 5, 1)
+    t_cb = timeit(st.backward_factors, 5, 1)
+    fl_f, fl_b = 2 * 3 * nb * b ** 3, 2 * 4 * nb * b ** 3
+    print(f"cnp fwd {t_cf:.3f} ms ({fl_f / t_cf / 1e9:.0f} TF/s), cnp bwd {t_cb:.3f} ms ({fl_b / t_cb / 1e9:.0f} TF/s)")
 
 
 if __name__ == "__main__":
