@@ -374,6 +374,41 @@ __global__ void permute_cols_kernel(int64_t rows, int64_t cols, const int32_t* _
   }
 }
 
+// BF16 feature permutation at HBM speed: each CTA stages whole rows in
+// shared memory with 16-byte coalesced loads, then writes the permuted row
+// with 16-byte coalesced stores, gathering 8 elements per store from smem
+// (the index vector stays L1-resident across rows).
+__global__ void __launch_bounds__(256) permute_cols_bf16_kernel(int64_t rows, int64_t cols,
+                                                              const int32_t* __restrict__ idx,
+                                                              const __nv_bfloat16* __restrict__ x,
+                                                              __nv_bfloat16* __restrict__ y) {
+  extern __shared__ __align__(16) __nv_bfloat16 srow[];
+  const int64_t nv = cols / 8;
+  const __nv_bfloat16* src0 = x;
+  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+    const uint4* src = reinterpret_cast<const uint4*>(src0 + r * cols);
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x)
+      reinterpret_cast<uint4*>(srow)[i] = __ldcs(src + i);
+    __syncthreads();
+    uint4* dst = reinterpret_cast<uint4*>(y + r * cols);
+    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+      const int4 ia = __ldg(reinterpret_cast<const int4*>(idx) + 2 * i);
+      const int4 ib = __ldg(reinterpret_cast<const int4*>(idx) + 2 * i + 1);
+      __nv_bfloat162 p0 = __halves2bfloat162(srow[ia.x], srow[ia.y]);
+      __nv_bfloat162 p1 = __halves2bfloat162(srow[ia.z], srow[ia.w]);
+      __nv_bfloat162 p2 = __halves2bfloat162(srow[ib.x], srow[ib.y]);
+      __nv_bfloat162 p3 = __halves2bfloat162(srow[ib.z], srow[ib.w]);
+      uint4 v;
+      v.x = *reinterpret_cast<uint32_t*>(&p0);
+      v.y = *reinterpret_cast<uint32_t*>(&p1);
+      v.z = *reinterpret_cast<uint32_t*>(&p2);
+      v.w = *reinterpret_cast<uint32_t*>(&p3);
+      __stcs(dst + i, v);
+    }
+    __syncthreads();
+  }
+}
+
 template <typename T>
 __global__ void gather2d_kernel(int64_t rows, int64_t cols, const int32_t* __restrict__ ridx,
                                 const int32_t* __restrict__ cidx, const T* __restrict__ x,
@@ -390,6 +425,25 @@ static int gather2d_t(int64_t rows, int64_t cols, const int32_t* ridx, const int
                       const void* x, void* y, cudaStream_t st) {
   if (rows <= 0 || cols <= 0) return POETX_OK;
   unsigned grid = static_cast<unsigned>(rows < 148 * 16 ? rows : 148 * 16);
+  if constexpr (sizeof(T) == 2) {
+    const size_t smem = static_cast<size_t>(cols) * 2;
+    if (ridx == nullptr && cidx != nullptr && cols % 8 == 0 && smem <= 96 * 1024 &&
+        ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+          reinterpret_cast<uintptr_t>(cidx)) & 15) == 0) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(permute_cols_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             96 * 1024);
+        attr = true;
+      }
+      unsigned g = static_cast<unsigned>(rows < 148 * 8 ? rows : 148 * 8);
+      permute_cols_bf16_kernel<<<g, 256, smem, st>>>(rows, cols, cidx,
+                                                      reinterpret_cast<const __nv_bfloat16*>(x),
+                                                      reinterpret_cast<__nv_bfloat16*>(y));
+      POETX_LAUNCHED("permute_cols_bf16");
+      return POETX_OK;
+    }
+  }
   if (ridx == nullptr && cidx != nullptr) {
     permute_cols_kernel<T><<<grid, 256, 0, st>>>(rows, cols, cidx, static_cast<const T*>(x),
                                                   static_cast<T*>(y));

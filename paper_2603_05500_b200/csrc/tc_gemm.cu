@@ -525,8 +525,9 @@ size_t tc_outer_ws_bytes(int64_t T, int64_t nb, int64_t b) {
 int tc_outer_splits(int64_t T, int64_t nb, int64_t b) {
   int64_t bn = b < 256 ? b : 256;
   int64_t tiles = nb * ((b + 127) / 128) * ((b + bn - 1) / bn);
-  int64_t want = (2 * 148 + tiles - 1) / tiles;
-  int64_t maxs = (T + 255) / 256;
+  // one wave of persistent CTAs: fewer fp32 partials to write and reduce
+  int64_t want = 148 / tiles;
+  int64_t maxs = (T + 511) / 512;
   if (want > maxs) want = maxs;
   if (want < 1) want = 1;
   if (want > 64) want = 64;
