@@ -378,20 +378,50 @@ __global__ void permute_cols_kernel(int64_t rows, int64_t cols, const int32_t* _
 // shared memory with 16-byte coalesced loads, then writes the permuted row
 // with 16-byte coalesced stores, gathering 8 elements per store from smem
 // (the index vector stays L1-resident across rows).
-__global__ void __launch_bounds__(256) permute_cols_bf16_kernel(int64_t rows, int64_t cols,
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// rows are processed in chunks of R rows; chunk i+1 streams into the other
+// smem buffer (cp.async) while chunk i is gathered and written
+__global__ void __launch_bounds__(256) permute_cols_bf16_kernel(int64_t rows, int64_t cols, int R,
                                                               const int32_t* __restrict__ idx,
                                                               const __nv_bfloat16* __restrict__ x,
                                                               __nv_bfloat16* __restrict__ y) {
-  extern __shared__ __align__(16) __nv_bfloat16 srow[];
+  extern __shared__ __align__(16) __nv_bfloat16 sbuf[];
   const int64_t nv = cols / 8;
-  const __nv_bfloat16* src0 = x;
-  for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
-    const uint4* src = reinterpret_cast<const uint4*>(src0 + r * cols);
-    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x)
-      reinterpret_cast<uint4*>(srow)[i] = __ldcs(src + i);
+  const int64_t chunk_elems = static_cast<int64_t>(R) * cols;
+  const int64_t nchunks = (rows + R - 1) / R;
+  auto issue = [&](int64_t c, int buf) {
+    if (c < nchunks) {
+      const int64_t r0 = c * R;
+      const int64_t nr = rows - r0 < R ? rows - r0 : R;
+      const uint4* src = reinterpret_cast<const uint4*>(x + r0 * cols);
+      uint4* dst = reinterpret_cast<uint4*>(sbuf + buf * chunk_elems);
+      for (int64_t i = threadIdx.x; i < nr * nv; i += blockDim.x) cp_async16(dst + i, src + i);
+    }
+    cp_async_commit();
+  };
+  int buf = 0;
+  issue(blockIdx.x, 0);
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+    issue(c + gridDim.x, buf ^ 1);
+    cp_async_wait<1>();
     __syncthreads();
-    uint4* dst = reinterpret_cast<uint4*>(y + r * cols);
-    for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) {
+    const __nv_bfloat16* srow0 = sbuf + buf * chunk_elems;
+    const int64_t r0 = c * R;
+    const int64_t nr = rows - r0 < R ? rows - r0 : R;
+    for (int64_t e = threadIdx.x; e < nr * nv; e += blockDim.x) {
+      const int64_t rr = e / nv, i = e % nv;
+      const __nv_bfloat16* srow = srow0 + rr * cols;
       const int4 ia = __ldg(reinterpret_cast<const int4*>(idx) + 2 * i);
       const int4 ib = __ldg(reinterpret_cast<const int4*>(idx) + 2 * i + 1);
       __nv_bfloat162 p0 = __halves2bfloat162(srow[ia.x], srow[ia.y]);
@@ -403,10 +433,12 @@ __global__ void __launch_bounds__(256) permute_cols_bf16_kernel(int64_t rows, in
       v.y = *reinterpret_cast<uint32_t*>(&p1);
       v.z = *reinterpret_cast<uint32_t*>(&p2);
       v.w = *reinterpret_cast<uint32_t*>(&p3);
-      __stcs(dst + i, v);
+      __stcs(reinterpret_cast<uint4*>(y + (r0 + rr) * cols) + i, v);
     }
     __syncthreads();
+    buf ^= 1;
   }
+  cp_async_wait<0>();
 }
 
 template <typename T>
@@ -426,18 +458,22 @@ static int gather2d_t(int64_t rows, int64_t cols, const int32_t* ridx, const int
   if (rows <= 0 || cols <= 0) return POETX_OK;
   unsigned grid = static_cast<unsigned>(rows < 148 * 16 ? rows : 148 * 16);
   if constexpr (sizeof(T) == 2) {
-    const size_t smem = static_cast<size_t>(cols) * 2;
-    if (ridx == nullptr && cidx != nullptr && cols % 8 == 0 && smem <= 96 * 1024 &&
+    // chunk of R rows ~ 12 KB, two buffers per CTA
+    int R = static_cast<int>((12 * 1024) / (cols * 2));
+    if (R < 1) R = 1;
+    const size_t smem = 2 * static_cast<size_t>(R) * cols * 2;
+    if (ridx == nullptr && cidx != nullptr && cols % 8 == 0 && smem <= 100 * 1024 &&
         ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
           reinterpret_cast<uintptr_t>(cidx)) & 15) == 0) {
       static bool attr = false;
       if (!attr) {
         cudaFuncSetAttribute(permute_cols_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             96 * 1024);
+                             100 * 1024);
         attr = true;
       }
-      unsigned g = static_cast<unsigned>(rows < 148 * 8 ? rows : 148 * 8);
-      permute_cols_bf16_kernel<<<g, 256, smem, st>>>(rows, cols, cidx,
+      int64_t chunks = (rows + R - 1) / R;
+      unsigned g = static_cast<unsigned>(chunks < 148 * 6 ? chunks : 148 * 6);
+      permute_cols_bf16_kernel<<<g, 256, smem, st>>>(rows, cols, R, cidx,
                                                       reinterpret_cast<const __nv_bfloat16*>(x),
                                                       reinterpret_cast<__nv_bfloat16*>(y));
       POETX_LAUNCHED("permute_cols_bf16");

@@ -80,9 +80,32 @@ def layer():
     print(f"cnp fwd {t_cf:.3f} ms ({fl_f / t_cf / 1e9:.0f} TF/s), cnp bwd {t_cb:.3f} ms ({fl_b / t_cb / 1e9:.0f} TF/s)")
 
 
+def hbm():
+    import paper_2603_05500_b200 as P
+    print("== HBM-bound kernels (bf16, T=8192) ==")
+    T = 8192
+    for cols in (2048, 5632):
+        x = torch.randn((T, cols), device="cuda").bfloat16()
+        pm = P.sample_permutation(cols, P.Rng(1))
+        ms = timeit(lambda: P.permute_features(x, pm, "inverse"))
+        print(f"permute T x {cols}: {ms * 1e3:.1f} us  {2 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
+        for b in (256, 64):
+            G = P.BlockDiagonalFactor((0.1 * torch.randn((cols // b, b, b), device="cuda")).bfloat16())
+            for tr in (False, True):
+                ms = timeit(lambda: P.apply_to_features(G, x, transpose=tr))
+                print(f"apply b={b} T x {cols} transpose={tr}: {ms * 1e3:.1f} us  "
+                      f"{2 * x.numel() * 2 / ms / 1e6:.0f} GB/s  {2 * x.numel() * b / ms / 1e9:.0f} TF/s")
+            y = torch.randn_like(x)
+            ms = timeit(lambda: P.segmented_outer(x, y, b))
+            print(f"segmented_outer b={b} T x {cols}: {ms * 1e3:.1f} us  {2 * x.numel() * 2 / ms / 1e6:.0f} GB/s "
+                  f"{2 * x.numel() * b / ms / 1e9:.0f} TF/s")
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("gemm", "all"):
         gemm()
+    if what in ("hbm", "all"):
+        hbm()
     if what in ("layer", "all"):
         layer()
