@@ -350,6 +350,28 @@ class PoetLlama(torch.nn.Module):
             self.dense.view(self.dense.grad, name, g.shape).add_(g)
 
 
+def average_gradients(buffers, group) -> None:
+    """Token-batch data parallelism: average flat gradient buffers over the
+    ranks of ``group`` (one collective per buffer; NCCL AVG over NVLink, or
+    SUM then scale on backends without AVG, e.g. gloo)."""
+    import torch.distributed as dist
+
+    backend = dist.get_backend(group)
+    for buf in buffers:
+        if backend == "nccl":
+            dist.all_reduce(buf, op=dist.ReduceOp.AVG, group=group)
+        else:
+            dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group)
+            buf.div_(dist.get_world_size(group))
+
+
+def merge_rngs(seed: int, step: int, n_layers: int):
+    """Per-layer merge streams Rng.keyed(seed, "merge", step, idx)
+    (runner.py:304-307): identical on every rank, so merges need no
+    communication."""
+    return [Rng.keyed(seed, "merge", step, idx) for idx in range(n_layers)]
+
+
 class Trainer:
     """One training step = forward, backward, (all-reduce), clip+AdamW, merge."""
 
@@ -379,10 +401,7 @@ class Trainer:
         model.backward_dense_grads(loss)       # layers leave dG in model.stack.dg
         model.stack.backward_factors()         # batched CNP backward -> packed grads
         if self.pg is not None:
-            import torch.distributed as dist
-
-            dist.all_reduce(model.poet.grad, op=dist.ReduceOp.AVG, group=self.pg)
-            dist.all_reduce(model.dense.grad, op=dist.ReduceOp.AVG, group=self.pg)
+            average_gradients([model.poet.grad, model.dense.grad], self.pg)
         s = self.sched
         thr = clip_threshold_at(self.step_idx, self.since_merge, s)
         model.poet.t += 1
@@ -401,7 +420,8 @@ class Trainer:
         return loss.detach()
 
     def merge(self):
-        for idx, lay in enumerate(self.model.poet_layers()):
-            lay.merge_and_reinit(Rng.keyed(self.seed, "merge", self.step_idx, idx))
+        layers = self.model.poet_layers()
+        for lay, rng in zip(layers, merge_rngs(self.seed, self.step_idx, len(layers))):
+            lay.merge_and_reinit(rng)
         self.model.poet.reset_moments()
         self.since_merge = 0
