@@ -44,6 +44,8 @@ int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int t
 
 // y_s = x_s g[s] (or g[s]^T) for every length-b segment s; BF16.
 int tc_blockdiag(const GemmDesc& d, cudaStream_t st);
+int tc_blockdiag_apply(int64_t T, int64_t nb, int64_t b, const void* g, int transpose,
+                       const void* x, void* y, cudaStream_t st);
 
 // split-K factor used by the tensor-core segmented outer product
 int tc_outer_splits(int64_t T, int64_t nb, int64_t b);
