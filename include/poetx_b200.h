@@ -45,6 +45,15 @@ enum {
 };
 /* layer variants (layer.py:68) */
 enum { POETX_FAST = 0, POETX_MEM = 1 };
+/* layer boundary flags: let the caller own a permutation so it can be fused
+ * into a neighbouring kernel (norm, RoPE, SwiGLU, residual add).  Semantics
+ * are unchanged: u = x[:, pi_in], z = v[:, pi_out^-1] (permute.py:95-110). */
+enum {
+  POETX_IN_GATHERED = 1,     /* x passed is already u = x[:, pi_in] */
+  POETX_OUT_UNSCATTERED = 2, /* forward writes v; caller applies z = v[:, pi_out^-1] */
+  POETX_DZ_GATHERED = 4,     /* dz passed is already dv = dz[:, pi_out] */
+  POETX_DX_UNSCATTERED = 8   /* backward writes du; caller applies dx = du[:, pi_in^-1] */
+};
 
 const char* poetx_last_error(void);
 int poetx_abi_version(void);
@@ -200,6 +209,10 @@ int poetx_layer_factors(const poetx_layer_desc* d, poetx_layer_factors_t* f, voi
 int poetx_layer_forward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
                         const void* x, void* z, void* saved_t, void* ws, size_t ws_bytes,
                         void* stream);
+/* forward with boundary flags (POETX_IN_GATHERED, POETX_OUT_UNSCATTERED) */
+int poetx_layer_forward_ex(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                           const void* x, void* z, void* saved_t, int flags, void* ws,
+                           size_t ws_bytes, void* stream);
 /* grads: dx[T,m] (may be NULL), packed grads (param type; accumulate != 0
  * adds into them).  saved_t NULL => recompute (mem variant). */
 int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
@@ -209,11 +222,12 @@ int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t*
 /* Same chain, but instead of running the CNP backward per layer it leaves
  * the block-factor cotangents dG_R [m/b,b,b], dG_P [n/b,b,b] (fp32; F64 for
  * F64 layers) in caller buffers (accumulate != 0 adds) so one batched
- * poetx_cnp_backward_tc can serve every layer of a model. */
+ * poetx_cnp_backward_tc can serve every layer of a model.  flags:
+ * POETX_IN_GATHERED (x is u), POETX_DZ_GATHERED, POETX_DX_UNSCATTERED. */
 int poetx_layer_backward_dg(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
                             const void* x, const void* dz, const void* saved_t, void* dx,
-                            void* dg_r, void* dg_p, int accumulate, void* ws, size_t ws_bytes,
-                            void* stream);
+                            void* dg_r, void* dg_p, int accumulate, int flags, void* ws,
+                            size_t ws_bytes, void* stream);
 /* merge_and_reinit numerics (layer.py:260-314): new premerged
  * PM'[i,j] = M[inv_in(new_in(i)), inv_out(new_out(j))] with
  * M = blockdiag(G_R) PM blockdiag(G_P) computed in fp32/fp64 from the
@@ -223,6 +237,39 @@ int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_
                       const int32_t* new_in_fwd, const int32_t* new_out_fwd,
                       void* premerged_out, void* w_out, void* ws, size_t ws_bytes,
                       void* stream);
+
+/* ------------------------------------------------ fused neighbour kernels --
+ * BF16 row-staged kernels that apply the layer permutations inside the
+ * elementwise ops a decoder block needs anyway (used with the
+ * POETX_IN_GATHERED / POETX_OUT_UNSCATTERED layer flags).  All index
+ * arrays are DEVICE int32; rows are [T, dim] row-major, dim % 8 == 0.   */
+/* y = rmsnorm(x) * w (fp32 math), out[k] = y[:, idx[k]] for k < K <= 3;
+ * rstd[T] (fp32) saved for the backward */
+int poetx_rmsnorm_gather(int64_t T, int64_t d, const void* x, const float* w, float eps, int K,
+                         const int32_t* const* idx, void* const* out, float* rstd, void* stream);
+size_t poetx_rmsnorm_gather_bwd_workspace_bytes(int64_t T, int64_t d);
+/* dy = sum_k du[k][:, inv[k]]; dx = RMSNorm backward; dw (+)= sum_t dy x rstd
+ * (deterministic per-CTA partials) */
+int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w, const float* rstd,
+                             int K, const int32_t* const* inv, const void* const* du, void* dx,
+                             float* dw, int accumulate_dw, void* ws, size_t ws_bytes, void* stream);
+/* out[:, j] = silu(vg[:, cg[j]]) * vu[:, cu[j]] */
+int poetx_swiglu_gather(int64_t T, int64_t f, const void* vg, const void* vu, const int32_t* cg,
+                        const int32_t* cu, void* out, void* stream);
+/* dvg[:, j] = du[:, A[j]] silu'(vg[:, j]) vu[:, B[j]];  dvu[:, j] = du[:, C[j]] silu(vg[:, D[j]]) */
+int poetx_swiglu_gather_bwd(int64_t T, int64_t f, const void* vg, const void* vu, const void* du,
+                            const int32_t* A, const int32_t* B, const int32_t* C, const int32_t* D,
+                            void* dvg, void* dvu, void* stream);
+/* out = RoPE(v[:, inv]) per head (pairs c, c + hd/2; position t % S) */
+int poetx_rope_scatter(int64_t T, int64_t S, int64_t H, int64_t hd, const void* v,
+                       const int32_t* inv, const float* cosb, const float* sinb, void* out,
+                       void* stream);
+int poetx_rope_scatter_bwd(int64_t T, int64_t S, int64_t H, int64_t hd, const void* dout,
+                           const int32_t* fwd, const float* cosb, const float* sinb, void* dv,
+                           void* stream);
+/* out = h + v[:, inv]  (residual add with the output scatter) */
+int poetx_scatter_add(int64_t T, int64_t d, const void* h, const void* v, const int32_t* inv,
+                      void* out, void* stream);
 
 /* ------------------------------------------------------------ optimizer --
  * optim.py.  Multi-tensor: host arrays of device pointers.               */

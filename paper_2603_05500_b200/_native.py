@@ -20,6 +20,7 @@ LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpoetx_b2
 
 F32, F64, BF16 = 0, 1, 2
 FAST, MEM = 0, 1
+IN_GATHERED, OUT_UNSCATTERED, DZ_GATHERED, DX_UNSCATTERED = 1, 2, 4, 8
 _CODES = {1: ShapeError, 2: ConfigError, 3: StateError, 4: NumericsError, 5: PoetxError}
 
 VP = C.c_void_p
@@ -89,7 +90,17 @@ _SIGS = {
     "poetx_cnp_forward_tc": (I32, [I64, I64, VP, VP, VP, VP, VP, SZ, VP]),
     "poetx_cnp_backward_tc": (I32, [I64, I64, VP, VP, VP, I32, VP, SZ, VP]),
     "poetx_layer_backward_dg": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I64, VP, VP, VP,
-                                      VP, VP, VP, I32, VP, SZ, VP]),
+                                      VP, VP, VP, I32, I32, VP, SZ, VP]),
+    "poetx_layer_forward_ex": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I64, VP, VP, VP,
+                                     I32, VP, SZ, VP]),
+    "poetx_rmsnorm_gather": (I32, [I64, I64, VP, VP, C.c_float, I32, VP, VP, VP, VP]),
+    "poetx_rmsnorm_gather_bwd_workspace_bytes": (SZ, [I64, I64]),
+    "poetx_rmsnorm_gather_bwd": (I32, [I64, I64, VP, VP, VP, I32, VP, VP, VP, VP, I32, VP, SZ, VP]),
+    "poetx_swiglu_gather": (I32, [I64, I64, VP, VP, VP, VP, VP, VP]),
+    "poetx_swiglu_gather_bwd": (I32, [I64, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP]),
+    "poetx_rope_scatter": (I32, [I64, I64, I64, I64, VP, VP, VP, VP, VP, VP]),
+    "poetx_rope_scatter_bwd": (I32, [I64, I64, I64, I64, VP, VP, VP, VP, VP, VP]),
+    "poetx_scatter_add": (I32, [I64, I64, VP, VP, VP, VP, VP]),
     "poetx_orthogonality_error": (I32, [I32, I64, I64, VP, VP, VP, SZ, VP]),
     "poetx_permute_cols": (I32, [I32, I64, I64, VP, VP, VP, VP]),
     "poetx_permute_rows": (I32, [I32, I64, I64, VP, VP, VP, VP]),

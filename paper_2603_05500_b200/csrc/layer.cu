@@ -132,9 +132,9 @@ int poetx_layer_factors(const poetx_layer_desc* d, poetx_layer_factors_t* f, voi
   return POETX_OK;
 }
 
-int poetx_layer_forward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
-                        const void* x, void* z, void* saved_t, void* ws, size_t ws_bytes,
-                        void* stream) {
+int poetx_layer_forward_ex(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                           const void* x, void* z, void* saved_t, int flags, void* ws,
+                           size_t ws_bytes, void* stream) {
   POETX_TRY(check_desc(d));
   POETX_REQUIRE(T >= 0 && x && z && f, POETX_ESHAPE, "layer_forward: bad arguments");
   if (T == 0) return POETX_OK;
@@ -142,29 +142,41 @@ int poetx_layer_forward(const poetx_layer_desc* d, const poetx_layer_factors_t* 
   const int dt = d->dtype;
   const int64_t w = d->m > d->n ? d->m : d->n;
   const size_t e = elt_size(dt);
+  const bool in_gathered = flags & POETX_IN_GATHERED, out_raw = flags & POETX_OUT_UNSCATTERED;
   Workspace wsp(ws, ws_bytes);
   void* b1 = wsp.take_bytes(T * w * e);
   void* b2 = wsp.take_bytes(T * w * e);
   void* b3 = wsp.take_bytes(T * w * e);
   POETX_REQUIRE(b1 && b2 && b3, POETX_ESHAPE, "layer_forward: workspace too small");
   void* t = saved_t ? saved_t : b3;
-  // u = x[:, pi_in]  (permute_features 'inverse', layer.py:220)
-  POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b1, st));
+  // u = x[:, pi_in]  (permute_features 'inverse', layer.py:220) -- or supplied
+  const void* u = x;
+  if (!in_gathered) {
+    POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b1, st));
+    u = b1;
+  }
   // a = u blockdiag(G_R)  (mm1, layer.py:221)
-  POETX_TRY(apply_features(dt, T, d->m / d->b, d->b, act_g(d, f->g_r, f->g_r_lowp), 0, b1, b2, st));
+  POETX_TRY(apply_features(dt, T, d->m / d->b, d->b, act_g(d, f->g_r, f->g_r_lowp), 0, u, b2, st));
   // t = a PM  (mm2, layer.py:222)
   POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b2, d->m, 0, d->premerged, d->n, 0, t, d->n, 0, stream));
   // v = t blockdiag(G_P)  (mm3, layer.py:223)
-  POETX_TRY(apply_features(dt, T, d->n / d->b, d->b, act_g(d, f->g_p, f->g_p_lowp), 0, t, b1, st));
-  // z = v[:, pi_out^-1]  (permute_features 'forward', layer.py:224)
-  POETX_TRY(gather2d(dt, T, d->n, nullptr, d->perm_out_inv, b1, z, st));
+  void* v = out_raw ? z : b1;
+  POETX_TRY(apply_features(dt, T, d->n / d->b, d->b, act_g(d, f->g_p, f->g_p_lowp), 0, t, v, st));
+  // z = v[:, pi_out^-1]  (permute_features 'forward', layer.py:224) -- or left to the caller
+  if (!out_raw) POETX_TRY(gather2d(dt, T, d->n, nullptr, d->perm_out_inv, b1, z, st));
   return POETX_OK;
+}
+
+int poetx_layer_forward(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
+                        const void* x, void* z, void* saved_t, void* ws, size_t ws_bytes,
+                        void* stream) {
+  return poetx_layer_forward_ex(d, f, T, x, z, saved_t, 0, ws, ws_bytes, stream);
 }
 
 static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_factors_t* f,
                                int64_t T, const void* x, const void* dz, const void* saved_t,
                                void* dx, void* dpacked_r, void* dpacked_p, void* dg_r_out,
-                               void* dg_p_out, int accumulate, void* ws, size_t ws_bytes,
+                               void* dg_p_out, int accumulate, int flags, void* ws, size_t ws_bytes,
                                void* stream) {
   cudaStream_t st = as_stream(stream);
   const int dt = d->dtype, pdt = param_dtype(dt);
@@ -184,31 +196,49 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   Workspace tail(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
   const void* gr = act_g(d, f->g_r, f->g_r_lowp);
   const void* gp = act_g(d, f->g_p, f->g_p_lowp);
-  // dv = dz[:, pi_out]  (layer.py:238)
-  POETX_TRY(gather2d(dt, T, d->n, nullptr, d->perm_out_fwd, dz, b1, st));
+  const bool in_gathered = flags & POETX_IN_GATHERED, dz_gathered = flags & POETX_DZ_GATHERED;
+  const bool dx_raw = flags & POETX_DX_UNSCATTERED;
+  // dv = dz[:, pi_out]  (layer.py:238) -- or supplied
+  const void* dv = dz;
+  if (!dz_gathered) {
+    POETX_TRY(gather2d(dt, T, d->n, nullptr, d->perm_out_fwd, dz, b1, st));
+    dv = b1;
+  }
   const void* t = saved_t;
   if (!t) {
     // mem variant: recompute u, a, t with the forward's kernels (bitwise equal)
-    POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b2, st));
-    POETX_TRY(apply_features(dt, T, nbr, b, gr, 0, b2, b3, st));
+    const void* u0 = x;
+    if (!in_gathered) {
+      POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b2, st));
+      u0 = b2;
+    }
+    POETX_TRY(apply_features(dt, T, nbr, b, gr, 0, u0, b3, st));
     POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b3, d->m, 0, d->premerged, d->n, 0, b4, d->n, 0, stream));
     t = b4;
   }
   // dG_P = segmented_outer(t, dv)  (layer.py:247)
-  POETX_TRY(segmented_outer(dt, T, nbp, b, t, b1, dgp, dg_acc, tail, st));
+  POETX_TRY(segmented_outer(dt, T, nbp, b, t, dv, dgp, dg_acc, tail, st));
   // dt = dv blockdiag(G_P)^T  (layer.py:248)
-  POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, b1, b2, st));
+  POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, dv, b2, st));
   // da = dt PM^T  (layer.py:249)
   POETX_TRY(poetx_matmul(dt, T, d->m, d->n, b2, d->n, 0, d->premerged, d->n, 1, b3, d->m, 0, stream));
-  // u = x[:, pi_in]  (layer.py:250)
-  POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b1, st));
+  // u = x[:, pi_in]  (layer.py:250) -- or the supplied pre-gathered input
+  const void* u = x;
+  if (!in_gathered) {
+    POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_fwd, x, b1, st));
+    u = b1;
+  }
   // dG_R = segmented_outer(u, da)  (layer.py:251)
   Workspace tail2(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
-  POETX_TRY(segmented_outer(dt, T, nbr, b, b1, b3, dgr, dg_acc, tail2, st));
+  POETX_TRY(segmented_outer(dt, T, nbr, b, u, b3, dgr, dg_acc, tail2, st));
   if (dx) {
     // du = da blockdiag(G_R)^T ; dx = du[:, pi_in^-1]  (layer.py:252-253)
-    POETX_TRY(apply_features(dt, T, nbr, b, gr, 1, b3, b2, st));
-    POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_inv, b2, dx, st));
+    if (dx_raw) {
+      POETX_TRY(apply_features(dt, T, nbr, b, gr, 1, b3, dx, st));
+    } else {
+      POETX_TRY(apply_features(dt, T, nbr, b, gr, 1, b3, b2, st));
+      POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_inv, b2, dx, st));
+    }
   }
   if (dg_mode) return POETX_OK;
   // packed grads = P(cnp_backward(.))  (layer.py:254-255)
@@ -230,18 +260,18 @@ int poetx_layer_backward(const poetx_layer_desc* d, const poetx_layer_factors_t*
   POETX_REQUIRE(T >= 0 && x && dz && f && dpacked_r && dpacked_p, POETX_ESHAPE,
                 "layer_backward: bad arguments");
   return layer_backward_impl(d, f, T, x, dz, saved_t, dx, dpacked_r, dpacked_p, nullptr, nullptr,
-                             accumulate, ws, ws_bytes, stream);
+                             accumulate, 0, ws, ws_bytes, stream);
 }
 
 int poetx_layer_backward_dg(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int64_t T,
                             const void* x, const void* dz, const void* saved_t, void* dx,
-                            void* dg_r, void* dg_p, int accumulate, void* ws, size_t ws_bytes,
-                            void* stream) {
+                            void* dg_r, void* dg_p, int accumulate, int flags, void* ws,
+                            size_t ws_bytes, void* stream) {
   POETX_TRY(check_desc(d));
   POETX_REQUIRE(T >= 0 && x && dz && f && dg_r && dg_p, POETX_ESHAPE,
                 "layer_backward_dg: bad arguments");
   return layer_backward_impl(d, f, T, x, dz, saved_t, dx, nullptr, nullptr, dg_r, dg_p,
-                             accumulate, ws, ws_bytes, stream);
+                             accumulate, flags, ws, ws_bytes, stream);
 }
 
 size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d) {

@@ -163,7 +163,7 @@ class _PoetFn(torch.autograd.Function):
         # leaves dG_R / dG_P in the model's dG stack; the CNP backward of all
         # layers runs afterwards in one batched call (PoetStack.backward_factors)
         N.call("poetx_layer_backward_dg", mod.desc, mod.fstruct, T, x.data_ptr(), dz.data_ptr(),
-               N.ptr(t), dx.data_ptr(), mod.dg_r.data_ptr(), mod.dg_p.data_ptr(), 0, ws, wsb,
+               N.ptr(t), dx.data_ptr(), mod.dg_r.data_ptr(), mod.dg_p.data_ptr(), 0, 0, ws, wsb,
                N.stream_ptr(x.device))
         return dx, None
 
@@ -255,6 +255,160 @@ class PoetLinear(torch.nn.Module):
 
 
 # --------------------------------------------------------------------------
+# fused path: the layer core u -> v, permutations owned by neighbour kernels
+# --------------------------------------------------------------------------
+
+
+class _PoetRawFn(torch.autograd.Function):
+    """POET-X layer core with the caller owning both permutations:
+    u = x[:, pi_in] in, v (before the pi_out scatter) out (csrc/layer.cu flags)."""
+
+    @staticmethod
+    def forward(ctx, u, mod):
+        T = u.shape[0]
+        v = torch.empty((T, mod.n), dtype=torch.bfloat16, device=u.device)
+        saved = torch.empty((T, mod.n), dtype=torch.bfloat16, device=u.device) if mod.variant == "fast" else None
+        ws, wsb = N.workspace(mod.ws_bytes(T), u.device)
+        N.call("poetx_layer_forward_ex", mod.desc, mod.fstruct, T, u.data_ptr(), v.data_ptr(), N.ptr(saved),
+               N.IN_GATHERED | N.OUT_UNSCATTERED, ws, wsb, N.stream_ptr(u.device))
+        ctx.mod = mod
+        ctx.save_for_backward(u, saved) if saved is not None else ctx.save_for_backward(u)
+        return v
+
+    @staticmethod
+    def backward(ctx, dv):
+        mod = ctx.mod
+        saved = ctx.saved_tensors
+        u = saved[0]
+        t = saved[1] if len(saved) > 1 else None
+        dv = dv.contiguous()
+        T = u.shape[0]
+        du = torch.empty_like(u)
+        ws, wsb = N.workspace(mod.ws_bytes(T), u.device)
+        N.call("poetx_layer_backward_dg", mod.desc, mod.fstruct, T, u.data_ptr(), dv.data_ptr(), N.ptr(t),
+               du.data_ptr(), mod.dg_r.data_ptr(), mod.dg_p.data_ptr(), 0,
+               N.IN_GATHERED | N.DZ_GATHERED | N.DX_UNSCATTERED, ws, wsb, N.stream_ptr(u.device))
+        return du, None
+
+
+def _ptrs(ts):
+    import ctypes as C
+    return (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
+
+
+class _RMSNormGather(torch.autograd.Function):
+    """y = rmsnorm(h) * w, then u_k = y[:, pi_in_k] for each consumer."""
+
+    @staticmethod
+    def forward(ctx, h, w, fwds, invs):
+        T, d = h.shape
+        outs = [torch.empty_like(h) for _ in fwds]
+        rstd = torch.empty(T, dtype=torch.float32, device=h.device)
+        N.call("poetx_rmsnorm_gather", T, d, h.data_ptr(), w.data_ptr(), 1e-6, len(fwds), _ptrs(fwds),
+               _ptrs(outs), rstd.data_ptr(), N.stream_ptr(h.device))
+        ctx.invs = invs
+        ctx.save_for_backward(h, w, rstd)
+        return tuple(outs)
+
+    @staticmethod
+    def backward(ctx, *dus):
+        h, w, rstd = ctx.saved_tensors
+        T, d = h.shape
+        dus = [g.contiguous() for g in dus]
+        dx = torch.empty_like(h)
+        dw = torch.empty_like(w)
+        ws, wsb = N.workspace(N.lib().poetx_rmsnorm_gather_bwd_workspace_bytes(T, d), h.device)
+        N.call("poetx_rmsnorm_gather_bwd", T, d, h.data_ptr(), w.data_ptr(), rstd.data_ptr(), len(dus),
+               _ptrs(ctx.invs), _ptrs(dus), dx.data_ptr(), dw.data_ptr(), 0, ws, wsb, N.stream_ptr(h.device))
+        return dx, dw, None, None
+
+
+class _SwiGLUGather(torch.autograd.Function):
+    """u_down = silu(z_gate) * z_up gathered for the down projection in one pass:
+    u_down[:, j] = silu(v_g[:, cg[j]]) * v_u[:, cu[j]]."""
+
+    @staticmethod
+    def forward(ctx, vg, vu, maps):
+        T, f = vg.shape
+        out = torch.empty_like(vg)
+        N.call("poetx_swiglu_gather", T, f, vg.data_ptr(), vu.data_ptr(), maps["cg"].data_ptr(),
+               maps["cu"].data_ptr(), out.data_ptr(), N.stream_ptr(vg.device))
+        ctx.maps = maps
+        ctx.save_for_backward(vg, vu)
+        return out
+
+    @staticmethod
+    def backward(ctx, du):
+        vg, vu = ctx.saved_tensors
+        T, f = vg.shape
+        m = ctx.maps
+        dvg, dvu = torch.empty_like(vg), torch.empty_like(vu)
+        N.call("poetx_swiglu_gather_bwd", T, f, vg.data_ptr(), vu.data_ptr(), du.contiguous().data_ptr(),
+               m["A"].data_ptr(), m["B"].data_ptr(), m["C"].data_ptr(), m["D"].data_ptr(),
+               dvg.data_ptr(), dvu.data_ptr(), N.stream_ptr(vg.device))
+        return dvg, dvu, None
+
+
+class _RopeScatter(torch.autograd.Function):
+    """q = RoPE(v[:, pi_out^-1]) with the scatter fused (rope on [T, H, hd])."""
+
+    @staticmethod
+    def forward(ctx, v, inv, fwd, cos, sin, S, H, hd):
+        T = v.shape[0]
+        out = torch.empty_like(v)
+        N.call("poetx_rope_scatter", T, S, H, hd, v.data_ptr(), inv.data_ptr(), cos.data_ptr(),
+               sin.data_ptr(), out.data_ptr(), N.stream_ptr(v.device))
+        ctx.args = (fwd, cos, sin, S, H, hd)
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        fwd, cos, sin, S, H, hd = ctx.args
+        dout = dout.contiguous()
+        dv = torch.empty_like(dout)
+        N.call("poetx_rope_scatter_bwd", dout.shape[0], S, H, hd, dout.data_ptr(), fwd.data_ptr(),
+               cos.data_ptr(), sin.data_ptr(), dv.data_ptr(), N.stream_ptr(dout.device))
+        return dv, None, None, None, None, None, None, None
+
+
+def _permute_cols(x, idx):
+    y = torch.empty_like(x)
+    N.call("poetx_permute_cols", N.BF16, x.shape[0], x.shape[1], idx.data_ptr(), x.data_ptr(), y.data_ptr(),
+           N.stream_ptr(x.device))
+    return y
+
+
+class _ScatterAdd(torch.autograd.Function):
+    """h + v[:, pi_out^-1] (residual add with the output scatter fused)."""
+
+    @staticmethod
+    def forward(ctx, h, v, inv, fwd):
+        out = torch.empty_like(h)
+        N.call("poetx_scatter_add", h.shape[0], h.shape[1], h.data_ptr(), v.data_ptr(), inv.data_ptr(),
+               out.data_ptr(), N.stream_ptr(h.device))
+        ctx.fwd = fwd
+        return out
+
+    @staticmethod
+    def backward(ctx, dout):
+        dout = dout.contiguous()
+        return dout, _permute_cols(dout, ctx.fwd), None, None
+
+
+class _Permute(torch.autograd.Function):
+    """y = x[:, idx] ; dx = dy[:, inv]  (permute_features on [T, dim])."""
+
+    @staticmethod
+    def forward(ctx, x, idx, inv):
+        ctx.inv = inv
+        return _permute_cols(x.contiguous(), idx)
+
+    @staticmethod
+    def backward(ctx, dy):
+        return _permute_cols(dy.contiguous(), ctx.inv), None, None
+
+
+# --------------------------------------------------------------------------
 # Llama
 # --------------------------------------------------------------------------
 
@@ -267,7 +421,7 @@ def _rope(x, cos, sin):
 class PoetLlama(torch.nn.Module):
     PROJ = ("q", "k", "v", "o", "gate", "up", "down")
 
-    def __init__(self, cfg: LlamaConfig, seed: int = 0, device="cuda"):
+    def __init__(self, cfg: LlamaConfig, seed: int = 0, device="cuda", fused: bool = True):
         super().__init__()
         self.cfg = cfg
         dev = torch.device(device)
@@ -304,6 +458,22 @@ class PoetLlama(torch.nn.Module):
         ang = torch.outer(torch.arange(cfg.seq, device=dev, dtype=torch.float32), inv)
         self.cos = ang.cos().to(torch.bfloat16)
         self.sin = ang.sin().to(torch.bfloat16)
+        self.cos32 = ang.cos().contiguous()
+        self.sin32 = ang.sin().contiguous()
+        self.fused = fused
+        self.refresh_maps()
+
+    def refresh_maps(self):
+        """Composite index maps of the fused SwiGLU (gate/up output scatters and
+        the down-projection input gather); rebuilt whenever permutations change."""
+        self.swiglu_maps = []
+        for mods in self.layers:
+            fg, ig = mods["gate"].perm_out.forward, mods["gate"].perm_out.inverse
+            fu, iu = mods["up"].perm_out.forward, mods["up"].perm_out.inverse
+            fd, idn = mods["down"].perm_in.forward, mods["down"].perm_in.inverse
+            maps = {"cg": ig[fd], "cu": iu[fd], "A": idn[fg], "B": iu[fg], "C": idn[fu], "D": ig[fu]}
+            dev = mods["gate"].device
+            self.swiglu_maps.append({k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in maps.items()})
 
     def poet_layers(self):
         return [mods[p] for mods in self.layers for p in self.PROJ]
@@ -323,6 +493,9 @@ class PoetLlama(torch.nn.Module):
             n1 = self.dense_param(f"{i}.norm1", (d,)).detach().requires_grad_(True)
             n2 = self.dense_param(f"{i}.norm2", (d,)).detach().requires_grad_(True)
             leaves += [n1, n2]
+            if self.fused:
+                h = self._block_fused(i, mods, h, n1, n2, B, S)
+                continue
             x = F.rms_norm(h, (d,), n1.to(torch.bfloat16), 1e-6)
             q = mods["q"](x).view(B, S, H, hd)
             k = mods["k"](x).view(B, S, H, hd)
@@ -341,6 +514,30 @@ class PoetLlama(torch.nn.Module):
         loss = F.cross_entropy(logits.float(), targets.reshape(-1))
         self._leaves = leaves
         return loss
+
+    def _block_fused(self, i, mods, h, n1, n2, B, S):
+        """One decoder block with every POET-X permutation fused into a
+        neighbouring kernel (no standalone permutation pass except around
+        the cuDNN attention)."""
+        cfg = self.cfg
+        d, H, hd = cfg.d, cfg.heads, cfg.head_dim
+        q, k, v, o = mods["q"], mods["k"], mods["v"], mods["o"]
+        gate, up, down = mods["gate"], mods["up"], mods["down"]
+        pin = lambda m: m.perm_in.device(m.device)  # noqa: E731
+        pout = lambda m: m.perm_out.device(m.device)  # noqa: E731
+        uq, uk, uv = _RMSNormGather.apply(h, n1, [pin(q)[0], pin(k)[0], pin(v)[0]],
+                                          [pin(q)[1], pin(k)[1], pin(v)[1]])
+        vq, vk, vv = _PoetRawFn.apply(uq, q), _PoetRawFn.apply(uk, k), _PoetRawFn.apply(uv, v)
+        qr = _RopeScatter.apply(vq, pout(q)[1], pout(q)[0], self.cos32, self.sin32, S, H, hd)
+        kr = _RopeScatter.apply(vk, pout(k)[1], pout(k)[0], self.cos32, self.sin32, S, H, hd)
+        vz = _Permute.apply(vv, pout(v)[1], pout(v)[0])
+        a = F.scaled_dot_product_attention(qr.view(B, S, H, hd).transpose(1, 2), kr.view(B, S, H, hd).transpose(1, 2),
+                                           vz.view(B, S, H, hd).transpose(1, 2), is_causal=True)
+        uo = _Permute.apply(a.transpose(1, 2).reshape(B * S, d), pin(o)[0], pin(o)[1])
+        h = _ScatterAdd.apply(h, _PoetRawFn.apply(uo, o), pout(o)[1], pout(o)[0])
+        ug, uu = _RMSNormGather.apply(h, n2, [pin(gate)[0], pin(up)[0]], [pin(gate)[1], pin(up)[1]])
+        ud = _SwiGLUGather.apply(_PoetRawFn.apply(ug, gate), _PoetRawFn.apply(uu, up), self.swiglu_maps[i])
+        return _ScatterAdd.apply(h, _PoetRawFn.apply(ud, down), pout(down)[1], pout(down)[0])
 
     def backward_dense_grads(self, loss):
         """Backprop; dense grads land in the flat dense grad buffer."""
@@ -376,10 +573,11 @@ class Trainer:
     """One training step = forward, backward, (all-reduce), clip+AdamW, merge."""
 
     def __init__(self, cfg: LlamaConfig, micro_batch: int, seed: int = 0, merge_gap: int = 400,
-                 total_steps: int = 10_000, base_lr: float = 1e-3, device="cuda", pg=None):
+                 total_steps: int = 10_000, base_lr: float = 1e-3, device="cuda", pg=None,
+                 fused: bool = True):
         self.cfg = cfg
         self.device = torch.device(device)
-        self.model = PoetLlama(cfg, seed=seed, device=self.device)
+        self.model = PoetLlama(cfg, seed=seed, device=self.device, fused=fused)
         self.micro_batch = micro_batch
         self.seed = seed
         self.merge_gap = merge_gap
@@ -423,5 +621,6 @@ class Trainer:
         layers = self.model.poet_layers()
         for lay, rng in zip(layers, merge_rngs(self.seed, self.step_idx, len(layers))):
             lay.merge_and_reinit(rng)
+        self.model.refresh_maps()
         self.model.poet.reset_moments()
         self.since_merge = 0

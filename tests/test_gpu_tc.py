@@ -124,7 +124,7 @@ def test_layer_backward_dg_matches_packed(N):
     d = layer._desc()
     ws, wsb = N.workspace(N.lib().poetx_layer_workspace_bytes(d, T))
     N.call("poetx_layer_backward_dg", d, f.struct, T, x.data_ptr(), dz.data_ptr(), cache.saved_mm2.data_ptr(),
-           dx.data_ptr(), dgr.data_ptr(), dgp.data_ptr(), 0, ws, wsb, N.stream_ptr())
+           dx.data_ptr(), dgr.data_ptr(), dgp.data_ptr(), 0, 0, ws, wsb, N.stream_ptr())
     assert torch.equal(dx, g_ref.x)
     _, qq2r, _ = P.cnp_forward_tc(f.packed_r, b)
     _, qq2p, _ = P.cnp_forward_tc(f.packed_p, b)
