@@ -14,6 +14,8 @@
 //
 // Tiles of rows per CTA iteration (grid-stride), staged in shared memory with
 // 16-byte coalesced loads, outputs written with 16-byte coalesced stores.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace poetx {
@@ -378,7 +380,11 @@ int check_rows(int64_t T, int64_t d, size_t smem) {
 // rows per tile: ~48 KB of staged rows per CTA (index loads amortised over
 // the tile, several CTAs per SM for latency hiding)
 int pick_rt(int64_t bytes_per_row) {
-  int64_t rt = (48 * 1024) / (bytes_per_row > 0 ? bytes_per_row : 1);
+  static int64_t budget = [] {
+    const char* e = getenv("POETX_ROW_TILE_KB");
+    return static_cast<int64_t>(e ? atoi(e) : 48) * 1024;
+  }();
+  int64_t rt = budget / (bytes_per_row > 0 ? bytes_per_row : 1);
   if (rt >= 8) return 8;
   if (rt >= 4) return 4;
   if (rt >= 2) return 2;

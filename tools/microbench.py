@@ -101,10 +101,58 @@ def hbm():
                   f"{2 * x.numel() * b / ms / 1e9:.0f} TF/s")
 
 
+def rows():
+    import ctypes as C
+    from paper_2603_05500_b200.trainer import _ptrs
+    print("== fused row kernels (bf16, T=8192) ==", os.environ.get("POETX_ROW_TILE_KB", "48"), "KB tiles")
+    T, d, f, H, hd, S = 8192, 2048, 5632, 32, 64, 256
+    dev = "cuda"
+    st = N.stream_ptr()
+    x = torch.randn((T, d), device=dev).bfloat16()
+    w = torch.ones(d, device=dev)
+    perms = [torch.randperm(d, device=dev).int() for _ in range(3)]
+    outs = [torch.empty_like(x) for _ in range(3)]
+    rstd = torch.empty(T, device=dev)
+    ms = timeit(lambda: N.call("poetx_rmsnorm_gather", T, d, x.data_ptr(), w.data_ptr(), 1e-6, 3, _ptrs(perms),
+                               _ptrs(outs), rstd.data_ptr(), st))
+    print(f"rmsnorm_gather K=3: {ms * 1e3:.1f} us  {4 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
+    dx = torch.empty_like(x)
+    dw = torch.empty_like(w)
+    ws, wsb = N.workspace(N.lib().poetx_rmsnorm_gather_bwd_workspace_bytes(T, d))
+    ms = timeit(lambda: N.call("poetx_rmsnorm_gather_bwd", T, d, x.data_ptr(), w.data_ptr(), rstd.data_ptr(), 3,
+                               _ptrs(perms), _ptrs(outs), dx.data_ptr(), dw.data_ptr(), 0, ws, wsb, st))
+    print(f"rmsnorm_gather_bwd K=3: {ms * 1e3:.1f} us  {5 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
+    vg = torch.randn((T, f), device=dev).bfloat16()
+    vu = torch.randn_like(vg)
+    o = torch.empty_like(vg)
+    pf = [torch.randperm(f, device=dev).int() for _ in range(4)]
+    ms = timeit(lambda: N.call("poetx_swiglu_gather", T, f, vg.data_ptr(), vu.data_ptr(), pf[0].data_ptr(),
+                               pf[1].data_ptr(), o.data_ptr(), st))
+    print(f"swiglu_gather: {ms * 1e3:.1f} us  {3 * vg.numel() * 2 / ms / 1e6:.0f} GB/s")
+    o2 = torch.empty_like(vg)
+    ms = timeit(lambda: N.call("poetx_swiglu_gather_bwd", T, f, vg.data_ptr(), vu.data_ptr(), o.data_ptr(),
+                               pf[0].data_ptr(), pf[1].data_ptr(), pf[2].data_ptr(), pf[3].data_ptr(),
+                               o2.data_ptr(), outs[0].data_ptr() if False else torch.empty_like(vg).data_ptr(), st))
+    print(f"swiglu_gather_bwd: {ms * 1e3:.1f} us  {5 * vg.numel() * 2 / ms / 1e6:.0f} GB/s")
+    ang = torch.outer(torch.arange(S, device=dev).float(), torch.rand(hd // 2, device=dev))
+    cs, sn = ang.cos().contiguous(), ang.sin().contiguous()
+    ms = timeit(lambda: N.call("poetx_rope_scatter", T, S, H, hd, x.data_ptr(), perms[0].data_ptr(), cs.data_ptr(),
+                               sn.data_ptr(), outs[1].data_ptr(), st))
+    print(f"rope_scatter: {ms * 1e3:.1f} us  {2 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
+    ms = timeit(lambda: N.call("poetx_rope_scatter_bwd", T, S, H, hd, x.data_ptr(), perms[0].data_ptr(),
+                               cs.data_ptr(), sn.data_ptr(), outs[1].data_ptr(), st))
+    print(f"rope_scatter_bwd: {ms * 1e3:.1f} us  {2 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
+    ms = timeit(lambda: N.call("poetx_scatter_add", T, d, x.data_ptr(), outs[0].data_ptr(), perms[0].data_ptr(),
+                               outs[2].data_ptr(), st))
+    print(f"scatter_add: {ms * 1e3:.1f} us  {3 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("gemm", "all"):
         gemm()
+    if what in ("rows", "all"):
+        rows()
     if what in ("hbm", "all"):
         hbm()
     if what in ("layer", "all"):
