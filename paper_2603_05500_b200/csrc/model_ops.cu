@@ -33,83 +33,112 @@ __device__ __forceinline__ float bf(const __nv_bfloat16 v) { return __bfloat162f
 
 // ---------------------------------------------------------------------------
 // All kernels process TILES of RT rows per iteration: the rows are staged in
-// shared memory with 16-byte loads, and every index vector (8 columns per
-// int4 pair) is loaded once per tile and applied to all RT rows.
+// shared memory with cp.async 16-byte copies, every index vector (8 columns
+// per int4 pair) is loaded once per tile and applied to all RT rows, and all
+// global stores are 16-byte vectors.  In-row offsets are 32-bit.
 // ---------------------------------------------------------------------------
 
-template <int RT>
-__device__ __forceinline__ int64_t tile_rows(int64_t r0, int64_t T) { return T - r0 < RT ? T - r0 : RT; }
-
-__device__ __forceinline__ void load_rows(__nv_bfloat16* s, const __nv_bfloat16* g, int64_t nrows,
-                                          int64_t n) {
-  const uint4* src = reinterpret_cast<const uint4*>(g);
-  uint4* dst = reinterpret_cast<uint4*>(s);
-  for (int64_t i = threadIdx.x; i < nrows * (n / 8); i += blockDim.x) dst[i] = __ldcs(src + i);
+__device__ __forceinline__ void cp16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<uint32_t>(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
 }
 
-__device__ __forceinline__ void load_idx8(const int32_t* idx, int64_t j0, int (&o)[8]) {
+// stage nrows consecutive rows of n bf16 (n % 8 == 0) into smem
+__device__ __forceinline__ void stage_rows(__nv_bfloat16* s, const __nv_bfloat16* g, int nrows, int n) {
+  const uint4* src = reinterpret_cast<const uint4*>(g);
+  uint4* dst = reinterpret_cast<uint4*>(s);
+  const int nv = nrows * (n / 8);
+  for (int i = threadIdx.x; i < nv; i += blockDim.x) cp16(dst + i, src + i);
+}
+
+__device__ __forceinline__ void load_idx8(const int32_t* idx, int j0, int (&o)[8]) {
   const int4 a = __ldg(reinterpret_cast<const int4*>(idx + j0));
   const int4 b = __ldg(reinterpret_cast<const int4*>(idx + j0 + 4));
   o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
 }
-
-__device__ __forceinline__ uint4 pack8(const float (&v)[8]) {
-  __nv_bfloat162 p0 = __floats2bfloat162_rn(v[0], v[1]);
-  __nv_bfloat162 p1 = __floats2bfloat162_rn(v[2], v[3]);
-  __nv_bfloat162 p2 = __floats2bfloat162_rn(v[4], v[5]);
-  __nv_bfloat162 p3 = __floats2bfloat162_rn(v[6], v[7]);
-  uint4 u;
-  u.x = *reinterpret_cast<uint32_t*>(&p0);
-  u.y = *reinterpret_cast<uint32_t*>(&p1);
-  u.z = *reinterpret_cast<uint32_t*>(&p2);
-  u.w = *reinterpret_cast<uint32_t*>(&p3);
-  return u;
+__device__ __forceinline__ void load_f8(const float* p, float (&o)[8]) {
+  const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+  const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+  o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
 }
-
-// per-row sum of squares: warp w reduces rows w, w + 8, ...
-__device__ __forceinline__ void rows_rstd(const __nv_bfloat16* xs, int64_t nrows, int64_t d, float eps,
-                                          float* rstd_s) {
-  const int w = threadIdx.x / 32, l = threadIdx.x % 32;
-  for (int64_t r = w; r < nrows; r += blockDim.x / 32) {
-    float ss = 0.f;
-    for (int64_t c = l; c < d; c += 32) {
-      const float v = bf(xs[r * d + c]);
-      ss += v * v;
-    }
-    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    if (l == 0) rstd_s[r] = rsqrtf(ss / static_cast<float>(d) + eps);
+__device__ __forceinline__ void unpack8(const uint4 u, float (&o)[8]) {
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const float2 f = __bfloat1622float2(h[q]);
+    o[2 * q] = f.x;
+    o[2 * q + 1] = f.y;
   }
 }
+__device__ __forceinline__ uint4 pack8(const float (&v)[8]) {
+  uint4 u;
+  uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    __nv_bfloat162 p = __floats2bfloat162_rn(v[2 * q], v[2 * q + 1]);
+    w[q] = *reinterpret_cast<uint32_t*>(&p);
+  }
+  return u;
+}
+__device__ __forceinline__ float sigmoid_f(float v) { return __frcp_rn(1.f + __expf(-v)); }
 
 template <int RT>
 __global__ void __launch_bounds__(kThreads) rmsnorm_gather_kernel(
-    int64_t T, int64_t d, const __nv_bfloat16* __restrict__ x, const float* __restrict__ w,
+    int64_t T, int d, const __nv_bfloat16* __restrict__ x, const float* __restrict__ w,
     float eps, int K, IdxList outs, float* __restrict__ rstd_out) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);
   float* rstd_s = reinterpret_cast<float*>(sm + RT * d * 2);
+  const int wp = threadIdx.x / 32, l = threadIdx.x % 32, nvec = d / 8;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
-    const int64_t nr = tile_rows<RT>(r0, T);
-    load_rows(xs, x + r0 * d, nr, d);
+    const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
+    stage_rows(xs, x + r0 * d, nr, d);
+    cp_wait_all();
     __syncthreads();
-    rows_rstd(xs, nr, d, eps, rstd_s);
+    for (int r = wp; r < nr; r += kThreads / 32) {  // warp per row: sum of squares
+      float ss = 0.f;
+      const uint4* row = reinterpret_cast<const uint4*>(xs + r * d);
+      for (int i = l; i < nvec; i += 32) {
+        float v[8];
+        unpack8(row[i], v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) ss += v[q] * v[q];
+      }
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (l == 0) rstd_s[r] = rsqrtf(ss / static_cast<float>(d) + eps);
+    }
     __syncthreads();
-    for (int64_t e = threadIdx.x; e < nr * d; e += blockDim.x) {
-      const int64_t r = e / d, c = e % d;
-      xs[e] = __float2bfloat16_rn(bf(xs[e]) * rstd_s[r] * w[c]);
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {  // y = x * rstd * w in place
+      float wv[8];
+      load_f8(w + 8 * i, wv);
+      for (int r = 0; r < nr; ++r) {
+        uint4* p = reinterpret_cast<uint4*>(xs + r * d) + i;
+        float v[8];
+        unpack8(*p, v);
+        const float rs = rstd_s[r];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) v[q] = v[q] * rs * wv[q];
+        *p = pack8(v);
+      }
     }
     if (threadIdx.x < nr) rstd_out[r0 + threadIdx.x] = rstd_s[threadIdx.x];
     __syncthreads();
     for (int k = 0; k < K; ++k) {
       __nv_bfloat16* o = static_cast<__nv_bfloat16*>(outs.ptr[k]) + r0 * d;
-      for (int64_t i = threadIdx.x; i < d / 8; i += blockDim.x) {
+      for (int i = threadIdx.x; i < nvec; i += kThreads) {
         int id[8];
         load_idx8(outs.idx[k], 8 * i, id);
-        for (int64_t r = 0; r < nr; ++r) {
+        for (int r = 0; r < nr; ++r) {
+          const __nv_bfloat16* row = xs + r * d;
           float v[8];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) v[q] = bf(xs[r * d + id[q]]);
-          __stcs(reinterpret_cast<uint4*>(o + r * d) + i, pack8(v));
+          for (int q = 0; q < 8; ++q) v[q] = bf(row[id[q]]);
+          __stcs(reinterpret_cast<uint4*>(o + static_cast<int64_t>(r) * d) + i, pack8(v));
         }
       }
     }
@@ -121,60 +150,93 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_kernel(
 // dw partial[c] += dy*x*rstd  (per CTA, reduced later in fixed order)
 template <int RT>
 __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
-    int64_t T, int64_t d, const __nv_bfloat16* __restrict__ x, const float* __restrict__ w,
+    int64_t T, int d, const __nv_bfloat16* __restrict__ x, const float* __restrict__ w,
     const float* __restrict__ rstd_in, int K, IdxList dus, __nv_bfloat16* __restrict__ dx,
     float* __restrict__ dw_part) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);   // RT rows
   __nv_bfloat16* dus_s = xs + RT * d;                         // K x RT rows
   float* dy = reinterpret_cast<float*>(dus_s + K * RT * d);    // RT rows fp32
-  float* dot_s = dy + RT * d;                                  // RT
-  float dwacc[16];
+  float* red = dy + RT * d;                                    // [RT][8] warp partials
+  const int wp = threadIdx.x / 32, l = threadIdx.x % 32, nvec = d / 8;
+  float dwacc[2][8];
 #pragma unroll
-  for (int i = 0; i < 16; ++i) dwacc[i] = 0.f;
-  const int wp = threadIdx.x / 32, l = threadIdx.x % 32;
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) dwacc[a][q] = 0.f;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
-    const int64_t nr = tile_rows<RT>(r0, T);
-    load_rows(xs, x + r0 * d, nr, d);
+    const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
+    stage_rows(xs, x + r0 * d, nr, d);
     for (int k = 0; k < K; ++k)
-      load_rows(dus_s + k * RT * d, static_cast<const __nv_bfloat16*>(dus.ptr[k]) + r0 * d, nr, d);
+      stage_rows(dus_s + k * RT * d, static_cast<const __nv_bfloat16*>(dus.ptr[k]) + r0 * d, nr, d);
+    cp_wait_all();
     __syncthreads();
-    // dy (gathers amortised over the tile's rows)
-    for (int64_t c = threadIdx.x; c < d; c += blockDim.x) {
-      int iv[kMaxK];
-      for (int k = 0; k < K; ++k) iv[k] = __ldg(dus.idx[k] + c);
-      for (int64_t r = 0; r < nr; ++r) {
-        float s = 0.f;
-        for (int k = 0; k < K; ++k) s += bf(dus_s[(k * RT + r) * d + iv[k]]);
-        dy[r * d + c] = s;
+    float dot[RT];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) dot[r] = 0.f;
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      int iv[kMaxK][8];
+      for (int k = 0; k < K; ++k) load_idx8(dus.idx[k], 8 * i, iv[k]);
+      float wv[8];
+      load_f8(w + 8 * i, wv);
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        if (r >= nr) break;
+        float s[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) s[q] = 0.f;
+        for (int k = 0; k < K; ++k) {
+          const __nv_bfloat16* row = dus_s + (k * RT + r) * d;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) s[q] += bf(row[iv[k][q]]);
+        }
+        float xv[8];
+        unpack8(reinterpret_cast<const uint4*>(xs + r * d)[i], xv);
+        float4* dyp = reinterpret_cast<float4*>(dy + r * d + 8 * i);
+        dyp[0] = make_float4(s[0], s[1], s[2], s[3]);
+        dyp[1] = make_float4(s[4], s[5], s[6], s[7]);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dot[r] += s[q] * wv[q] * xv[q];
       }
     }
-    __syncthreads();
-    for (int64_t r = wp; r < nr; r += blockDim.x / 32) {
-      float acc = 0.f;
-      for (int64_t c = l; c < d; c += 32) acc += dy[r * d + c] * w[c] * bf(xs[r * d + c]);
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-      if (l == 0) dot_s[r] = acc;
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      float v = dot[r];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (l == 0) red[r * 8 + wp] = v;
     }
     __syncthreads();
-    int q = 0;
-    for (int64_t c = threadIdx.x; c < d; c += blockDim.x, ++q) {
-      const float wc = w[c];
-      float dwc = 0.f;
-      for (int64_t r = 0; r < nr; ++r) {
+    int slot = 0;
+    for (int i = threadIdx.x; i < nvec; i += kThreads, ++slot) {
+      float wv[8];
+      load_f8(w + 8 * i, wv);
+      for (int r = 0; r < nr; ++r) {
+        float tot = 0.f;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) tot += red[r * 8 + k];
         const float rs = rstd_in[r0 + r];
-        const float xv = bf(xs[r * d + c]);
-        const float coef = rs * rs * rs * dot_s[r] / static_cast<float>(d);
-        dx[(r0 + r) * d + c] = __float2bfloat16_rn(rs * dy[r * d + c] * wc - coef * xv);
-        dwc += dy[r * d + c] * xv * rs;
+        const float coef = rs * rs * rs * tot / static_cast<float>(d);
+        float xv[8], o[8];
+        unpack8(reinterpret_cast<const uint4*>(xs + r * d)[i], xv);
+        const float4* dyp = reinterpret_cast<const float4*>(dy + r * d + 8 * i);
+        const float4 d0 = dyp[0], d1 = dyp[1];
+        const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          o[q] = rs * dv[q] * wv[q] - coef * xv[q];
+          if (slot < 2) dwacc[slot][q] += dv[q] * xv[q] * rs;
+        }
+        __stcs(reinterpret_cast<uint4*>(dx + (r0 + r) * d) + i, pack8(o));
       }
-      if (q < 16) dwacc[q] += dwc;
     }
     __syncthreads();
   }
-  int q = 0;
-  for (int64_t c = threadIdx.x; c < d && q < 16; c += blockDim.x, ++q)
-    dw_part[blockIdx.x * d + c] = dwacc[q];
+  int slot = 0;
+  for (int i = threadIdx.x; i < nvec && slot < 2; i += kThreads, ++slot) {
+    float4* dst = reinterpret_cast<float4*>(dw_part + static_cast<int64_t>(blockIdx.x) * d + 8 * i);
+    dst[0] = make_float4(dwacc[slot][0], dwacc[slot][1], dwacc[slot][2], dwacc[slot][3]);
+    dst[1] = make_float4(dwacc[slot][4], dwacc[slot][5], dwacc[slot][6], dwacc[slot][7]);
+  }
 }
 
 // column sums of a [rows, d] partial matrix: 8 warps split the rows of a
@@ -199,32 +261,33 @@ __global__ void __launch_bounds__(256) colsum_kernel(int64_t rows, int64_t d, co
   }
 }
 
-__device__ __forceinline__ float silu_f(float v) { return v / (1.f + __expf(-v)); }
-__device__ __forceinline__ float dsilu_f(float v) {
-  const float s = 1.f / (1.f + __expf(-v));
-  return s * (1.f + v * (1.f - s));
-}
-
 template <int RT>
 __global__ void __launch_bounds__(kThreads) swiglu_gather_kernel(
-    int64_t T, int64_t f, const __nv_bfloat16* __restrict__ vg, const __nv_bfloat16* __restrict__ vu,
+    int64_t T, int f, const __nv_bfloat16* __restrict__ vg, const __nv_bfloat16* __restrict__ vu,
     const int32_t* __restrict__ cg, const int32_t* __restrict__ cu, __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* gs = reinterpret_cast<__nv_bfloat16*>(sm);
   __nv_bfloat16* us = gs + RT * f;
+  const int nvec = f / 8;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
-    const int64_t nr = tile_rows<RT>(r0, T);
-    load_rows(gs, vg + r0 * f, nr, f);
-    load_rows(us, vu + r0 * f, nr, f);
+    const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
+    stage_rows(gs, vg + r0 * f, nr, f);
+    stage_rows(us, vu + r0 * f, nr, f);
+    cp_wait_all();
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < f / 8; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
       int ig[8], iu[8];
       load_idx8(cg, 8 * i, ig);
       load_idx8(cu, 8 * i, iu);
-      for (int64_t r = 0; r < nr; ++r) {
+      for (int r = 0; r < nr; ++r) {
+        const __nv_bfloat16* grow = gs + r * f;
+        const __nv_bfloat16* urow = us + r * f;
         float v[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) v[q] = silu_f(bf(gs[r * f + ig[q]])) * bf(us[r * f + iu[q]]);
+        for (int q = 0; q < 8; ++q) {
+          const float gv = bf(grow[ig[q]]);
+          v[q] = gv * sigmoid_f(gv) * bf(urow[iu[q]]);
+        }
         __stcs(reinterpret_cast<uint4*>(out + (r0 + r) * f) + i, pack8(v));
       }
     }
@@ -235,7 +298,7 @@ __global__ void __launch_bounds__(kThreads) swiglu_gather_kernel(
 // dv_g[j] = du[A[j]] * silu'(v_g[j]) * v_u[B[j]] ; dv_u[j] = du[C[j]] * silu(v_g[D[j]])
 template <int RT>
 __global__ void __launch_bounds__(kThreads) swiglu_gather_bwd_kernel(
-    int64_t T, int64_t f, const __nv_bfloat16* __restrict__ vg, const __nv_bfloat16* __restrict__ vu,
+    int64_t T, int f, const __nv_bfloat16* __restrict__ vg, const __nv_bfloat16* __restrict__ vu,
     const __nv_bfloat16* __restrict__ du, const int32_t* __restrict__ A,
     const int32_t* __restrict__ B, const int32_t* __restrict__ Cc, const int32_t* __restrict__ D,
     __nv_bfloat16* __restrict__ dvg, __nv_bfloat16* __restrict__ dvu) {
@@ -243,25 +306,30 @@ __global__ void __launch_bounds__(kThreads) swiglu_gather_bwd_kernel(
   __nv_bfloat16* gs = reinterpret_cast<__nv_bfloat16*>(sm);
   __nv_bfloat16* us = gs + RT * f;
   __nv_bfloat16* ds = us + RT * f;
+  const int nvec = f / 8;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
-    const int64_t nr = tile_rows<RT>(r0, T);
-    load_rows(gs, vg + r0 * f, nr, f);
-    load_rows(us, vu + r0 * f, nr, f);
-    load_rows(ds, du + r0 * f, nr, f);
+    const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
+    stage_rows(gs, vg + r0 * f, nr, f);
+    stage_rows(us, vu + r0 * f, nr, f);
+    stage_rows(ds, du + r0 * f, nr, f);
+    cp_wait_all();
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < f / 8; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
       int ia[8], ib[8], ic[8], id[8];
       load_idx8(A, 8 * i, ia);
       load_idx8(B, 8 * i, ib);
       load_idx8(Cc, 8 * i, ic);
       load_idx8(D, 8 * i, id);
-      for (int64_t r = 0; r < nr; ++r) {
-        const int64_t o = r * f;
-        float g[8], u[8];
+      for (int r = 0; r < nr; ++r) {
+        const int o = r * f;
+        float gself[8], g[8], u[8];
+        unpack8(reinterpret_cast<const uint4*>(gs + o)[i], gself);
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          g[q] = bf(ds[o + ia[q]]) * dsilu_f(bf(gs[o + 8 * i + q])) * bf(us[o + ib[q]]);
-          u[q] = bf(ds[o + ic[q]]) * silu_f(bf(gs[o + id[q]]));
+          const float sg = sigmoid_f(gself[q]);
+          g[q] = bf(ds[o + ia[q]]) * (sg * (1.f + gself[q] * (1.f - sg))) * bf(us[o + ib[q]]);
+          const float gd = bf(gs[o + id[q]]);
+          u[q] = bf(ds[o + ic[q]]) * gd * sigmoid_f(gd);
         }
         __stcs(reinterpret_cast<uint4*>(dvg + (r0 + r) * f) + i, pack8(g));
         __stcs(reinterpret_cast<uint4*>(dvu + (r0 + r) * f) + i, pack8(u));
@@ -271,36 +339,40 @@ __global__ void __launch_bounds__(kThreads) swiglu_gather_bwd_kernel(
   }
 }
 
-// out = RoPE(z), z[c] = v[inv[c]]; 8 outputs per vector all lie in one half of a head
+// out = RoPE(z), z[c] = v[inv[c]]; the 8 outputs of a vector lie in one half
+// of one head (hd/2 % 8 == 0); hd is a power of two
 template <int RT>
 __global__ void __launch_bounds__(kThreads) rope_scatter_kernel(
-    int64_t T, int64_t S, int64_t H, int64_t hd, const __nv_bfloat16* __restrict__ v,
+    int64_t T, int S, int H, int hd, const __nv_bfloat16* __restrict__ v,
     const int32_t* __restrict__ inv, const float* __restrict__ cosb, const float* __restrict__ sinb,
     __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* vs = reinterpret_cast<__nv_bfloat16*>(sm);
-  const int64_t d = H * hd, half = hd / 2;
+  const int d = H * hd, half = hd / 2, nvec = d / 8;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
-    const int64_t nr = tile_rows<RT>(r0, T);
-    load_rows(vs, v + r0 * d, nr, d);
+    const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
+    stage_rows(vs, v + r0 * d, nr, d);
+    cp_wait_all();
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < d / 8; i += blockDim.x) {
-      const int64_t c0 = 8 * i, hh = c0 / hd, wi = c0 % hd;
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      const int c0 = 8 * i, wi = c0 & (hd - 1);
       const bool first = wi < half;
-      const int64_t pc0 = first ? c0 + half : c0 - half;  // partner columns
-      const int64_t i0 = first ? wi : wi - half;          // frequency index
+      const int pc0 = first ? c0 + half : c0 - half;
+      const int f0 = first ? wi : wi - half;
       int me[8], pa[8];
       load_idx8(inv, c0, me);
       load_idx8(inv, pc0, pa);
-      (void)hh;
-      for (int64_t r = 0; r < nr; ++r) {
-        const int64_t s = (r0 + r) % S;
+      for (int r = 0; r < nr; ++r) {
+        const int s = static_cast<int>((r0 + r) % S);
+        float cs[8], sn[8];
+        load_f8(cosb + s * half + f0, cs);
+        load_f8(sinb + s * half + f0, sn);
+        const __nv_bfloat16* row = vs + r * d;
         float o[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const float cs = cosb[s * half + i0 + q], sn = sinb[s * half + i0 + q];
-          const float zm = bf(vs[r * d + me[q]]), zp = bf(vs[r * d + pa[q]]);
-          o[q] = first ? zm * cs - zp * sn : zm * cs + zp * sn;
+          const float zm = bf(row[me[q]]), zp = bf(row[pa[q]]);
+          o[q] = first ? zm * cs[q] - zp * sn[q] : zm * cs[q] + zp * sn[q];
         }
         __stcs(reinterpret_cast<uint4*>(out + (r0 + r) * d) + i, pack8(o));
       }
@@ -312,30 +384,39 @@ __global__ void __launch_bounds__(kThreads) rope_scatter_kernel(
 // dv[j] = dz[fwd[j]], dz = RoPE^T(dout) computed on the fly from the staged row
 template <int RT>
 __global__ void __launch_bounds__(kThreads) rope_scatter_bwd_kernel(
-    int64_t T, int64_t S, int64_t H, int64_t hd, const __nv_bfloat16* __restrict__ dout,
+    int64_t T, int S, int H, int hd, const __nv_bfloat16* __restrict__ dout,
     const int32_t* __restrict__ fwd, const float* __restrict__ cosb, const float* __restrict__ sinb,
     __nv_bfloat16* __restrict__ dv) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* os = reinterpret_cast<__nv_bfloat16*>(sm);
-  const int64_t d = H * hd, half = hd / 2;
+  const int d = H * hd, half = hd / 2, nvec = d / 8;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
-    const int64_t nr = tile_rows<RT>(r0, T);
-    load_rows(os, dout + r0 * d, nr, d);
+    const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
+    stage_rows(os, dout + r0 * d, nr, d);
+    cp_wait_all();
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < d / 8; i += blockDim.x) {
-      int cc[8];
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      int cc[8], pp[8], ff[8];
+      bool first[8];
       load_idx8(fwd, 8 * i, cc);
-      for (int64_t r = 0; r < nr; ++r) {
-        const int64_t s = (r0 + r) % S;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int wi = cc[q] & (hd - 1);
+        first[q] = wi < half;
+        ff[q] = first[q] ? wi : wi - half;
+        pp[q] = first[q] ? cc[q] + half : cc[q] - half;
+      }
+      for (int r = 0; r < nr; ++r) {
+        const int s = static_cast<int>((r0 + r) % S);
+        const float* cr = cosb + s * half;
+        const float* sr = sinb + s * half;
+        const __nv_bfloat16* row = os + r * d;
         float o[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          const int64_t c = cc[q], wi = c % hd;
-          const bool first = wi < half;
-          const int64_t fi = first ? wi : wi - half;
-          const float cs = cosb[s * half + fi], sn = sinb[s * half + fi];
-          const float g = bf(os[r * d + c]), gp = bf(os[r * d + (first ? c + half : c - half)]);
-          o[q] = first ? g * cs + gp * sn : g * cs - gp * sn;
+          const float cs = __ldg(cr + ff[q]), sn = __ldg(sr + ff[q]);
+          const float g = bf(row[cc[q]]), gp = bf(row[pp[q]]);
+          o[q] = first[q] ? g * cs + gp * sn : g * cs - gp * sn;
         }
         __stcs(reinterpret_cast<uint4*>(dv + (r0 + r) * d) + i, pack8(o));
       }
@@ -346,23 +427,25 @@ __global__ void __launch_bounds__(kThreads) rope_scatter_bwd_kernel(
 
 template <int RT>
 __global__ void __launch_bounds__(kThreads) scatter_add_kernel(
-    int64_t T, int64_t d, const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ v,
+    int64_t T, int d, const __nv_bfloat16* __restrict__ h, const __nv_bfloat16* __restrict__ v,
     const int32_t* __restrict__ inv, __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* vs = reinterpret_cast<__nv_bfloat16*>(sm);
+  const int nvec = d / 8;
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
-    const int64_t nr = tile_rows<RT>(r0, T);
-    load_rows(vs, v + r0 * d, nr, d);
+    const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
+    stage_rows(vs, v + r0 * d, nr, d);
+    cp_wait_all();
     __syncthreads();
-    for (int64_t i = threadIdx.x; i < d / 8; i += blockDim.x) {
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
       int id[8];
       load_idx8(inv, 8 * i, id);
-      for (int64_t r = 0; r < nr; ++r) {
-        uint4 hv = __ldcs(reinterpret_cast<const uint4*>(h + (r0 + r) * d) + i);
-        const __nv_bfloat16* hh = reinterpret_cast<const __nv_bfloat16*>(&hv);
-        float o[8];
+      for (int r = 0; r < nr; ++r) {
+        float hv[8], o[8];
+        unpack8(__ldcs(reinterpret_cast<const uint4*>(h + (r0 + r) * d) + i), hv);
+        const __nv_bfloat16* row = vs + r * d;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) o[q] = bf(hh[q]) + bf(vs[r * d + id[q]]);
+        for (int q = 0; q < 8; ++q) o[q] = hv[q] + bf(row[id[q]]);
         __stcs(reinterpret_cast<uint4*>(out + (r0 + r) * d) + i, pack8(o));
       }
     }
@@ -443,8 +526,9 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
                              float* dw, int accumulate_dw, void* ws, size_t ws_bytes, void* stream) {
   POETX_REQUIRE(K >= 1 && K <= kMaxK, POETX_ESHAPE, "rmsnorm_gather_bwd: 1..3 inputs");
   POETX_REQUIRE(d <= 16 * kThreads, POETX_ESHAPE, "rmsnorm_gather_bwd: d > %d", 16 * kThreads);
+  POETX_REQUIRE(d % 8 == 0, POETX_ESHAPE, "rmsnorm_gather_bwd: d %% 8");
   const int rt = bwd_rt(d, K);
-  const size_t smem = rt * d * 2 * (1 + K) + rt * d * 4 + 64 * 4;
+  const size_t smem = rt * d * 2 * (1 + K) + rt * d * 4 + rt * 8 * 4;
   POETX_TRY(check_rows(T, d, smem));
   if (T == 0) return POETX_OK;
   const unsigned grid = row_grid(T, rt);
@@ -496,8 +580,8 @@ int poetx_swiglu_gather_bwd(int64_t T, int64_t f, const void* vg, const void* vu
 int poetx_rope_scatter(int64_t T, int64_t S, int64_t H, int64_t hd, const void* v,
                        const int32_t* inv, const float* cosb, const float* sinb, void* out,
                        void* stream) {
-  POETX_REQUIRE(hd % 2 == 0 && S > 0 && (hd / 2) % 8 == 0, POETX_ESHAPE,
-                "rope_scatter: head_dim/2 must be a multiple of 8, seq > 0");
+  POETX_REQUIRE(S > 0 && hd >= 16 && (hd & (hd - 1)) == 0, POETX_ESHAPE,
+                "rope_scatter: head_dim must be a power of two >= 16, seq > 0");
   const int rt = pick_rt(H * hd * 2);
   const size_t smem = rt * H * hd * 2;
   POETX_TRY(check_rows(T, H * hd, smem));
@@ -513,7 +597,8 @@ int poetx_rope_scatter(int64_t T, int64_t S, int64_t H, int64_t hd, const void* 
 int poetx_rope_scatter_bwd(int64_t T, int64_t S, int64_t H, int64_t hd, const void* dout,
                            const int32_t* fwd, const float* cosb, const float* sinb, void* dv,
                            void* stream) {
-  POETX_REQUIRE(hd % 2 == 0 && S > 0, POETX_ESHAPE, "rope_scatter_bwd: bad head dim / seq");
+  POETX_REQUIRE(S > 0 && hd >= 16 && (hd & (hd - 1)) == 0, POETX_ESHAPE,
+                "rope_scatter_bwd: head_dim must be a power of two >= 16, seq > 0");
   const int rt = pick_rt(H * hd * 2);
   const size_t smem = rt * H * hd * 2;
   POETX_TRY(check_rows(T, H * hd, smem));
