@@ -289,6 +289,13 @@ int poetx_adamw(int dtype, int ntensors, void* const* p, void* const* g, void* c
                 double eps, double weight_decay, double bc1, double bc2, const double* sqnorm,
                 double clip_threshold, int write_back_grads, void* stream);
 
+/* same update with the step-dependent scalars read from DEVICE memory
+ * dyn = {lr, lr*weight_decay, 1-beta1^t, 1-beta2^t, clip_threshold} (double),
+ * so a captured CUDA graph replays every step with fresh values. */
+int poetx_adamw_dyn(int dtype, int ntensors, void* const* p, void* const* g, void* const* m,
+                    void* const* v, const int64_t* numel, double beta1, double beta2, double eps,
+                    const double* dyn, const double* sqnorm, int write_back_grads, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

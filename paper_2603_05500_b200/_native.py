@@ -120,6 +120,8 @@ _SIGS = {
     "poetx_layer_merge": (I32, [C.POINTER(LayerDesc), VP, VP, VP, VP, VP, VP, VP, SZ, VP]),
     "poetx_sqnorm_workspace_bytes": (SZ, [I32, VP]),
     "poetx_sqnorm": (I32, [I32, I32, VP, VP, VP, VP, VP, SZ, VP]),
+    "poetx_adamw_dyn": (I32, [I32, I32, VP, VP, VP, VP, VP, C.c_double, C.c_double, C.c_double, VP, VP,
+                              I32, VP]),
     "poetx_adamw": (I32, [I32, I32, VP, VP, VP, VP, VP, C.c_double, C.c_double, C.c_double,
                           C.c_double, C.c_double, C.c_double, C.c_double, VP, C.c_double, I32, VP]),
 }

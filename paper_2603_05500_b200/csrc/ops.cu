@@ -646,7 +646,14 @@ __device__ __forceinline__ double op_sqrt(double a) { return __dsqrt_rn(a); }
 template <typename T>
 __global__ void adamw_kernel(int64_t n, T* __restrict__ p, T* __restrict__ g, T* __restrict__ m,
                              T* __restrict__ v, AdamScalars s, const double* __restrict__ sqnorm,
-                             int write_back) {
+                             int write_back, const double* __restrict__ dyn) {
+  if (dyn) {  // step-dependent scalars from device memory (CUDA-graph replays)
+    s.lr = dyn[0];
+    s.lrwd = dyn[1];
+    s.bc1 = dyn[2];
+    s.bc2 = dyn[3];
+    s.thr = dyn[4];
+  }
   const T b1 = static_cast<T>(s.b1), b2 = static_cast<T>(s.b2), one = T(1);
   const T omb1 = op_sub(one, b1), omb2 = op_sub(one, b2);
   const T bc1 = static_cast<T>(s.bc1), bc2 = static_cast<T>(s.bc2);
@@ -850,13 +857,35 @@ int poetx_sqnorm(int dtype, int ntensors, const void* const* g, const int64_t* n
   return POETX_OK;
 }
 
+static int adamw_launch(int dtype, int ntensors, void* const* p, void* const* g, void* const* m,
+                        void* const* v, const int64_t* numel, const AdamScalars& s,
+                        const double* sqnorm, int write_back_grads, const double* dyn,
+                        cudaStream_t st);
+
+int poetx_adamw_dyn(int dtype, int ntensors, void* const* p, void* const* g, void* const* m,
+                    void* const* v, const int64_t* numel, double beta1, double beta2, double eps,
+                    const double* dyn, const double* sqnorm, int write_back_grads, void* stream) {
+  POETX_REQUIRE(dtype == POETX_F32 || dtype == POETX_F64, POETX_ESHAPE, "adamw: bad dtype");
+  POETX_REQUIRE(dyn != nullptr, POETX_ESHAPE, "adamw_dyn: null scalars");
+  AdamScalars s{0.0, beta1, beta2, eps, 0.0, 1.0, 1.0, 0.0};
+  return adamw_launch(dtype, ntensors, p, g, m, v, numel, s, sqnorm, write_back_grads, dyn,
+                      as_stream(stream));
+}
+
 int poetx_adamw(int dtype, int ntensors, void* const* p, void* const* g, void* const* m,
                 void* const* v, const int64_t* numel, double lr, double beta1, double beta2,
                 double eps, double weight_decay, double bc1, double bc2, const double* sqnorm,
                 double clip_threshold, int write_back_grads, void* stream) {
   POETX_REQUIRE(dtype == POETX_F32 || dtype == POETX_F64, POETX_ESHAPE, "adamw: bad dtype");
-  cudaStream_t st = as_stream(stream);
   AdamScalars s{lr, beta1, beta2, eps, lr * weight_decay, bc1, bc2, clip_threshold};
+  return adamw_launch(dtype, ntensors, p, g, m, v, numel, s, sqnorm, write_back_grads, nullptr,
+                      as_stream(stream));
+}
+
+static int adamw_launch(int dtype, int ntensors, void* const* p, void* const* g, void* const* m,
+                        void* const* v, const int64_t* numel, const AdamScalars& s,
+                        const double* sqnorm, int write_back_grads, const double* dyn,
+                        cudaStream_t st) {
   for (int i = 0; i < ntensors; ++i) {
     if (numel[i] <= 0) continue;
     unsigned grid = grid_for(numel[i], 256, 148 * 8);
@@ -864,13 +893,13 @@ int poetx_adamw(int dtype, int ntensors, void* const* p, void* const* g, void* c
       adamw_kernel<float><<<grid, 256, 0, st>>>(numel[i], static_cast<float*>(p[i]),
                                                  static_cast<float*>(g[i]), static_cast<float*>(m[i]),
                                                  static_cast<float*>(v[i]), s, sqnorm,
-                                                 write_back_grads);
+                                                 write_back_grads, dyn);
     else
       adamw_kernel<double><<<grid, 256, 0, st>>>(numel[i], static_cast<double*>(p[i]),
                                                   static_cast<double*>(g[i]),
                                                   static_cast<double*>(m[i]),
                                                   static_cast<double*>(v[i]), s, sqnorm,
-                                                  write_back_grads);
+                                                  write_back_grads, dyn);
     POETX_LAUNCHED("adamw");
   }
   return POETX_OK;

@@ -228,3 +228,22 @@ def fused_clip_adamw(groups, threshold: float, sched: ScheduleConfig):
     for ps, gs, ms, vs, lr, t in groups:
         _adamw_launch(ps, gs, ms, vs, lr, sched, t, sqnorm=sq, threshold=threshold, write_back=0)
     return sq, bad
+
+
+def fused_clip_adamw_dyn(groups, sched: ScheduleConfig):
+    """CUDA-graph-friendly trainer update: per group (params, grads, m, v,
+    dyn) where ``dyn`` is a DEVICE float64 tensor {lr, lr*wd, bc1, bc2,
+    clip threshold} refreshed before each (replayed) step."""
+    allg = [g for grp in groups for g in grp[1]]
+    sq, bad = device_sqnorm(allg)
+    for ps, gs, ms, vs, dyn in groups:
+        P, G, M, V = ps, gs, ms, vs
+        N.call("poetx_adamw_dyn", N.dtype_code(P[0].dtype), len(P), _ptr_array(P), _ptr_array(G),
+               _ptr_array(M), _ptr_array(V), _numel_array(P), sched.beta1, sched.beta2, sched.eps,
+               dyn.data_ptr(), sq.data_ptr(), 0, N.stream_ptr(P[0].device))
+    return sq, bad
+
+
+def adamw_dyn_values(lr: float, t: int, threshold: float, sched: ScheduleConfig):
+    """Host values of the ``dyn`` vector for fused_clip_adamw_dyn."""
+    return [lr, lr * sched.weight_decay, 1.0 - sched.beta1 ** t, 1.0 - sched.beta2 ** t, threshold]

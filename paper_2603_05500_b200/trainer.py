@@ -29,7 +29,7 @@ import torch.nn.functional as F
 
 from . import _native as N
 from .cnp import num_pairs
-from .optim import ScheduleConfig, clip_threshold_at, fused_clip_adamw, lr_at
+from .optim import ScheduleConfig, adamw_dyn_values, clip_threshold_at, fused_clip_adamw_dyn, lr_at
 from .permute import PermutationMap, sample_permutation
 from .rng import Rng
 
@@ -195,6 +195,10 @@ class PoetLinear(torch.nn.Module):
         w = (torch.randn((m, n), generator=gen, device=self.device, dtype=torch.float32) * std).to(torch.bfloat16)
         self.perm_in = sample_permutation(m, rng)
         self.perm_out = sample_permutation(n, rng)
+        # device index buffers at FIXED addresses (updated in place at merge), so
+        # a captured CUDA graph of the step stays valid across merges
+        self.pin_dev = tuple(t.clone() for t in self.perm_in.device(self.device))
+        self.pout_dev = tuple(t.clone() for t in self.perm_out.device(self.device))
         self.premerged = torch.empty((m, n), dtype=torch.bfloat16, device=self.device)
         self._install(w)
         del w
@@ -210,8 +214,8 @@ class PoetLinear(torch.nn.Module):
         self._set_desc()
 
     def _set_desc(self):
-        fi, ii = self.perm_in.device(self.device)
-        fo, io = self.perm_out.device(self.device)
+        fi, ii = self.pin_dev
+        fo, io = self.pout_dev
         d = N.LayerDesc()
         d.dtype, d.variant, d.neumann_k = N.BF16, (N.FAST if self.variant == "fast" else N.MEM), self.k
         d.m, d.n, d.b = self.m, self.n, self.b
@@ -248,9 +252,10 @@ class PoetLinear(torch.nn.Module):
                pm_new.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
         self.premerged.copy_(pm_new)
         self.perm_in, self.perm_out = new_in, new_out
+        for dst, src in zip(self.pin_dev + self.pout_dev, new_in.device(self.device) + new_out.device(self.device)):
+            dst.copy_(src)
         self.packed_r.zero_()
         self.packed_p.zero_()
-        self._set_desc()
         self.merge_count += 1
 
 
@@ -474,6 +479,13 @@ class PoetLlama(torch.nn.Module):
             maps = {"cg": ig[fd], "cu": iu[fd], "A": idn[fg], "B": iu[fg], "C": idn[fu], "D": ig[fu]}
             dev = mods["gate"].device
             self.swiglu_maps.append({k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in maps.items()})
+        if getattr(self, "_maps_dev", None) is None:
+            self._maps_dev = self.swiglu_maps
+        else:  # keep device addresses fixed (CUDA-graph replays read them)
+            for old, new in zip(self._maps_dev, self.swiglu_maps):
+                for k in old:
+                    old[k].copy_(new[k])
+            self.swiglu_maps = self._maps_dev
 
     def poet_layers(self):
         return [mods[p] for mods in self.layers for p in self.PROJ]
@@ -523,8 +535,8 @@ class PoetLlama(torch.nn.Module):
         d, H, hd = cfg.d, cfg.heads, cfg.head_dim
         q, k, v, o = mods["q"], mods["k"], mods["v"], mods["o"]
         gate, up, down = mods["gate"], mods["up"], mods["down"]
-        pin = lambda m: m.perm_in.device(m.device)  # noqa: E731
-        pout = lambda m: m.perm_out.device(m.device)  # noqa: E731
+        pin = lambda m: m.pin_dev  # noqa: E731
+        pout = lambda m: m.pout_dev  # noqa: E731
         uq, uk, uv = _RMSNormGather.apply(h, n1, [pin(q)[0], pin(k)[0], pin(v)[0]],
                                           [pin(q)[1], pin(k)[1], pin(v)[1]])
         vq, vk, vv = _PoetRawFn.apply(uq, q), _PoetRawFn.apply(uk, k), _PoetRawFn.apply(uv, v)
@@ -587,11 +599,17 @@ class Trainer:
         self.pg = pg
         self.last_sq = None
         self.last_bad = None
+        self.graph = None
+        self.dyn_ring = [torch.zeros((2, 5), dtype=torch.float64).pin_memory() for _ in range(4)]
+        self.dyn_events = [None] * len(self.dyn_ring)
+        self.dyn = torch.zeros((2, 5), dtype=torch.float64, device=self.device)
 
     def tokens_per_step(self) -> int:
         return self.micro_batch * self.cfg.seq
 
-    def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+    def _compute(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        """The device work of one step (capturable: no host syncs, step-dependent
+        optimizer scalars read from ``self.dyn``)."""
         model = self.model
         model.dense.grad.zero_()
         model.stack.forward_factors()          # CNP of every block, one batched call
@@ -600,22 +618,70 @@ class Trainer:
         model.stack.backward_factors()         # batched CNP backward -> packed grads
         if self.pg is not None:
             average_gradients([model.poet.grad, model.dense.grad], self.pg)
-        s = self.sched
+        self.last_sq, self.last_bad = fused_clip_adamw_dyn(
+            [([model.poet.param], [model.poet.grad], [model.poet.m], [model.poet.v], self.dyn[0]),
+             ([model.dense.param], [model.dense.grad], [model.dense.m], [model.dense.v], self.dyn[1])],
+            self.sched)
+        return loss.detach()
+
+    def _prepare_scalars(self):
+        """Host side of runner.py:288-296: lr schedule, POET lr scale, clip ramp,
+        bias corrections (AdamW t per group, reset at merges)."""
+        model, s = self.model, self.sched
         thr = clip_threshold_at(self.step_idx, self.since_merge, s)
         model.poet.t += 1
         model.dense.t += 1
-        self.last_sq, self.last_bad = fused_clip_adamw(
-            [([model.poet.param], [model.poet.grad], [model.poet.m], [model.poet.v],
-              lr_at(self.step_idx, s, poet=True), model.poet.t),
-             ([model.dense.param], [model.dense.grad], [model.dense.m], [model.dense.v],
-              lr_at(self.step_idx, s), model.dense.t)],
-            thr, s)
+        vals = [adamw_dyn_values(lr_at(self.step_idx, s, poet=True), model.poet.t, thr, s),
+                adamw_dyn_values(lr_at(self.step_idx, s), model.dense.t, thr, s)]
+        # ring of pinned host slots: a slot is rewritten only after the stream
+        # has consumed its previous H2D copy (the CPU runs ahead of the GPU)
+        slot = self.step_idx % len(self.dyn_ring)
+        if self.dyn_events[slot] is not None:
+            self.dyn_events[slot].synchronize()
+        self.dyn_ring[slot].copy_(torch.tensor(vals, dtype=torch.float64))
+        self.dyn.copy_(self.dyn_ring[slot], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self.dyn_events[slot] = ev
+
+    def _advance(self):
         self.step_idx += 1
         if self.since_merge is not None:
             self.since_merge += 1
         if self.merge_gap and self.step_idx % self.merge_gap == 0:
             self.merge()
-        return loss.detach()
+
+    def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
+        self._prepare_scalars()
+        if self.graph is not None:
+            self.static_tokens.copy_(tokens, non_blocking=True)
+            self.static_targets.copy_(targets, non_blocking=True)
+            self.graph.replay()
+            loss = self.static_loss
+        else:
+            loss = self._compute(tokens, targets)
+        self._advance()
+        return loss
+
+    def capture(self, tokens: torch.Tensor, targets: torch.Tensor, warmup: int = 2):
+        """Capture one full step (forward, backward, CNP, all-reduce, update) as a
+        CUDA graph; later ``step`` calls replay it.  Merges run eagerly between
+        replays and update every buffer the graph reads in place."""
+        self.static_tokens = tokens.clone()
+        self.static_targets = targets.clone()
+        side = torch.cuda.Stream(self.device)
+        side.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(side):
+            for _ in range(warmup):
+                self.step(self.static_tokens, self.static_targets)
+        torch.cuda.current_stream(self.device).wait_stream(side)
+        self._prepare_scalars()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.static_loss = self._compute(self.static_tokens, self.static_targets)
+        self._advance()  # the capture ran the step once
+        self.graph = g
+        return self.static_loss
 
     def merge(self):
         layers = self.model.poet_layers()

@@ -46,3 +46,25 @@ def test_fused_block_matches_unfused_reference_path():
         cos = torch.nn.functional.cosine_similarity(a.double(), b.double(), dim=0).item()
         assert cos > 0.995, cos
         assert (a - b).norm() <= 0.1 * a.norm()
+
+
+def test_cuda_graph_replay_matches_eager_including_merge():
+    """A captured step replays the same computation as eager steps, and stays
+    valid across a merge (all buffers the graph reads are updated in place)."""
+    from paper_2603_05500_b200.trainer import Trainer, llama_config
+
+    cfg = llama_config("llama-60m", layers=2, seq=64)
+    toks = [torch.randint(0, cfg.vocab, (4, cfg.seq + 1), generator=torch.Generator().manual_seed(i)).cuda()
+            for i in range(6)]
+    eager = Trainer(cfg, micro_batch=4, seed=2, merge_gap=4, base_lr=3e-3)
+    graphed = Trainer(cfg, micro_batch=4, seed=2, merge_gap=4, base_lr=3e-3)
+    # the capture itself runs warmup steps + the captured step: mirror them eagerly
+    le = [float(eager.step(t[:, :-1], t[:, 1:])) for t in toks[:1] * 3]
+    graphed.capture(toks[0][:, :-1], toks[0][:, 1:], warmup=2)
+    assert graphed.step_idx == eager.step_idx == 3
+    for t in toks[1:]:
+        a = float(eager.step(t[:, :-1], t[:, 1:]))
+        b = float(graphed.step(t[:, :-1], t[:, 1:]))
+        assert abs(a - b) <= 1e-3 * abs(a), (a, b)
+    assert eager.model.poet_layers()[0].merge_count == graphed.model.poet_layers()[0].merge_count == 2
+    assert torch.allclose(eager.model.poet.param, graphed.model.poet.param, atol=1e-5, rtol=1e-3)
