@@ -219,6 +219,8 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         ms = start.elapsed_time(stop)
         launches = N.launch_count() - launches0
+        if trainer.graph is not None:
+            launches += n * trainer.graph_launches  # kernels inside each graph replay
         if world > 1:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -227,6 +229,9 @@ def run_ours(args, rank, world, local_rank):
 
     for i in range(args.warmup):
         trainer.step(dev_batches[i % 4][:, :-1], dev_batches[i % 4][:, 1:])
+    if args.graph:
+        tb = dev_batches[0]
+        trainer.capture(tb[:, :-1], tb[:, 1:])
     torch.cuda.reset_peak_memory_stats(dev)
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -239,10 +244,12 @@ def run_ours(args, rank, world, local_rank):
 
     # dominant-kernel roofline: CUDA events around each tcgen05 GEMM launch
     lib = N.lib()
+    graph, trainer.graph = trainer.graph, None  # host-side event hooks need eager launches
     lib.poetx_prof_reset()
     lib.poetx_prof_enable(1)
     timed(args.steps, resident=True, prof=True)
     lib.poetx_prof_enable(0)
+    trainer.graph = graph
     import ctypes as C
 
     tot_ms, cnt, flops = C.c_double(), C.c_int64(), C.c_double()
@@ -280,6 +287,7 @@ def run_ours(args, rank, world, local_rank):
                 "global_batch": B * world, "parallelism": f"dp{world}",
                 "l2": "working set (2.5 GB frozen weights + activations) far larger than the 126 MB L2",
                 "merge_gap": args.merge_gap,
+                "cuda_graph": bool(args.graph),
             },
             "peak_hbm_gb": {"allocated": round(peak_alloc, 2), "reserved": round(peak_res, 2)},
             "step_tc_roofline": {"achieved_tflops": round(step_tc, 1), "peak": tf_sus,
@@ -342,6 +350,8 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-tokens", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="launch eagerly instead of replaying a captured CUDA graph of the step")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
 

@@ -677,9 +677,12 @@ class Trainer:
         torch.cuda.current_stream(self.device).wait_stream(side)
         self._prepare_scalars()
         g = torch.cuda.CUDAGraph()
+        before = N.launch_count()
         with torch.cuda.graph(g):
             self.static_loss = self._compute(self.static_tokens, self.static_targets)
-        self._advance()  # the capture ran the step once
+        self.graph_launches = N.launch_count() - before  # library kernels per replayed step
+        g.replay()  # capture only records: run the captured step once for real
+        self._advance()
         self.graph = g
         return self.static_loss
 
