@@ -248,11 +248,13 @@ int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_
 int poetx_rmsnorm_gather(int64_t T, int64_t d, const void* x, const float* w, float eps, int K,
                          const int32_t* const* idx, void* const* out, float* rstd, void* stream);
 size_t poetx_rmsnorm_gather_bwd_workspace_bytes(int64_t T, int64_t d);
-/* dy = sum_k du[k][:, inv[k]]; dx = RMSNorm backward; dw (+)= sum_t dy x rstd
+/* dy = sum_k du[k][:, inv[k]]; dx = RMSNorm backward (+ dres, the residual
+ * stream's own gradient, when non-NULL); dw (+)= sum_t dy x rstd
  * (deterministic per-CTA partials) */
 int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w, const float* rstd,
-                             int K, const int32_t* const* inv, const void* const* du, void* dx,
-                             float* dw, int accumulate_dw, void* ws, size_t ws_bytes, void* stream);
+                             int K, const int32_t* const* inv, const void* const* du,
+                             const void* dres, void* dx, float* dw, int accumulate_dw, void* ws,
+                             size_t ws_bytes, void* stream);
 /* out[:, j] = silu(vg[:, cg[j]]) * vu[:, cu[j]] */
 int poetx_swiglu_gather(int64_t T, int64_t f, const void* vg, const void* vu, const int32_t* cg,
                         const int32_t* cu, void* out, void* stream);

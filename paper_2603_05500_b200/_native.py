@@ -95,7 +95,7 @@ _SIGS = {
                                      I32, VP, SZ, VP]),
     "poetx_rmsnorm_gather": (I32, [I64, I64, VP, VP, C.c_float, I32, VP, VP, VP, VP]),
     "poetx_rmsnorm_gather_bwd_workspace_bytes": (SZ, [I64, I64]),
-    "poetx_rmsnorm_gather_bwd": (I32, [I64, I64, VP, VP, VP, I32, VP, VP, VP, VP, I32, VP, SZ, VP]),
+    "poetx_rmsnorm_gather_bwd": (I32, [I64, I64, VP, VP, VP, I32, VP, VP, VP, VP, VP, I32, VP, SZ, VP]),
     "poetx_swiglu_gather": (I32, [I64, I64, VP, VP, VP, VP, VP, VP]),
     "poetx_swiglu_gather_bwd": (I32, [I64, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP]),
     "poetx_rope_scatter": (I32, [I64, I64, I64, I64, VP, VP, VP, VP, VP, VP]),

@@ -151,8 +151,8 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_kernel(
 template <int RT>
 __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
     int64_t T, int d, const __nv_bfloat16* __restrict__ x, const float* __restrict__ w,
-    const float* __restrict__ rstd_in, int K, IdxList dus, __nv_bfloat16* __restrict__ dx,
-    float* __restrict__ dw_part) {
+    const float* __restrict__ rstd_in, int K, IdxList dus, const __nv_bfloat16* __restrict__ dres,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ dw_part) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);   // RT rows
   __nv_bfloat16* dus_s = xs + RT * d;                         // K x RT rows
@@ -206,8 +206,10 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
       if (l == 0) red[r * 8 + wp] = v;
     }
     __syncthreads();
-    int slot = 0;
-    for (int i = threadIdx.x; i < nvec; i += kThreads, ++slot) {
+#pragma unroll
+    for (int slot = 0; slot < 2; ++slot) {  // compile-time slot: dwacc stays in registers
+      const int i = threadIdx.x + slot * kThreads;
+      if (i >= nvec) break;
       float wv[8];
       load_f8(w + 8 * i, wv);
       for (int r = 0; r < nr; ++r) {
@@ -216,23 +218,28 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
         for (int k = 0; k < 8; ++k) tot += red[r * 8 + k];
         const float rs = rstd_in[r0 + r];
         const float coef = rs * rs * rs * tot / static_cast<float>(d);
-        float xv[8], o[8];
+        float xv[8], o[8], res[8];
         unpack8(reinterpret_cast<const uint4*>(xs + r * d)[i], xv);
+        if (dres)
+          unpack8(__ldcs(reinterpret_cast<const uint4*>(dres + (r0 + r) * d) + i), res);
         const float4* dyp = reinterpret_cast<const float4*>(dy + r * d + 8 * i);
         const float4 d0 = dyp[0], d1 = dyp[1];
         const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           o[q] = rs * dv[q] * wv[q] - coef * xv[q];
-          if (slot < 2) dwacc[slot][q] += dv[q] * xv[q] * rs;
+          if (dres) o[q] += res[q];  // residual-stream gradient fused (dh = dres + dx)
+          dwacc[slot][q] += dv[q] * xv[q] * rs;
         }
         __stcs(reinterpret_cast<uint4*>(dx + (r0 + r) * d) + i, pack8(o));
       }
     }
     __syncthreads();
   }
-  int slot = 0;
-  for (int i = threadIdx.x; i < nvec && slot < 2; i += kThreads, ++slot) {
+#pragma unroll
+  for (int slot = 0; slot < 2; ++slot) {
+    const int i = threadIdx.x + slot * kThreads;
+    if (i >= nvec) break;
     float4* dst = reinterpret_cast<float4*>(dw_part + static_cast<int64_t>(blockIdx.x) * d + 8 * i);
     dst[0] = make_float4(dwacc[slot][0], dwacc[slot][1], dwacc[slot][2], dwacc[slot][3]);
     dst[1] = make_float4(dwacc[slot][4], dwacc[slot][5], dwacc[slot][6], dwacc[slot][7]);
@@ -522,8 +529,9 @@ size_t poetx_rmsnorm_gather_bwd_workspace_bytes(int64_t T, int64_t d) {
 }
 
 int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w, const float* rstd,
-                             int K, const int32_t* const* inv, const void* const* du, void* dx,
-                             float* dw, int accumulate_dw, void* ws, size_t ws_bytes, void* stream) {
+                             int K, const int32_t* const* inv, const void* const* du,
+                             const void* dres, void* dx, float* dw, int accumulate_dw, void* ws,
+                             size_t ws_bytes, void* stream) {
   POETX_REQUIRE(K >= 1 && K <= kMaxK, POETX_ESHAPE, "rmsnorm_gather_bwd: 1..3 inputs");
   POETX_REQUIRE(d <= 16 * kThreads, POETX_ESHAPE, "rmsnorm_gather_bwd: d > %d", 16 * kThreads);
   POETX_REQUIRE(d % 8 == 0, POETX_ESHAPE, "rmsnorm_gather_bwd: d %% 8");
@@ -540,7 +548,8 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
   float* part = static_cast<float*>(ws);
   POETX_RT_DISPATCH(rt, rmsnorm_gather_bwd_kernel, set_smem(k, smem);
                     k<<<grid, kThreads, smem, st>>>(T, d, static_cast<const __nv_bfloat16*>(x), w, rstd,
-                                                    K, L, static_cast<__nv_bfloat16*>(dx), part));
+                                                    K, L, static_cast<const __nv_bfloat16*>(dres),
+                                                    static_cast<__nv_bfloat16*>(dx), part));
   POETX_LAUNCHED("rmsnorm_gather_bwd");
   colsum_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(grid, d, part, dw, accumulate_dw);
   POETX_LAUNCHED("colsum");

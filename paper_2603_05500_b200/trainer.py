@@ -313,18 +313,23 @@ class _RMSNormGather(torch.autograd.Function):
                _ptrs(outs), rstd.data_ptr(), N.stream_ptr(h.device))
         ctx.invs = invs
         ctx.save_for_backward(h, w, rstd)
-        return tuple(outs)
+        # h is also passed through (the residual stream), so its gradient comes
+        # back here and is added inside the fused backward kernel
+        return tuple(outs) + (h.view_as(h),)
 
     @staticmethod
-    def backward(ctx, *dus):
+    def backward(ctx, *grads):
         h, w, rstd = ctx.saved_tensors
         T, d = h.shape
+        dus, dres = grads[:-1], grads[-1]
         dus = [g.contiguous() for g in dus]
+        dres = None if dres is None else dres.contiguous()
         dx = torch.empty_like(h)
         dw = torch.empty_like(w)
         ws, wsb = N.workspace(N.lib().poetx_rmsnorm_gather_bwd_workspace_bytes(T, d), h.device)
         N.call("poetx_rmsnorm_gather_bwd", T, d, h.data_ptr(), w.data_ptr(), rstd.data_ptr(), len(dus),
-               _ptrs(ctx.invs), _ptrs(dus), dx.data_ptr(), dw.data_ptr(), 0, ws, wsb, N.stream_ptr(h.device))
+               _ptrs(ctx.invs), _ptrs(dus), N.ptr(dres), dx.data_ptr(), dw.data_ptr(), 0, ws, wsb,
+               N.stream_ptr(h.device))
         return dx, dw, None, None
 
 
@@ -537,7 +542,7 @@ class PoetLlama(torch.nn.Module):
         gate, up, down = mods["gate"], mods["up"], mods["down"]
         pin = lambda m: m.pin_dev  # noqa: E731
         pout = lambda m: m.pout_dev  # noqa: E731
-        uq, uk, uv = _RMSNormGather.apply(h, n1, [pin(q)[0], pin(k)[0], pin(v)[0]],
+        uq, uk, uv, h = _RMSNormGather.apply(h, n1, [pin(q)[0], pin(k)[0], pin(v)[0]],
                                           [pin(q)[1], pin(k)[1], pin(v)[1]])
         vq, vk, vv = _PoetRawFn.apply(uq, q), _PoetRawFn.apply(uk, k), _PoetRawFn.apply(uv, v)
         qr = _RopeScatter.apply(vq, pout(q)[1], pout(q)[0], self.cos32, self.sin32, S, H, hd)
@@ -547,7 +552,7 @@ class PoetLlama(torch.nn.Module):
                                            vz.view(B, S, H, hd).transpose(1, 2), is_causal=True)
         uo = _Permute.apply(a.transpose(1, 2).reshape(B * S, d), pin(o)[0], pin(o)[1])
         h = _ScatterAdd.apply(h, _PoetRawFn.apply(uo, o), pout(o)[1], pout(o)[0])
-        ug, uu = _RMSNormGather.apply(h, n2, [pin(gate)[0], pin(up)[0]], [pin(gate)[1], pin(up)[1]])
+        ug, uu, h = _RMSNormGather.apply(h, n2, [pin(gate)[0], pin(up)[0]], [pin(gate)[1], pin(up)[1]])
         ud = _SwiGLUGather.apply(_PoetRawFn.apply(ug, gate), _PoetRawFn.apply(uu, up), self.swiglu_maps[i])
         return _ScatterAdd.apply(h, _PoetRawFn.apply(ud, down), pout(down)[1], pout(down)[0])
 

@@ -120,8 +120,9 @@ def rows():
     dw = torch.empty_like(w)
     ws, wsb = N.workspace(N.lib().poetx_rmsnorm_gather_bwd_workspace_bytes(T, d))
     ms = timeit(lambda: N.call("poetx_rmsnorm_gather_bwd", T, d, x.data_ptr(), w.data_ptr(), rstd.data_ptr(), 3,
-                               _ptrs(perms), _ptrs(outs), dx.data_ptr(), dw.data_ptr(), 0, ws, wsb, st))
-    print(f"rmsnorm_gather_bwd K=3: {ms * 1e3:.1f} us  {5 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
+                               _ptrs(perms), _ptrs(outs), outs[1].data_ptr(), dx.data_ptr(), dw.data_ptr(), 0,
+                               ws, wsb, st))
+    print(f"rmsnorm_gather_bwd K=3 (+dres): {ms * 1e3:.1f} us  {6 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
     vg = torch.randn((T, f), device=dev).bfloat16()
     vu = torch.randn_like(vg)
     o = torch.empty_like(vg)
