@@ -47,11 +47,20 @@ namespace tc {
 constexpr int THREADS = 256;
 constexpr int A_BYTES = BM * BK * 2;  // 16 KB
 
-template <int BN> struct Cfg {
+// MS = number of 128-row M sub-tiles per CTA tile sharing each B stage
+// (MS = 2 halves the B operand traffic of tall-K, small-N problems such as
+// the segmented outer product).
+template <int BN, int MS> struct Cfg {
+  static constexpr int A_BYTES_T = MS * A_BYTES;
   static constexpr int B_BYTES = BN * BK * 2;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int STAGES = (BN == 256) ? 4 : (BN == 128 ? 6 : 8);
-  static constexpr int TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  static constexpr int STAGE_BYTES = A_BYTES_T + B_BYTES;
+  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int ACC_COLS = MS * BN;                 // one accumulator (all sub-tiles)
+  static constexpr int NACC = (2 * ACC_COLS <= 512) ? 2 : 1;
+  static constexpr int TMEM_NEED = NACC * ACC_COLS;
+  static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128
+                                 : TMEM_NEED <= 256 ? 256 : 512;
   static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
@@ -68,19 +77,19 @@ struct Args {
 };
 
 // ------------------------------------------------------------------ kernel --
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int MS>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
               Args args) {
-  using CF = Cfg<BN>;
-  constexpr int STAGES = CF::STAGES;
+  using CF = Cfg<BN, MS>;
+  constexpr int STAGES = CF::STAGES, NACC = CF::NACC, TM = BM * MS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
   uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;  // [2]
-  uint64_t* tempty = tfull + 2;      // [2]
+  uint64_t* tfull = empty + STAGES;  // [NACC]
+  uint64_t* tempty = tfull + 2;      // [NACC]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -92,7 +101,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < NACC; ++a) {
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], 4);  // one arrive per epilogue warp
     }
@@ -116,7 +125,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     int r = tile % (tiles_per_split * args.splits);
     s = r / tiles_per_split;
     r %= tiles_per_split;
-    m0 = (r / args.n_tiles) * BM;
+    m0 = (r / args.n_tiles) * TM;
     n0 = (r % args.n_tiles) * BN;
     int k0 = s * args.kps;
     int k1 = k0 + args.kps < args.K ? k0 + args.kps : args.K;
@@ -139,12 +148,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int kb = kb0; kb < kb0 + kbn; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * CF::STAGE_BYTES;
-          uint8_t* sb = sa + A_BYTES;
+          uint8_t* sb = sa + CF::A_BYTES_T;
           const int k = kb * BK;
           mbar_expect_tx(&full[stage], CF::STAGE_BYTES);
           if constexpr (A_MN) {
 #pragma unroll
-            for (int j = 0; j < BM / 64; ++j)
+            for (int j = 0; j < TM / 64; ++j)
               tma_load_2d(sa + j * (BK * 128), &map_a, &full[stage], ag0 + m0 + j * 64, ag1 + k);
           } else {
             tma_load_2d(sa, &map_a, &full[stage], ag0 + k, ag1 + m0);
@@ -172,17 +181,21 @@ __global__ void __launch_bounds__(THREADS, 1)
       decode(tile, g, s, m0, n0, kb0, kbn);
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       fence_after();
-      const uint32_t tmem_d = tmem_base + acc * BN;
+      const uint32_t tmem_d = tmem_base + acc * CF::ACC_COLS;
       for (int kb = 0; kb < kbn; ++kb) {
         mbar_wait(&full[stage], phase);
         fence_after();
         if (lane == 0) {
           const uint32_t a_addr = smem_u32(smem + stage * CF::STAGE_BYTES);
-          const uint32_t b_addr = a_addr + A_BYTES;
+          const uint32_t b_addr = a_addr + CF::A_BYTES_T;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16(tmem_d, operand_desc<A_MN>(a_addr, k), operand_desc<B_MN>(b_addr, k), idesc,
-                      (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t bd = operand_desc<B_MN>(b_addr, k);
+#pragma unroll
+            for (int ms = 0; ms < MS; ++ms)  // 128-row sub-tile ms: +16 KB in either major
+              umma_bf16(tmem_d + ms * BN, operand_desc<A_MN>(a_addr + ms * A_BYTES, k), bd, idesc,
+                        (kb | k) != 0);
+          }
           umma_commit(&empty[stage]);  // smem stage free once these MMAs retire
           if (kb == kbn - 1) umma_commit(&tfull[acc]);
         }
@@ -191,7 +204,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (kbn == 0 && lane == 0) umma_commit(&tfull[acc]);  // empty K range
       __syncwarp();
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
     }
   } else if (warp >= 4) {
     // ===================== epilogue =====================
@@ -203,45 +216,48 @@ __global__ void __launch_bounds__(THREADS, 1)
       decode(tile, g, s, m0, n0, kb0, kbn);
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
-      const int row = m0 + ew * 32 + lane;
-      const int64_t base = g * args.c_goff + s * args.c_soff + static_cast<int64_t>(row) * args.ldc;
-      const bool row_ok = row < args.M;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c, r);
-        if (kbn == 0) {
+      for (int ms = 0; ms < MS; ++ms) {
+        const int row = m0 + ms * BM + ew * 32 + lane;
+        const int64_t base = g * args.c_goff + s * args.c_soff + static_cast<int64_t>(row) * args.ldc;
+        const bool row_ok = row < args.M;
+#pragma unroll 1
+        for (int c = 0; c < BN; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * CF::ACC_COLS + ms * BN + c, r);
+          if (kbn == 0) {
 #pragma unroll
-          for (int q = 0; q < 32; ++q) r[q] = 0u;
-        }
-        if (args.alpha != 1.0f) {
+            for (int q = 0; q < 32; ++q) r[q] = 0u;
+          }
+          if (args.alpha != 1.0f) {
 #pragma unroll
-          for (int q = 0; q < 32; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * args.alpha);
-        }
-        if (row_ok && n0 + c < args.N) {
-          if (args.out_f32) {
-            float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.C) + base + n0 + c);
+            for (int q = 0; q < 32; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * args.alpha);
+          }
+          if (row_ok && n0 + c < args.N) {
+            if (args.out_f32) {
+              float4* dst = reinterpret_cast<float4*>(static_cast<float*>(args.C) + base + n0 + c);
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
-              float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                     __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-              if (args.accumulate) {
-                const float4 o = dst[q];
-                v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+              for (int q = 0; q < 8; ++q) {
+                float4 v = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                       __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                if (args.accumulate) {
+                  const float4 o = dst[q];
+                  v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+                }
+                dst[q] = v;
               }
-              dst[q] = v;
-            }
-          } else {
-            uint4* dst =
-                reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + base + n0 + c);
+            } else {
+              uint4* dst =
+                  reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(args.C) + base + n0 + c);
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              uint4 v;
-              v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
-              v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
-              v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
-              v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
-              dst[q] = v;
+              for (int q = 0; q < 4; ++q) {
+                uint4 v;
+                v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
+                v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
+                v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
+                v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
+                dst[q] = v;
+              }
             }
           }
         }
@@ -249,7 +265,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
     }
   }
 
@@ -320,32 +336,36 @@ int num_sms() {
   return n;
 }
 
-template <int BN, bool A_MN, bool B_MN>
+template <int BN, bool A_MN, bool B_MN, int MS>
 int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Args& a, const char* name,
              cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(tc_kernel<BN, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         Cfg<BN>::SMEM_BYTES);
+    cudaFuncSetAttribute(tc_kernel<BN, A_MN, B_MN, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         Cfg<BN, MS>::SMEM_BYTES);
     attr_set = true;
   }
   int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles * a.splits * a.groups;
   int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
   if (grid <= 0) return POETX_OK;
   void* tok = prof_begin(st);
-  tc_kernel<BN, A_MN, B_MN><<<grid, THREADS, Cfg<BN>::SMEM_BYTES, st>>>(ma, mb, a);
+  tc_kernel<BN, A_MN, B_MN, MS><<<grid, THREADS, Cfg<BN, MS>::SMEM_BYTES, st>>>(ma, mb, a);
   prof_end(tok, name, 2.0 * a.M * a.N * static_cast<double>(a.K) * a.groups, st);
   POETX_LAUNCHED(name);
   return POETX_OK;
 }
 
 template <int BN>
-int launch_bn(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const Args& a,
-              const char* name, cudaStream_t st) {
-  if (!a_mn && !b_mn) return launch_t<BN, false, false>(ma, mb, a, name, st);
-  if (!a_mn && b_mn) return launch_t<BN, false, true>(ma, mb, a, name, st);
-  if (a_mn && !b_mn) return launch_t<BN, true, false>(ma, mb, a, name, st);
-  return launch_t<BN, true, true>(ma, mb, a, name, st);
+int launch_bn(bool a_mn, bool b_mn, int ms, const CUtensorMap& ma, const CUtensorMap& mb,
+              const Args& a, const char* name, cudaStream_t st) {
+  if (ms == 2) {
+    if (a_mn && b_mn) return launch_t<BN, true, true, 2>(ma, mb, a, name, st);
+    return POETX_ENOTSUPPORTED;
+  }
+  if (!a_mn && !b_mn) return launch_t<BN, false, false, 1>(ma, mb, a, name, st);
+  if (!a_mn && b_mn) return launch_t<BN, false, true, 1>(ma, mb, a, name, st);
+  if (a_mn && !b_mn) return launch_t<BN, true, false, 1>(ma, mb, a, name, st);
+  return launch_t<BN, true, true, 1>(ma, mb, a, name, st);
 }
 
 }  // namespace tc
@@ -364,7 +384,8 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
     return POETX_ENOTSUPPORTED;
   if (p.N % 32) return POETX_ENOTSUPPORTED;
   CUtensorMap ma, mb;
-  POETX_TRY(make_map(&ma, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : BM));
+  const int ms = p.ms == 2 ? 2 : 1;
+  POETX_TRY(make_map(&ma, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : BM * ms));
   POETX_TRY(make_map(&mb, B.ptr, B.cols, B.rows, B.pitch, 64, B.mn_major ? BK : BN));
   Args a{};
   a.M = static_cast<int>(p.M);
@@ -375,7 +396,7 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
   int64_t kps = (p.K + a.splits - 1) / a.splits;
   kps = (kps + BK - 1) / BK * BK;
   a.kps = static_cast<int>(kps > 0 ? kps : BK);
-  a.m_tiles = static_cast<int>((p.M + BM - 1) / BM);
+  a.m_tiles = static_cast<int>((p.M + BM * ms - 1) / (BM * ms));
   a.n_tiles = static_cast<int>((p.N + BN - 1) / BN);
   a.a_g0 = p.a_g0; a.a_g1 = p.a_g1; a.b_g0 = p.b_g0; a.b_g1 = p.b_g1;
   a.C = p.C;
@@ -385,9 +406,9 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
   if (p.accumulate && !p.out_f32) return POETX_ENOTSUPPORTED;
   a.alpha = p.alpha;
   const char* name = p.name ? p.name : "tc_gemm";
-  if (BN == 256) return launch_bn<256>(A.mn_major, B.mn_major, ma, mb, a, name, st);
-  if (BN == 128) return launch_bn<128>(A.mn_major, B.mn_major, ma, mb, a, name, st);
-  return launch_bn<64>(A.mn_major, B.mn_major, ma, mb, a, name, st);
+  if (BN == 256) return launch_bn<256>(A.mn_major, B.mn_major, ms, ma, mb, a, name, st);
+  if (BN == 128) return launch_bn<128>(A.mn_major, B.mn_major, ms, ma, mb, a, name, st);
+  return launch_bn<64>(A.mn_major, B.mn_major, ms, ma, mb, a, name, st);
 }
 
 int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
@@ -422,7 +443,8 @@ size_t tc_outer_ws_bytes(int64_t T, int64_t nb, int64_t b) {
 
 int tc_outer_splits(int64_t T, int64_t nb, int64_t b) {
   int64_t bn = b < 256 ? b : 256;
-  int64_t tiles = nb * ((b + 127) / 128) * ((b + bn - 1) / bn);
+  int64_t tm = b >= 256 ? 256 : 128;  // two M sub-tiles per CTA for b = 256
+  int64_t tiles = nb * ((b + tm - 1) / tm) * ((b + bn - 1) / bn);
   // one wave of persistent CTAs: fewer fp32 partials to write and reduce
   int64_t want = 148 / tiles;
   int64_t maxs = (T + 511) / 512;

@@ -34,6 +34,7 @@ struct TcProblem {
   int accumulate;  // fp32 output only: C += alpha * AB
   float alpha;
   const char* name;
+  int ms;  // 2: two 128-row M sub-tiles per CTA share each B stage (A and B MN-major)
 };
 
 int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaStream_t st);
