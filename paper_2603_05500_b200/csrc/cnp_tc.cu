@@ -111,7 +111,7 @@ TcProblem stack_problem(int64_t nb, int64_t b, int64_t N, void* C, int64_t ldc, 
   p.a_g1 = static_cast<int>(b);
   p.b_g1 = static_cast<int>(b);
   p.C = C; p.ldc = ldc; p.c_goff = c_goff;
-  p.out_f32 = out_f32; p.accumulate = accumulate; p.alpha = alpha; p.name = name;
+  p.out_f32 = out_f32; p.accumulate = accumulate; p.alpha = alpha; p.name = name; p.tma_epi = 1;
   return p;
 }
 

@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstring>
 #include <mutex>
 
 #include "tc_common.cuh"
@@ -54,14 +55,15 @@ template <int BN, int MS> struct Cfg {
   static constexpr int A_BYTES_T = MS * A_BYTES;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE_BYTES = A_BYTES_T + B_BYTES;
-  static constexpr int STAGES_RAW = (196 * 1024) / STAGE_BYTES;
+  static constexpr int STAGES_RAW = (192 * 1024) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+  static constexpr int EPI_BYTES = 4 * 2 * 32 * 128;  // per warp: 2 x (32 rows x 128 B)
   static constexpr int ACC_COLS = MS * BN;                 // one accumulator (all sub-tiles)
   static constexpr int NACC = (2 * ACC_COLS <= 512) ? 2 : 1;
   static constexpr int TMEM_NEED = NACC * ACC_COLS;
   static constexpr int TMEM_COLS = TMEM_NEED <= 32 ? 32 : TMEM_NEED <= 64 ? 64 : TMEM_NEED <= 128 ? 128
                                  : TMEM_NEED <= 256 ? 256 : 512;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 + 256;
 };
 
 struct Args {
@@ -74,19 +76,23 @@ struct Args {
   int out_f32;
   int accumulate;  // fp32 output only: C += alpha * AB
   float alpha;
+  int tma_epi;     // 1: epilogue through smem staging + TMA bulk store (reduce-add if accumulate)
+  int64_t c_row0;  // row of C (in map_c) where group 0 / split 0 starts ... per-group/split rows:
+  int64_t c_grow, c_srow;
 };
 
 // ------------------------------------------------------------------ kernel --
 template <int BN, bool A_MN, bool B_MN, int MS>
 __global__ void __launch_bounds__(THREADS, 1)
     tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-              Args args) {
+              const __grid_constant__ CUtensorMap map_c, Args args) {
   using CF = Cfg<BN, MS>;
   constexpr int STAGES = CF::STAGES, NACC = CF::NACC, TM = BM * MS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * CF::STAGE_BYTES);
+  uint8_t* epi = smem + STAGES * CF::STAGE_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + CF::EPI_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;  // [NACC]
   uint64_t* tempty = tfull + 2;      // [NACC]
@@ -209,6 +215,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp >= 4) {
     // ===================== epilogue =====================
     const int ew = warp - 4;  // TMEM lanes 32*ew .. 32*ew+31
+    uint8_t* stg = epi + ew * (2 * 32 * 128);
+    int buf = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
@@ -218,13 +226,62 @@ __global__ void __launch_bounds__(THREADS, 1)
       fence_after();
 #pragma unroll 1
       for (int ms = 0; ms < MS; ++ms) {
-        const int row = m0 + ms * BM + ew * 32 + lane;
+        const int row0 = m0 + ms * BM + ew * 32;  // this warp's 32 rows
+        const int row = row0 + lane;
+        const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * CF::ACC_COLS + ms * BN;
+        if (args.tma_epi) {
+          // TMEM -> regs -> 128B-swizzled smem (32 rows x 128 B) -> TMA bulk store
+          const bool rows_ok = row0 < args.M;  // M % 32 == 0 on this path
+          const int64_t crow = args.c_row0 + g * args.c_grow + s * args.c_srow + row0;
+          const int step = args.out_f32 ? 32 : 64;
+#pragma unroll 1
+          for (int c = 0; c < BN; c += step) {
+            uint32_t r[64];
+            tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+            if (!args.out_f32) tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+            if (kbn == 0) {
+#pragma unroll
+              for (int q = 0; q < 64; ++q) r[q] = 0u;
+            }
+            if (args.alpha != 1.0f) {
+#pragma unroll
+              for (int q = 0; q < 64; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * args.alpha);
+            }
+            if (lane == 0) bulk_wait_read<1>();  // staging buffer `buf` free again
+            __syncwarp();
+            uint8_t* rowp = stg + buf * (32 * 128) + lane * 128;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              uint4 v;
+              if (args.out_f32) {
+                v = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+              } else {
+                v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
+                v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
+                v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
+                v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
+              }
+              *reinterpret_cast<uint4*>(rowp + ((q ^ (lane & 7)) * 16)) = v;
+            }
+            fence_async_smem();
+            __syncwarp();
+            if (lane == 0 && rows_ok && n0 + c < args.N) {
+              if (args.accumulate)
+                tma_reduce_add_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
+              else
+                tma_store_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
+            }
+            if (lane == 0) bulk_commit();
+            buf ^= 1;
+          }
+          continue;
+        }
         const int64_t base = g * args.c_goff + s * args.c_soff + static_cast<int64_t>(row) * args.ldc;
         const bool row_ok = row < args.M;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t r[32];
-          tmem_ld32(tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * CF::ACC_COLS + ms * BN + c, r);
+          tmem_ld32(tbase + c, r);
           if (kbn == 0) {
 #pragma unroll
             for (int q = 0; q < 32; ++q) r[q] = 0u;
@@ -267,6 +324,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lane == 0) mbar_arrive(&tempty[acc]);
       if (++acc == NACC) { acc = 0; acc_phase ^= 1; }
     }
+    if (lane == 0) bulk_wait<0>();  // bulk stores finished reading smem (and landed)
   }
 
   fence_before();
@@ -337,8 +395,8 @@ int num_sms() {
 }
 
 template <int BN, bool A_MN, bool B_MN, int MS>
-int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Args& a, const char* name,
-             cudaStream_t st) {
+int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& a,
+             const char* name, cudaStream_t st) {
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(tc_kernel<BN, A_MN, B_MN, MS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -349,7 +407,7 @@ int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Args& a, const 
   int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
   if (grid <= 0) return POETX_OK;
   void* tok = prof_begin(st);
-  tc_kernel<BN, A_MN, B_MN, MS><<<grid, THREADS, Cfg<BN, MS>::SMEM_BYTES, st>>>(ma, mb, a);
+  tc_kernel<BN, A_MN, B_MN, MS><<<grid, THREADS, Cfg<BN, MS>::SMEM_BYTES, st>>>(ma, mb, mc, a);
   prof_end(tok, name, 2.0 * a.M * a.N * static_cast<double>(a.K) * a.groups, st);
   POETX_LAUNCHED(name);
   return POETX_OK;
@@ -357,15 +415,15 @@ int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const Args& a, const 
 
 template <int BN>
 int launch_bn(bool a_mn, bool b_mn, int ms, const CUtensorMap& ma, const CUtensorMap& mb,
-              const Args& a, const char* name, cudaStream_t st) {
+              const CUtensorMap& mc, const Args& a, const char* name, cudaStream_t st) {
   if (ms == 2) {
-    if (a_mn && b_mn) return launch_t<BN, true, true, 2>(ma, mb, a, name, st);
+    if (a_mn && b_mn) return launch_t<BN, true, true, 2>(ma, mb, mc, a, name, st);
     return POETX_ENOTSUPPORTED;
   }
-  if (!a_mn && !b_mn) return launch_t<BN, false, false, 1>(ma, mb, a, name, st);
-  if (!a_mn && b_mn) return launch_t<BN, false, true, 1>(ma, mb, a, name, st);
-  if (a_mn && !b_mn) return launch_t<BN, true, false, 1>(ma, mb, a, name, st);
-  return launch_t<BN, true, true, 1>(ma, mb, a, name, st);
+  if (!a_mn && !b_mn) return launch_t<BN, false, false, 1>(ma, mb, mc, a, name, st);
+  if (!a_mn && b_mn) return launch_t<BN, false, true, 1>(ma, mb, mc, a, name, st);
+  if (a_mn && !b_mn) return launch_t<BN, true, false, 1>(ma, mb, mc, a, name, st);
+  return launch_t<BN, true, true, 1>(ma, mb, mc, a, name, st);
 }
 
 }  // namespace tc
@@ -404,11 +462,26 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
   a.out_f32 = p.out_f32;
   a.accumulate = p.accumulate;
   if (p.accumulate && !p.out_f32) return POETX_ENOTSUPPORTED;
+  // TMA-store epilogue when every (group, split) block of C starts on a row of
+  // one 2-D view of C and rows come in whole 32-row warp chunks
+  CUtensorMap mc;
+  memset(&mc, 0, sizeof(mc));
+  a.tma_epi = 0;
+  if (p.tma_epi && p.M % 32 == 0 && p.c_goff % p.ldc == 0 && p.c_soff % p.ldc == 0 &&
+      (p.ldc * (p.out_f32 ? 4 : 2)) % 16 == 0) {
+    a.c_row0 = 0;
+    a.c_grow = p.c_goff / p.ldc;
+    a.c_srow = p.c_soff / p.ldc;
+    const int64_t rows = (p.groups - 1) * a.c_grow + (a.splits - 1) * a.c_srow + p.M;
+    int rc = p.out_f32 ? make_map_f32(&mc, p.C, p.N, rows, p.ldc, 32, 32)
+                       : make_map(&mc, p.C, p.N, rows, p.ldc, 64, 32);
+    if (rc == POETX_OK) a.tma_epi = 1;
+  }
   a.alpha = p.alpha;
   const char* name = p.name ? p.name : "tc_gemm";
-  if (BN == 256) return launch_bn<256>(A.mn_major, B.mn_major, ms, ma, mb, a, name, st);
-  if (BN == 128) return launch_bn<128>(A.mn_major, B.mn_major, ms, ma, mb, a, name, st);
-  return launch_bn<64>(A.mn_major, B.mn_major, ms, ma, mb, a, name, st);
+  if (BN == 256) return launch_bn<256>(A.mn_major, B.mn_major, ms, ma, mb, mc, a, name, st);
+  if (BN == 128) return launch_bn<128>(A.mn_major, B.mn_major, ms, ma, mb, mc, a, name, st);
+  return launch_bn<64>(A.mn_major, B.mn_major, ms, ma, mb, mc, a, name, st);
 }
 
 int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
@@ -421,7 +494,7 @@ int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int t
   TcOperand b{B, transB ? N : K, transB ? K : N, ldb, transB == 0};
   TcProblem p{};
   p.M = M; p.N = N; p.K = K; p.groups = 1; p.splits = 1; p.bn = 256;
-  p.C = C; p.ldc = ldc; p.alpha = 1.0f; p.name = "tc_gemm";
+  p.C = C; p.ldc = ldc; p.alpha = 1.0f; p.name = "tc_gemm"; p.tma_epi = 1;
   return tc_grouped(a, b, p, st);
 }
 

@@ -35,6 +35,7 @@ struct TcProblem {
   float alpha;
   const char* name;
   int ms;  // 2: two 128-row M sub-tiles per CTA share each B stage (A and B MN-major)
+  int tma_epi;  // 1: stage the epilogue in smem and write C with TMA bulk stores
 };
 
 int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaStream_t st);
