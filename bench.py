@@ -186,7 +186,7 @@ def run_ours(args, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    pg = dist.group.WORLD if world > 1 else None
+    pg = dist.group.WORLD if dist.is_initialized() else None
     cfg = llama_config(args.model, variant=args.variant)
     trainer = Trainer(cfg, args.micro_batch, seed=args.seed, merge_gap=args.merge_gap, device=dev, pg=pg)
     B, S = args.micro_batch, cfg.seq
@@ -196,7 +196,7 @@ def run_ours(args, rank, world, local_rank):
     loss_host = torch.empty((), dtype=torch.float32).pin_memory()
 
     def barrier():
-        if world > 1:
+        if pg is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
@@ -221,7 +221,7 @@ def run_ours(args, rank, world, local_rank):
         launches = N.launch_count() - launches0
         if trainer.graph is not None:
             launches += n * trainer.graph_launches  # kernels inside each graph replay
-        if world > 1:
+        if pg is not None:
             t = torch.tensor([ms], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ms = float(t.item())
@@ -229,6 +229,9 @@ def run_ours(args, rank, world, local_rank):
 
     for i in range(args.warmup):
         trainer.step(dev_batches[i % 4][:, :-1], dev_batches[i % 4][:, 1:])
+    # graph capture of the single-GPU step; with NCCL all-reduces in the step
+    # the eager path is used (collectives are issued by torch.distributed)
+    args.graph = args.graph and pg is None
     if args.graph:
         tb = dev_batches[0]
         trainer.capture(tb[:, :-1], tb[:, 1:])
@@ -365,7 +368,8 @@ def main():
         print(json.dumps(run_reference(args)), flush=True)
         return
 
-    if world > 1:
+    distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ  # torchrun, even at N=1
+    if distributed:
         import torch
         import torch.distributed as dist
 
@@ -380,7 +384,7 @@ def main():
             out["cpu_baseline"] = {"value": round(v, 4), "unit": UNIT, "cores": procs, "kind": "port",
                                    "sample": sample}
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if distributed:
         import torch.distributed as dist
 
         dist.barrier()

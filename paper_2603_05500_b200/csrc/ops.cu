@@ -583,7 +583,7 @@ int segmented_outer(int dt, int64_t T, int64_t nb, int64_t b, const void* x, con
     p.a_g0 = static_cast<int>(b); p.b_g0 = static_cast<int>(b);
     p.C = tgt; p.ldc = b; p.c_goff = b * b; p.c_soff = total; p.out_f32 = 1; p.alpha = 1.0f;
     p.name = "tc_outer";
-    p.ms = b >= 256 ? 2 : 1;  // M = 256 per CTA: the B operand is read once per block
+    p.ms = 1;  // (ms = 2 halves B traffic but doubles split-K partials: measured slower)
     p.tma_epi = 1;
     int rc = tc_grouped(xa, yb, p, st);
     if (rc != POETX_ENOTSUPPORTED) {

@@ -516,7 +516,7 @@ size_t tc_outer_ws_bytes(int64_t T, int64_t nb, int64_t b) {
 
 int tc_outer_splits(int64_t T, int64_t nb, int64_t b) {
   int64_t bn = b < 256 ? b : 256;
-  int64_t tm = b >= 256 ? 256 : 128;  // two M sub-tiles per CTA for b = 256
+  int64_t tm = 128;
   int64_t tiles = nb * ((b + tm - 1) / tm) * ((b + bn - 1) / bn);
   // one wave of persistent CTAs: fewer fp32 partials to write and reduce
   int64_t want = 148 / tiles;
