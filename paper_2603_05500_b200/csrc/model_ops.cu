@@ -87,10 +87,12 @@ __device__ __forceinline__ uint4 pack8(const float (&v)[8]) {
 }
 __device__ __forceinline__ float sigmoid_f(float v) { return __frcp_rn(1.f + __expf(-v)); }
 
-template <int RT>
+// K (number of consumers) is a template parameter: the IdxList entries and
+// per-consumer index registers must be compile-time indexed (else local memory)
+template <int RT, int K>
 __global__ void __launch_bounds__(kThreads) rmsnorm_gather_kernel(
     int64_t T, int d, const __nv_bfloat16* __restrict__ x, const float* __restrict__ w,
-    float eps, int K, IdxList outs, float* __restrict__ rstd_out) {
+    float eps, IdxList outs, float* __restrict__ rstd_out) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);
   float* rstd_s = reinterpret_cast<float*>(sm + RT * d * 2);
@@ -128,6 +130,7 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_kernel(
     }
     if (threadIdx.x < nr) rstd_out[r0 + threadIdx.x] = rstd_s[threadIdx.x];
     __syncthreads();
+#pragma unroll
     for (int k = 0; k < K; ++k) {
       __nv_bfloat16* o = static_cast<__nv_bfloat16*>(outs.ptr[k]) + r0 * d;
       for (int i = threadIdx.x; i < nvec; i += kThreads) {
@@ -148,10 +151,10 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_kernel(
 
 // dy = sum_k du_k[:, inv_k]; g = dy*w ; dx = rstd*g - rstd^3 x (g.x)/d ;
 // dw partial[c] += dy*x*rstd  (per CTA, reduced later in fixed order)
-template <int RT>
+template <int RT, int K>
 __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
     int64_t T, int d, const __nv_bfloat16* __restrict__ x, const float* __restrict__ w,
-    const float* __restrict__ rstd_in, int K, IdxList dus, const __nv_bfloat16* __restrict__ dres,
+    const float* __restrict__ rstd_in, IdxList dus, const __nv_bfloat16* __restrict__ dres,
     __nv_bfloat16* __restrict__ dx, float* __restrict__ dw_part) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* xs = reinterpret_cast<__nv_bfloat16*>(sm);   // RT rows
@@ -167,6 +170,7 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
     const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
     stage_rows(xs, x + r0 * d, nr, d);
+#pragma unroll
     for (int k = 0; k < K; ++k)
       stage_rows(dus_s + k * RT * d, static_cast<const __nv_bfloat16*>(dus.ptr[k]) + r0 * d, nr, d);
     cp_wait_all();
@@ -175,7 +179,8 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
 #pragma unroll
     for (int r = 0; r < RT; ++r) dot[r] = 0.f;
     for (int i = threadIdx.x; i < nvec; i += kThreads) {
-      int iv[kMaxK][8];
+      int iv[K][8];
+#pragma unroll
       for (int k = 0; k < K; ++k) load_idx8(dus.idx[k], 8 * i, iv[k]);
       float wv[8];
       load_f8(w + 8 * i, wv);
@@ -185,6 +190,7 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
         float s[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) s[q] = 0.f;
+#pragma unroll
         for (int k = 0; k < K; ++k) {
           const __nv_bfloat16* row = dus_s + (k * RT + r) * d;
 #pragma unroll
@@ -491,6 +497,19 @@ unsigned row_grid(int64_t T, int rt) {
     case 2: { auto k = KERNEL<2>; __VA_ARGS__; break; }       \
     default: { auto k = KERNEL<1>; __VA_ARGS__; break; }      \
   }
+#define POETX_RT_DISPATCH_K(rt, KK, KERNEL, ...)              \
+  switch (rt) {                                               \
+    case 8: { auto k = KERNEL<8, KK>; __VA_ARGS__; break; }   \
+    case 4: { auto k = KERNEL<4, KK>; __VA_ARGS__; break; }   \
+    case 2: { auto k = KERNEL<2, KK>; __VA_ARGS__; break; }   \
+    default: { auto k = KERNEL<1, KK>; __VA_ARGS__; break; }  \
+  }
+#define POETX_K_DISPATCH(K, rt, KERNEL, ...)                                          \
+  switch (K) {                                                                        \
+    case 1: POETX_RT_DISPATCH_K(rt, 1, KERNEL, __VA_ARGS__) break;                    \
+    case 2: POETX_RT_DISPATCH_K(rt, 2, KERNEL, __VA_ARGS__) break;                    \
+    default: POETX_RT_DISPATCH_K(rt, 3, KERNEL, __VA_ARGS__) break;                   \
+  }
 
 template <typename K>
 void set_smem(K kernel, size_t smem) {
@@ -514,9 +533,9 @@ int poetx_rmsnorm_gather(int64_t T, int64_t d, const void* x, const float* w, fl
   if (T == 0) return POETX_OK;
   IdxList L{};
   for (int k = 0; k < K; ++k) { L.idx[k] = idx[k]; L.ptr[k] = out[k]; }
-  POETX_RT_DISPATCH(rt, rmsnorm_gather_kernel, set_smem(k, smem);
-                    k<<<row_grid(T, rt), kThreads, smem, as_stream(stream)>>>(
-                        T, d, static_cast<const __nv_bfloat16*>(x), w, eps, K, L, rstd));
+  POETX_K_DISPATCH(K, rt, rmsnorm_gather_kernel, set_smem(k, smem);
+                   k<<<row_grid(T, rt), kThreads, smem, as_stream(stream)>>>(
+                       T, d, static_cast<const __nv_bfloat16*>(x), w, eps, L, rstd);)
   POETX_LAUNCHED("rmsnorm_gather");
   return POETX_OK;
 }
@@ -546,10 +565,10 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
   for (int k = 0; k < K; ++k) { L.idx[k] = inv[k]; L.ptr[k] = const_cast<void*>(du[k]); }
   cudaStream_t st = as_stream(stream);
   float* part = static_cast<float*>(ws);
-  POETX_RT_DISPATCH(rt, rmsnorm_gather_bwd_kernel, set_smem(k, smem);
-                    k<<<grid, kThreads, smem, st>>>(T, d, static_cast<const __nv_bfloat16*>(x), w, rstd,
-                                                    K, L, static_cast<const __nv_bfloat16*>(dres),
-                                                    static_cast<__nv_bfloat16*>(dx), part));
+  POETX_K_DISPATCH(K, rt, rmsnorm_gather_bwd_kernel, set_smem(k, smem);
+                   k<<<grid, kThreads, smem, st>>>(T, d, static_cast<const __nv_bfloat16*>(x), w, rstd,
+                                                   L, static_cast<const __nv_bfloat16*>(dres),
+                                                   static_cast<__nv_bfloat16*>(dx), part);)
   POETX_LAUNCHED("rmsnorm_gather_bwd");
   colsum_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(grid, d, part, dw, accumulate_dw);
   POETX_LAUNCHED("colsum");
