@@ -102,6 +102,14 @@ def hbm():
 
 
 def rows():
+    for on in (1, 0):
+        N.lib().poetx_set_rowpipe_enabled(on)
+        print("-- rowpipe", "on" if on else "off (staged kernels)")
+        _rows()
+    N.lib().poetx_set_rowpipe_enabled(1)
+
+
+def _rows():
     import ctypes as C
     from paper_2603_05500_b200.trainer import _ptrs
     print("== fused row kernels (bf16, T=8192) ==", os.environ.get("POETX_ROW_TILE_KB", "48"), "KB tiles")
