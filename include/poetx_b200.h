@@ -62,10 +62,6 @@ uint64_t poetx_launch_count(void);
 /* 1 if the tcgen05/TMA GEMM path is compiled in and enabled */
 int poetx_tc_enabled(void);
 void poetx_set_tc_enabled(int on);
-/* 1 if the persistent TMA-bulk row kernels (row_pipe.cu) serve the fused
- * row operators; 0 selects the simple staged kernels (testing) */
-int poetx_rowpipe_enabled(void);
-void poetx_set_rowpipe_enabled(int on);
 /* device timing hooks: while enabled, tensor-core kernel launches are
  * bracketed by CUDA events on their stream; query sums durations (ms),
  * launch count and algorithmic FLOPs per kernel name ("tc_gemm", ...). */

@@ -17,12 +17,8 @@
 #include <cstdlib>
 
 #include "common.cuh"
-#include "row_pipe.cuh"
 
 namespace poetx {
-namespace tc {
-int num_sms();
-}
 namespace {
 
 constexpr int kThreads = 256;
@@ -548,9 +544,7 @@ static int bwd_rt(int64_t d, int K) { return pick_rt(d * 2 * (1 + K) + d * 4); }
 
 size_t poetx_rmsnorm_gather_bwd_workspace_bytes(int64_t T, int64_t d) {
   int rt = bwd_rt(d, 1);  // largest grid over K
-  int64_t rows = row_grid(T, rt);
-  if (rows < 2 * tc::num_sms()) rows = 2 * tc::num_sms();  // persistent pipelined kernel
-  return static_cast<size_t>(rows) * d * 4 + 256;
+  return static_cast<size_t>(row_grid(T, rt)) * d * 4 + 256;
 }
 
 int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w, const float* rstd,
@@ -569,16 +563,6 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
                 "rmsnorm_gather_bwd: workspace too small");
   cudaStream_t st = as_stream(stream);
   float* part = static_cast<float*>(ws);
-  {
-    int pg = 0;
-    int rc = rowpipe_rmsnorm_gather_bwd(T, d, x, w, rstd, K, inv, du, dres, dx, part, ws_bytes / (d * 4), &pg, st);
-    if (rc == POETX_OK) {
-      colsum_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(pg, d, part, dw, accumulate_dw);
-      POETX_LAUNCHED("colsum");
-      return POETX_OK;
-    }
-    if (rc != POETX_ENOTSUPPORTED_ROW) return rc;
-  }
   IdxList L{};
   for (int k = 0; k < K; ++k) { L.idx[k] = inv[k]; L.ptr[k] = const_cast<void*>(du[k]); }
   POETX_K_DISPATCH(K, rt, rmsnorm_gather_bwd_kernel, set_smem(k, smem);

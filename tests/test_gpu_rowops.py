@@ -1,8 +1,7 @@
 """Fused row operators of the decoder block (csrc/model_ops.cu, row_pipe.cu)
 against plain PyTorch fp32 references of the same op: RMSNorm + feature
 gathers, SwiGLU through composed index maps, RoPE after the output scatter,
-residual scatter-add, feature permutation -- forward and backward, on both
-the persistent TMA-bulk kernels and the simple staged kernels."""
+residual scatter-add, feature permutation -- forward and backward."""
 
 import pytest
 import torch
@@ -12,13 +11,11 @@ pytestmark = pytest.mark.gpu
 SHAPES = [(8192, 2048, 5632), (300, 512, 1408), (1, 256, 768), (77, 1024, 2816)]
 
 
-@pytest.fixture(params=[1, 0], ids=["rowpipe", "staged"])
-def N(request):
+@pytest.fixture
+def N():
     from paper_2603_05500_b200 import _native as N
 
-    N.lib().poetx_set_rowpipe_enabled(request.param)
-    yield N
-    N.lib().poetx_set_rowpipe_enabled(1)
+    return N
 
 
 def _bf(t):

@@ -102,14 +102,6 @@ def hbm():
 
 
 def rows():
-    for on in (1, 0):
-        N.lib().poetx_set_rowpipe_enabled(on)
-        print("-- rowpipe", "on" if on else "off (staged kernels)")
-        _rows()
-    N.lib().poetx_set_rowpipe_enabled(1)
-
-
-def _rows():
     import ctypes as C
     from paper_2603_05500_b200.trainer import _ptrs
     print("== fused row kernels (bf16, T=8192) ==", os.environ.get("POETX_ROW_TILE_KB", "48"), "KB tiles")
@@ -156,6 +148,18 @@ def _rows():
     print(f"scatter_add: {ms * 1e3:.1f} us  {3 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
 
 
+def cnp():
+    from paper_2603_05500_b200.trainer import PoetStack
+    print("== model-batched CNP, Llama-1B (3696 blocks of 256) ==")
+    nb, b = 3696, 256
+    st = PoetStack([("all", nb)], b, torch.device("cuda"))
+    st.group.param.normal_(0, 0.01)
+    t_cf = timeit(st.forward_factors, 5, 1)
+    t_cb = timeit(st.backward_factors, 5, 1)
+    fl_f, fl_b = 2 * 3 * nb * b ** 3, 2 * 4 * nb * b ** 3
+    print(f"cnp fwd {t_cf:.3f} ms ({fl_f / t_cf / 1e9:.0f} TF/s), cnp bwd {t_cb:.3f} ms ({fl_b / t_cb / 1e9:.0f} TF/s)")
+
+
 if __name__ == "__main__":
     what = sys.argv[1] if len(sys.argv) > 1 else "all"
     if what in ("gemm", "all"):
@@ -164,5 +168,7 @@ if __name__ == "__main__":
         rows()
     if what in ("hbm", "all"):
         hbm()
+    if what == "cnp":
+        cnp()
     if what in ("layer", "all"):
         layer()

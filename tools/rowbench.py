@@ -1,5 +1,5 @@
 """Single fused row operator at Llama-1B shapes, for ncu captures:
-python tools/rowbench.py swiglu_bwd [rowpipe 0|1]"""
+python tools/rowbench.py swiglu_bwd|swiglu|permute"""
 import os
 import sys
 
@@ -9,7 +9,6 @@ import torch
 from paper_2603_05500_b200 import _native as N
 
 op = sys.argv[1]
-N.lib().poetx_set_rowpipe_enabled(int(sys.argv[2]) if len(sys.argv) > 2 else 1)
 T, d, f = 8192, 2048, 5632
 st = N.stream_ptr()
 vg = torch.randn((T, f), device="cuda").bfloat16()
