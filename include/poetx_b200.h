@@ -62,6 +62,10 @@ uint64_t poetx_launch_count(void);
 /* 1 if the tcgen05/TMA GEMM path is compiled in and enabled */
 int poetx_tc_enabled(void);
 void poetx_set_tc_enabled(int on);
+/* 1 if large single-group BF16 products (mm2, adjoint) run on the CTA-pair
+ * (cta_group::2, 256 x 256 tile) kernel; 0 selects the single-CTA kernel */
+int poetx_gemm_pair_enabled(void);
+void poetx_set_gemm_pair_enabled(int on);
 /* device timing hooks: while enabled, tensor-core kernel launches are
  * bracketed by CUDA events on their stream; query sums durations (ms),
  * launch count and algorithmic FLOPs per kernel name ("tc_gemm", ...). */

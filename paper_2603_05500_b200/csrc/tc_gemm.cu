@@ -29,6 +29,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -337,6 +338,243 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ------------------------------------------------------- CTA-pair kernel --
+// 2-SM variant for the big single-group products (mm2 / adjoint): a cluster
+// of two CTAs on one TPC computes a 256 x 256 tile with tcgen05.mma
+// cta_group::2 (M = 256, N = 256, issued by the even CTA).  Each CTA stages
+// its own 128-row half of A and 128-column half of B per K block, so per-SM
+// operand traffic (smem fill and L2 reads) per FLOP halves against the
+// 128 x 256 single-CTA tile; each CTA's TMEM holds its 128 rows of the
+// accumulator (double-buffered, 2 x 256 columns).
+//   leader  warp 0: TMA (own halves; completion to the leader's full barrier)
+//           warp 1: MMA issue, commits multicast to both CTAs' barriers
+//   both    warps 4..7: epilogue of their own 128 rows, TMA bulk stores;
+//           release the accumulator on the leader's tempty barrier.
+namespace pair {
+
+constexpr int HALF = 128;                       // rows of A / columns of B per CTA
+constexpr int A_B = HALF * BK * 2;              // 16 KB
+constexpr int B_B = HALF * BK * 2;              // 16 KB
+constexpr int STAGE = A_B + B_B;
+constexpr int EPI = 4 * 2 * 32 * 128;
+constexpr int STAGES = (227 * 1024 - EPI - 2048) / STAGE > 8 ? 8 : (227 * 1024 - EPI - 2048) / STAGE;
+constexpr int SMEM = STAGES * STAGE + EPI + 1024 + 256;
+constexpr uint32_t PEER_MASK = 0xFEFFFFFFu;     // shared::cluster address of the even CTA
+
+__device__ __forceinline__ uint32_t cta_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2sm(void* dst, const CUtensorMap* map, uint32_t bar_cluster, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar_cluster), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void umma2_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                           uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void commit2(uint64_t* bar) {
+  const uint16_t mask = 3;
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void arrive_leader(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & PEER_MASK)
+               : "memory");
+}
+__device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t spins = 0;
+  while (true) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+    if (ok) break;
+    if (++spins == (1u << 28)) __trap();
+  }
+}
+
+template <bool A_MN, bool B_MN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+    tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+               const __grid_constant__ CUtensorMap map_c, Args args) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* epi = smem + STAGES * STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(epi + EPI);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = cta_rank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int num_tiles = args.m_tiles * args.n_tiles;  // 256 x 256 tiles
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 8);  // 4 epilogue warps in each CTA of the pair
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  fence_before();
+  cluster_sync();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
+      int stage = 0;
+      uint32_t phase = 0;
+      const int kbn = (args.K + BK - 1) / BK;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        const int m0 = (tile / args.n_tiles) * 256 + rank * HALF;  // this CTA's A rows
+        const int n0 = (tile % args.n_tiles) * 256 + rank * HALF;  // this CTA's B columns
+        for (int kb = 0; kb < kbn; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * STAGE;
+          uint8_t* sb = sa + A_B;
+          const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
+          if (leader) mbar_expect_tx(&full[stage], 2 * STAGE);
+          const int k = kb * BK;
+          if constexpr (A_MN) {
+#pragma unroll
+            for (int j = 0; j < HALF / 64; ++j) tma_load_2sm(sa + j * (BK * 128), &map_a, fb, m0 + j * 64, k);
+          } else {
+            tma_load_2sm(sa, &map_a, fb, k, m0);
+          }
+          if constexpr (B_MN) {
+#pragma unroll
+            for (int j = 0; j < HALF / 64; ++j) tma_load_2sm(sb + j * (BK * 128), &map_b, fb, n0 + j * 64, k);
+          } else {
+            tma_load_2sm(sb, &map_b, fb, k, n0);
+          }
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      constexpr uint32_t idesc = idesc_bf16(256, 256, A_MN, B_MN);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      const int kbn = (args.K + BK - 1) / BK;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        wait_cluster(&tempty[acc], acc_phase ^ 1);
+        fence_after();
+        const uint32_t tmem_d = tmem_base + acc * 256;
+        for (int kb = 0; kb < kbn; ++kb) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          if (lane == 0) {
+            const uint32_t a_addr = smem_u32(smem + stage * STAGE);
+            const uint32_t b_addr = a_addr + A_B;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma2_bf16(tmem_d, operand_desc<A_MN>(a_addr, k), operand_desc<B_MN>(b_addr, k), idesc,
+                         (kb | k) != 0);
+            commit2(&empty[stage]);
+            if (kb == kbn - 1) commit2(&tfull[acc]);
+          }
+          __syncwarp();
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else if (warp >= 4) {
+    const int ew = warp - 4;
+    uint8_t* stg = epi + ew * (2 * 32 * 128);
+    int buf = 0, acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      const int row0 = (tile / args.n_tiles) * 256 + rank * HALF + ew * 32;
+      const int n0 = (tile % args.n_tiles) * 256;
+      mbar_wait(&tfull[acc], acc_phase);
+      fence_after();
+      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * 256;
+#pragma unroll 1
+      for (int c = 0; c < 256; c += 64) {
+        uint32_t r[64];
+        tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+        tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        if (lane == 0) bulk_wait_read<1>();
+        __syncwarp();
+        uint8_t* rowp = stg + buf * (32 * 128) + lane * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint4 v;
+          v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
+          v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
+          v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
+          v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
+          *reinterpret_cast<uint4*>(rowp + ((q ^ (lane & 7)) * 16)) = v;
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&map_c, stg + buf * (32 * 128), n0 + c, row0);
+          bulk_commit();
+        }
+        buf ^= 1;
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) arrive_leader(&tempty[acc]);
+      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+    }
+    if (lane == 0) bulk_wait<0>();
+  }
+
+  fence_before();
+  cluster_sync();
+  fence_after();
+  if (warp == 2) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
+  }
+}
+
+}  // namespace pair
+
 // -------------------------------------------------------------- host side --
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -484,10 +722,70 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
   return launch_bn<64>(A.mn_major, B.mn_major, ms, ma, mb, mc, a, name, st);
 }
 
+static int g_pair_on = [] {
+  const char* e = getenv("POETX_GEMM_PAIR");
+  return e && e[0] == '0' ? 0 : 1;
+}();
+
+namespace tc {
+template <bool A_MN, bool B_MN>
+int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& a,
+                cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(pair::tc2_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM);
+    attr_set = true;
+  }
+  const int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles;
+  const int64_t pairs = num_sms() / 2;
+  const int grid = static_cast<int>(2 * (tiles < pairs ? tiles : pairs));
+  void* tok = prof_begin(st);
+  pair::tc2_kernel<A_MN, B_MN><<<grid, THREADS, pair::SMEM, st>>>(ma, mb, mc, a);
+  prof_end(tok, "tc_gemm", 2.0 * a.M * a.N * static_cast<double>(a.K), st);
+  POETX_LAUNCHED("tc_gemm_pair");
+  return POETX_OK;
+}
+}  // namespace tc
+
+// C = op(A) op(B) on a CTA pair: M, N multiples of 256, single group
+static int tc_matmul_pair(int64_t M, int64_t N, int64_t K, const TcOperand& A, const TcOperand& B, void* C,
+                          int64_t ldc, cudaStream_t st) {
+  using namespace tc;
+  if (M % 256 || N % 256 || K % BK || (ldc % 8)) return POETX_ENOTSUPPORTED;
+  for (const TcOperand* o : {&A, &B})
+    if ((reinterpret_cast<uintptr_t>(o->ptr) & 15) || (o->pitch % 8)) return POETX_ENOTSUPPORTED;
+  if (reinterpret_cast<uintptr_t>(C) & 15) return POETX_ENOTSUPPORTED;
+  CUtensorMap ma, mb, mc;
+  POETX_TRY(make_map(&ma, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : pair::HALF));
+  POETX_TRY(make_map(&mb, B.ptr, B.cols, B.rows, B.pitch, 64, B.mn_major ? BK : pair::HALF));
+  POETX_TRY(make_map(&mc, C, N, M, ldc, 64, 32));
+  Args a{};
+  a.M = static_cast<int>(M);
+  a.N = static_cast<int>(N);
+  a.K = static_cast<int>(K);
+  a.groups = 1;
+  a.splits = 1;
+  a.kps = static_cast<int>(K);
+  a.m_tiles = static_cast<int>(M / 256);
+  a.n_tiles = static_cast<int>(N / 256);
+  a.C = C;
+  a.ldc = ldc;
+  a.alpha = 1.0f;
+  a.tma_epi = 1;
+  if (A.mn_major) return B.mn_major ? launch_pair<true, true>(ma, mb, mc, a, st) : launch_pair<true, false>(ma, mb, mc, a, st);
+  return B.mn_major ? launch_pair<false, true>(ma, mb, mc, a, st) : launch_pair<false, false>(ma, mb, mc, a, st);
+}
+
 int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
               const void* B, int64_t ldb, int transB, void* C, int64_t ldc, cudaStream_t st) {
   if (M <= 0 || N <= 0) return POETX_OK;
   if (K <= 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return POETX_ENOTSUPPORTED;
+  if (g_pair_on) {
+    TcOperand pa{A, transA ? K : M, transA ? M : K, lda, transA != 0};
+    TcOperand pb{B, transB ? N : K, transB ? K : N, ldb, transB == 0};
+    int rc = tc_matmul_pair(M, N, K, pa, pb, C, ldc, st);
+    if (rc != POETX_ENOTSUPPORTED) return rc;
+  }
   // op(A)[M,K]: stored [M,K] (K-major) or [K,M] (MN-major)
   TcOperand a{A, transA ? K : M, transA ? M : K, lda, transA != 0};
   // op(B)[K,N]: stored [K,N] (MN-major) or [N,K] (K-major)
@@ -530,4 +828,6 @@ int tc_outer_splits(int64_t T, int64_t nb, int64_t b) {
 }  // namespace poetx
 
 extern "C" int poetx_tc_enabled(void) { return poetx::g_tc_on; }
+extern "C" int poetx_gemm_pair_enabled(void) { return poetx::g_pair_on; }
+extern "C" void poetx_set_gemm_pair_enabled(int on) { poetx::g_pair_on = on ? 1 : 0; }
 extern "C" void poetx_set_tc_enabled(int on) { poetx::g_tc_on = on ? 1 : 0; }

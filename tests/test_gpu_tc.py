@@ -43,6 +43,28 @@ def test_tc_gemm_matches_fp32_reference(N, M, Nn, K, trans_b):
     assert err <= 8e-3 * max(1.0, scale), (err, scale)
 
 
+@pytest.mark.parametrize("M,Nn,K", [(256, 256, 64), (512, 768, 320), (8192, 5632, 2048), (8192, 2048, 5632)])
+@pytest.mark.parametrize("trans_b", [0, 1])
+@pytest.mark.parametrize("pair", [1, 0], ids=["cta_pair", "single_cta"])
+def test_tc_gemm_pair_and_single_cta(N, M, Nn, K, trans_b, pair):
+    """The CTA-pair (cta_group::2) kernel and the single-CTA kernel agree with
+    the fp32 reference and with each other bit-for-bit (same K order)."""
+    g = torch.Generator("cuda").manual_seed(7 * M + Nn + K)
+    a = torch.randn((M, K), device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn((Nn, K) if trans_b else (K, Nn), device="cuda", generator=g).to(torch.bfloat16)
+    N.lib().poetx_set_gemm_pair_enabled(pair)
+    try:
+        c = matmul(N, a, b, trans_b)
+        N.lib().poetx_set_gemm_pair_enabled(1 - pair)
+        c2 = matmul(N, a, b, trans_b)
+    finally:
+        N.lib().poetx_set_gemm_pair_enabled(1)
+    ref = a.float() @ (b.float().t() if trans_b else b.float())
+    err = (c.float() - ref).abs().max().item()
+    assert err <= 8e-3 * max(1.0, ref.abs().max().item()), err
+    assert torch.equal(c, c2)
+
+
 @pytest.mark.parametrize("b,nb,T", [(64, 8, 1024), (128, 6, 300), (256, 8, 8192), (256, 22, 512)])
 @pytest.mark.parametrize("transpose", [False, True])
 def test_tc_blockdiag_apply(N, b, nb, T, transpose):
