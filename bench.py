@@ -232,10 +232,13 @@ def run_ours(args, rank, world, local_rank):
 
     # dominant-kernel roofline: CUDA events around each tcgen05 GEMM launch on its
     # stream, during an eager pass of the same steps (host hooks need eager launches)
+    # (projection chains serialised for this pass so each launch's duration is its own)
     lib = N.lib()
     lib.poetx_prof_reset()
     lib.poetx_prof_enable(1)
+    trainer.model.concurrent = False
     prof_ms, _ = timed(args.steps, resident=True, prof=True)
+    trainer.model.concurrent = True
     lib.poetx_prof_enable(0)
 
     # graph capture of the single-GPU step; with NCCL all-reduces in the step
@@ -304,7 +307,8 @@ def run_ours(args, rank, world, local_rank):
                 "traffic": None, "launches": cnt.value,
                 "share_of_step": round(k_share, 4) if k_share else None,
                 "peak_source": src + " sustained (kernel timed inside a long step)",
-                "timing": "CUDA events around every tc_gemm launch on its stream, extra profiled pass of the same steps",
+                "timing": "CUDA events around every tc_gemm launch on its stream, extra eager profiled pass of the "
+                          "same steps with the q/k/v and gate/up chains serialised",
             },
             "e2e": {"value": round(e2e, 1), "unit": UNIT,
                     "h2d_bytes_per_step": B * (S + 1) * 8, "d2h_bytes_per_step": 4},

@@ -544,6 +544,24 @@ __global__ void reduce_splits_kernel(int64_t total, int splits, const T* __restr
   }
 }
 
+// fp32, 4 elements per thread, partials read with streaming loads (same fixed order)
+__global__ void reduce_splits_f4_kernel(int64_t total4, int splits, const float4* __restrict__ part,
+                                        float4* __restrict__ out, int accumulate) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total4;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    float4 acc = __ldcs(part + e);
+    for (int s = 1; s < splits; ++s) {
+      const float4 v = __ldcs(part + s * total4 + e);
+      acc.x = acc.x + v.x; acc.y = acc.y + v.y; acc.z = acc.z + v.z; acc.w = acc.w + v.w;
+    }
+    if (accumulate) {
+      const float4 o = out[e];
+      acc.x = o.x + acc.x; acc.y = o.y + acc.y; acc.z = o.z + acc.z; acc.w = o.w + acc.w;
+    }
+    out[e] = acc;
+  }
+}
+
 static int outer_splits(int64_t T, int64_t nb, int64_t b) {
   int64_t tiles = nb * ((b + 63) / 64) * ((b + 63) / 64);
   int64_t want = (2 * 148 + tiles - 1) / tiles;
@@ -589,8 +607,13 @@ int segmented_outer(int dt, int64_t T, int64_t nb, int64_t b, const void* x, con
     if (rc != POETX_ENOTSUPPORTED) {
       POETX_TRY(rc);
       if (tgt != out) {
-        reduce_splits_kernel<float><<<grid_for(total, 256), 256, 0, st>>>(
-            total, s, tgt, static_cast<float*>(out), accumulate);
+        if (total % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
+          reduce_splits_f4_kernel<<<grid_for(total / 4, 256), 256, 0, st>>>(
+              total / 4, s, reinterpret_cast<const float4*>(tgt), static_cast<float4*>(out), accumulate);
+        } else {
+          reduce_splits_kernel<float><<<grid_for(total, 256), 256, 0, st>>>(
+              total, s, tgt, static_cast<float*>(out), accumulate);
+        }
         POETX_LAUNCHED("reduce_splits");
       }
       return POETX_OK;

@@ -432,12 +432,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
-  const int num_tiles = args.m_tiles * args.n_tiles;  // 256 x 256 tiles
+  const int tiles_per_split = args.m_tiles * args.n_tiles;  // 256 x 256 tiles
+  const int num_tiles = tiles_per_split * args.splits * args.groups;
+
+  // tile -> group, K split, 256-row / 256-column origin, K-block range
+  auto decode = [&](int tile, int& g, int& s, int& m0, int& n0, int& kb0, int& kbn) {
+    g = tile / (tiles_per_split * args.splits);
+    int r = tile % (tiles_per_split * args.splits);
+    s = r / tiles_per_split;
+    r %= tiles_per_split;
+    m0 = (r / args.n_tiles) * 256;
+    n0 = (r % args.n_tiles) * 256;
+    const int k0 = s * args.kps;
+    const int k1 = k0 + args.kps < args.K ? k0 + args.kps : args.K;
+    kb0 = k0 / BK;
+    kbn = (k1 - k0 + BK - 1) / BK;
+  };
 
   if (threadIdx.x == 0) {
-    for (int s = 0; s < STAGES; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int st = 0; st < STAGES; ++st) {
+      mbar_init(&full[st], 1);
+      mbar_init(&empty[st], 1);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -463,11 +478,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
       int stage = 0;
       uint32_t phase = 0;
-      const int kbn = (args.K + BK - 1) / BK;
       for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-        const int m0 = (tile / args.n_tiles) * 256 + rank * HALF;  // this CTA's A rows
-        const int n0 = (tile % args.n_tiles) * 256 + rank * HALF;  // this CTA's B columns
-        for (int kb = 0; kb < kbn; ++kb) {
+        int g, sp, m0, n0, kb0, kbn;
+        decode(tile, g, sp, m0, n0, kb0, kbn);
+        const int am = m0 + rank * HALF, bn = n0 + rank * HALF;  // this CTA's halves
+        const int ag0 = args.a_g0 * g, ag1 = args.a_g1 * g, bg0 = args.b_g0 * g, bg1 = args.b_g1 * g;
+        for (int kb = kb0; kb < kb0 + kbn; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE;
           uint8_t* sb = sa + A_B;
@@ -476,15 +492,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           const int k = kb * BK;
           if constexpr (A_MN) {
 #pragma unroll
-            for (int j = 0; j < HALF / 64; ++j) tma_load_2sm(sa + j * (BK * 128), &map_a, fb, m0 + j * 64, k);
+            for (int j = 0; j < HALF / 64; ++j) tma_load_2sm(sa + j * (BK * 128), &map_a, fb, ag0 + am + j * 64, ag1 + k);
           } else {
-            tma_load_2sm(sa, &map_a, fb, k, m0);
+            tma_load_2sm(sa, &map_a, fb, ag0 + k, ag1 + am);
           }
           if constexpr (B_MN) {
 #pragma unroll
-            for (int j = 0; j < HALF / 64; ++j) tma_load_2sm(sb + j * (BK * 128), &map_b, fb, n0 + j * 64, k);
+            for (int j = 0; j < HALF / 64; ++j) tma_load_2sm(sb + j * (BK * 128), &map_b, fb, bg0 + bn + j * 64, bg1 + k);
           } else {
-            tma_load_2sm(sb, &map_b, fb, k, n0);
+            tma_load_2sm(sb, &map_b, fb, bg0 + k, bg1 + bn);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -497,8 +513,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      const int kbn = (args.K + BK - 1) / BK;
       for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        int g, sp, m0, n0, kb0, kbn;
+        decode(tile, g, sp, m0, n0, kb0, kbn);
         wait_cluster(&tempty[acc], acc_phase ^ 1);
         fence_after();
         const uint32_t tmem_d = tmem_base + acc * 256;
@@ -518,6 +535,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           __syncwarp();
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
+        if (kbn == 0 && lane == 0) commit2(&tfull[acc]);  // empty K range
+        __syncwarp();
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       }
     }
@@ -526,35 +545,53 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     uint8_t* stg = epi + ew * (2 * 32 * 128);
     int buf = 0, acc = 0;
     uint32_t acc_phase = 0;
+    const int step = args.out_f32 ? 32 : 64;
     for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-      const int row0 = (tile / args.n_tiles) * 256 + rank * HALF + ew * 32;
-      const int n0 = (tile % args.n_tiles) * 256;
+      int g, sp, m0, n0, kb0, kbn;
+      decode(tile, g, sp, m0, n0, kb0, kbn);
+      const int row0 = m0 + rank * HALF + ew * 32;  // this warp's 32 rows (within the group)
+      const int64_t crow = args.c_row0 + g * args.c_grow + sp * args.c_srow + row0;
       mbar_wait(&tfull[acc], acc_phase);
       fence_after();
       const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * 256;
 #pragma unroll 1
-      for (int c = 0; c < 256; c += 64) {
+      for (int c = 0; c < 256; c += step) {
         uint32_t r[64];
         tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
-        tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        if (!args.out_f32) tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+        if (kbn == 0) {
+#pragma unroll
+          for (int q = 0; q < 64; ++q) r[q] = 0u;
+        }
+        if (args.alpha != 1.0f) {
+#pragma unroll
+          for (int q = 0; q < 64; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * args.alpha);
+        }
         if (lane == 0) bulk_wait_read<1>();
         __syncwarp();
         uint8_t* rowp = stg + buf * (32 * 128) + lane * 128;
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           uint4 v;
-          v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
-          v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
-          v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
-          v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
+          if (args.out_f32) {
+            v = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+          } else {
+            v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
+            v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
+            v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
+            v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
+          }
           *reinterpret_cast<uint4*>(rowp + ((q ^ (lane & 7)) * 16)) = v;
         }
         fence_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          tma_store_2d(&map_c, stg + buf * (32 * 128), n0 + c, row0);
-          bulk_commit();
+        if (lane == 0 && row0 < args.M && n0 + c < args.N) {
+          if (args.accumulate)
+            tma_reduce_add_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
+          else
+            tma_store_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
         }
+        if (lane == 0) bulk_commit();
         buf ^= 1;
       }
       fence_before();
@@ -666,6 +703,32 @@ int launch_bn(bool a_mn, bool b_mn, int ms, const CUtensorMap& ma, const CUtenso
 
 }  // namespace tc
 
+static int g_pair_on = [] {
+  const char* e = getenv("POETX_GEMM_PAIR");
+  return e && e[0] == '0' ? 0 : 1;
+}();
+
+namespace tc {
+template <bool A_MN, bool B_MN>
+int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& a,
+                const char* name, cudaStream_t st) {
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(pair::tc2_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM);
+    attr_set = true;
+  }
+  const int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles * a.splits * a.groups;
+  const int64_t pairs = num_sms() / 2;
+  const int grid = static_cast<int>(2 * (tiles < pairs ? tiles : pairs));
+  if (grid <= 0) return POETX_OK;
+  void* tok = prof_begin(st);
+  pair::tc2_kernel<A_MN, B_MN><<<grid, THREADS, pair::SMEM, st>>>(ma, mb, mc, a);
+  prof_end(tok, name, 2.0 * a.M * a.N * static_cast<double>(a.K) * a.groups, st);
+  POETX_LAUNCHED(name);
+  return POETX_OK;
+}
+}  // namespace tc
+
 // An operand is a row-major [rows, cols] bf16 view with a row pitch.
 // K-major: the contraction index runs along cols; MN-major: along rows.
 int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaStream_t st) {
@@ -679,6 +742,42 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
   if ((reinterpret_cast<uintptr_t>(p.C) & 15) || (p.ldc % 8) || (p.c_goff % 8) || (p.c_soff % 8))
     return POETX_ENOTSUPPORTED;
   if (p.N % 32) return POETX_ENOTSUPPORTED;
+  // CTA pair: 256 x 256 tiles; N whole tiles (groups may sit side by side in C),
+  // M whole tiles unless a single (group, split) block owns all rows of C
+  const int nblk = p.groups * (p.splits < 1 ? 1 : p.splits);
+  if (g_pair_on && p.ms != 2 && p.N % 256 == 0 && (p.M % 256 == 0 || nblk == 1) && p.tma_epi &&
+      p.c_goff % p.ldc == 0 && p.c_soff % p.ldc == 0 && (p.ldc * (p.out_f32 ? 4 : 2)) % 16 == 0 &&
+      !(p.accumulate && !p.out_f32)) {
+    CUtensorMap pa, pb, pc;
+    POETX_TRY(make_map(&pa, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : pair::HALF));
+    POETX_TRY(make_map(&pb, B.ptr, B.cols, B.rows, B.pitch, 64, B.mn_major ? BK : pair::HALF));
+    Args a{};
+    a.M = static_cast<int>(p.M);
+    a.N = static_cast<int>(p.N);
+    a.K = static_cast<int>(p.K);
+    a.groups = p.groups;
+    a.splits = p.splits < 1 ? 1 : p.splits;
+    int64_t kps = (p.K + a.splits - 1) / a.splits;
+    kps = (kps + BK - 1) / BK * BK;
+    a.kps = static_cast<int>(kps > 0 ? kps : BK);
+    a.m_tiles = static_cast<int>((p.M + 255) / 256);
+    a.n_tiles = static_cast<int>(p.N / 256);
+    a.a_g0 = p.a_g0; a.a_g1 = p.a_g1; a.b_g0 = p.b_g0; a.b_g1 = p.b_g1;
+    a.C = p.C;
+    a.ldc = p.ldc; a.c_goff = p.c_goff; a.c_soff = p.c_soff;
+    a.out_f32 = p.out_f32;
+    a.accumulate = p.accumulate;
+    a.alpha = p.alpha;
+    a.tma_epi = 1;
+    a.c_row0 = 0;
+    a.c_grow = p.c_goff / p.ldc;
+    a.c_srow = p.c_soff / p.ldc;
+    const int64_t rows = (p.groups - 1) * a.c_grow + (a.splits - 1) * a.c_srow + p.M;
+    POETX_TRY(p.out_f32 ? make_map_f32(&pc, p.C, p.N, rows, p.ldc, 32, 32) : make_map(&pc, p.C, p.N, rows, p.ldc, 64, 32));
+    const char* nm = p.name ? p.name : "tc_gemm";
+    if (A.mn_major) return B.mn_major ? launch_pair<true, true>(pa, pb, pc, a, nm, st) : launch_pair<true, false>(pa, pb, pc, a, nm, st);
+    return B.mn_major ? launch_pair<false, true>(pa, pb, pc, a, nm, st) : launch_pair<false, false>(pa, pb, pc, a, nm, st);
+  }
   CUtensorMap ma, mb;
   const int ms = p.ms == 2 ? 2 : 1;
   POETX_TRY(make_map(&ma, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : BM * ms));
@@ -722,70 +821,11 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
   return launch_bn<64>(A.mn_major, B.mn_major, ms, ma, mb, mc, a, name, st);
 }
 
-static int g_pair_on = [] {
-  const char* e = getenv("POETX_GEMM_PAIR");
-  return e && e[0] == '0' ? 0 : 1;
-}();
-
-namespace tc {
-template <bool A_MN, bool B_MN>
-int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& a,
-                cudaStream_t st) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(pair::tc2_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM);
-    attr_set = true;
-  }
-  const int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles;
-  const int64_t pairs = num_sms() / 2;
-  const int grid = static_cast<int>(2 * (tiles < pairs ? tiles : pairs));
-  void* tok = prof_begin(st);
-  pair::tc2_kernel<A_MN, B_MN><<<grid, THREADS, pair::SMEM, st>>>(ma, mb, mc, a);
-  prof_end(tok, "tc_gemm", 2.0 * a.M * a.N * static_cast<double>(a.K), st);
-  POETX_LAUNCHED("tc_gemm_pair");
-  return POETX_OK;
-}
-}  // namespace tc
-
-// C = op(A) op(B) on a CTA pair: M, N multiples of 256, single group
-static int tc_matmul_pair(int64_t M, int64_t N, int64_t K, const TcOperand& A, const TcOperand& B, void* C,
-                          int64_t ldc, cudaStream_t st) {
-  using namespace tc;
-  if (M % 256 || N % 256 || K % BK || (ldc % 8)) return POETX_ENOTSUPPORTED;
-  for (const TcOperand* o : {&A, &B})
-    if ((reinterpret_cast<uintptr_t>(o->ptr) & 15) || (o->pitch % 8)) return POETX_ENOTSUPPORTED;
-  if (reinterpret_cast<uintptr_t>(C) & 15) return POETX_ENOTSUPPORTED;
-  CUtensorMap ma, mb, mc;
-  POETX_TRY(make_map(&ma, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : pair::HALF));
-  POETX_TRY(make_map(&mb, B.ptr, B.cols, B.rows, B.pitch, 64, B.mn_major ? BK : pair::HALF));
-  POETX_TRY(make_map(&mc, C, N, M, ldc, 64, 32));
-  Args a{};
-  a.M = static_cast<int>(M);
-  a.N = static_cast<int>(N);
-  a.K = static_cast<int>(K);
-  a.groups = 1;
-  a.splits = 1;
-  a.kps = static_cast<int>(K);
-  a.m_tiles = static_cast<int>(M / 256);
-  a.n_tiles = static_cast<int>(N / 256);
-  a.C = C;
-  a.ldc = ldc;
-  a.alpha = 1.0f;
-  a.tma_epi = 1;
-  if (A.mn_major) return B.mn_major ? launch_pair<true, true>(ma, mb, mc, a, st) : launch_pair<true, false>(ma, mb, mc, a, st);
-  return B.mn_major ? launch_pair<false, true>(ma, mb, mc, a, st) : launch_pair<false, false>(ma, mb, mc, a, st);
-}
-
 int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
               const void* B, int64_t ldb, int transB, void* C, int64_t ldc, cudaStream_t st) {
   if (M <= 0 || N <= 0) return POETX_OK;
   if (K <= 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX) return POETX_ENOTSUPPORTED;
-  if (g_pair_on) {
-    TcOperand pa{A, transA ? K : M, transA ? M : K, lda, transA != 0};
-    TcOperand pb{B, transB ? N : K, transB ? K : N, ldb, transB == 0};
-    int rc = tc_matmul_pair(M, N, K, pa, pb, C, ldc, st);
-    if (rc != POETX_ENOTSUPPORTED) return rc;
-  }
+
   // op(A)[M,K]: stored [M,K] (K-major) or [K,M] (MN-major)
   TcOperand a{A, transA ? K : M, transA ? M : K, lda, transA != 0};
   // op(B)[K,N]: stored [K,N] (MN-major) or [N,K] (K-major)

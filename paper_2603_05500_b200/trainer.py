@@ -471,6 +471,11 @@ class PoetLlama(torch.nn.Module):
         self.cos32 = ang.cos().contiguous()
         self.sin32 = ang.sin().contiguous()
         self.fused = fused
+        # independent projection chains (q/k/v, gate/up) run on side streams so
+        # one chain's kernels fill the SMs another chain's kernel tail leaves
+        # idle; autograd replays the same stream assignment in backward
+        self.side = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)] if dev.type == "cuda" else []
+        self.concurrent = bool(self.side)
         self.refresh_maps()
 
     def refresh_maps(self):
@@ -532,6 +537,25 @@ class PoetLlama(torch.nn.Module):
         self._leaves = leaves
         return loss
 
+    def _branches(self, fns):
+        """Run independent callables concurrently: the first on the current
+        stream, the others on side streams; joins before returning."""
+        if not self.concurrent or len(fns) == 1:
+            return [f() for f in fns]
+        main = torch.cuda.current_stream()
+        outs = [None] * len(fns)
+        for k, f in enumerate(fns[1:], start=1):
+            st = self.side[k - 1]
+            st.wait_stream(main)
+            with torch.cuda.stream(st):
+                outs[k] = f()
+        outs[0] = fns[0]()
+        for k in range(1, len(fns)):
+            main.wait_stream(self.side[k - 1])
+            for t in (outs[k] if isinstance(outs[k], tuple) else (outs[k],)):
+                t.record_stream(main)
+        return outs
+
     def _block_fused(self, i, mods, h, n1, n2, B, S):
         """One decoder block with every POET-X permutation fused into a
         neighbouring kernel (no standalone permutation pass except around
@@ -544,16 +568,20 @@ class PoetLlama(torch.nn.Module):
         pout = lambda m: m.pout_dev  # noqa: E731
         uq, uk, uv, h = _RMSNormGather.apply(h, n1, [pin(q)[0], pin(k)[0], pin(v)[0]],
                                           [pin(q)[1], pin(k)[1], pin(v)[1]])
-        vq, vk, vv = _PoetRawFn.apply(uq, q), _PoetRawFn.apply(uk, k), _PoetRawFn.apply(uv, v)
-        qr = _RopeScatter.apply(vq, pout(q)[1], pout(q)[0], self.cos32, self.sin32, S, H, hd)
-        kr = _RopeScatter.apply(vk, pout(k)[1], pout(k)[0], self.cos32, self.sin32, S, H, hd)
-        vz = _Permute.apply(vv, pout(v)[1], pout(v)[0])
+        qr, kr, vz = self._branches([
+            lambda: _RopeScatter.apply(_PoetRawFn.apply(uq, q), pout(q)[1], pout(q)[0], self.cos32, self.sin32,
+                                       S, H, hd),
+            lambda: _RopeScatter.apply(_PoetRawFn.apply(uk, k), pout(k)[1], pout(k)[0], self.cos32, self.sin32,
+                                       S, H, hd),
+            lambda: _Permute.apply(_PoetRawFn.apply(uv, v), pout(v)[1], pout(v)[0]),
+        ])
         a = F.scaled_dot_product_attention(qr.view(B, S, H, hd).transpose(1, 2), kr.view(B, S, H, hd).transpose(1, 2),
                                            vz.view(B, S, H, hd).transpose(1, 2), is_causal=True)
         uo = _Permute.apply(a.transpose(1, 2).reshape(B * S, d), pin(o)[0], pin(o)[1])
         h = _ScatterAdd.apply(h, _PoetRawFn.apply(uo, o), pout(o)[1], pout(o)[0])
         ug, uu, h = _RMSNormGather.apply(h, n2, [pin(gate)[0], pin(up)[0]], [pin(gate)[1], pin(up)[1]])
-        ud = _SwiGLUGather.apply(_PoetRawFn.apply(ug, gate), _PoetRawFn.apply(uu, up), self.swiglu_maps[i])
+        vg, vu = self._branches([lambda: _PoetRawFn.apply(ug, gate), lambda: _PoetRawFn.apply(uu, up)])
+        ud = _SwiGLUGather.apply(vg, vu, self.swiglu_maps[i])
         return _ScatterAdd.apply(h, _PoetRawFn.apply(ud, down), pout(down)[1], pout(down)[0])
 
     def backward_dense_grads(self, loss):

@@ -1,0 +1,22 @@
+"""Block-diagonal apply / segmented outer at Llama-1B shapes (ncu target):
+python tools/blockbench.py apply|outer DIM [transpose]"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2603_05500_b200 as P
+
+op, dim = sys.argv[1], int(sys.argv[2])
+tr = len(sys.argv) > 3 and sys.argv[3] == "1"
+T, b = 8192, 256
+x = torch.randn((T, dim), device="cuda").bfloat16()
+y = torch.randn_like(x)
+G = P.BlockDiagonalFactor((0.1 * torch.randn((dim // b, b, b), device="cuda")).bfloat16())
+for _ in range(3):
+    if op == "apply":
+        P.apply_to_features(G, x, transpose=tr)
+    else:
+        P.segmented_outer(x, y, b)
+torch.cuda.synchronize()
