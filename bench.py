@@ -38,6 +38,16 @@ METRIC = "POET-X train tokens/s (Llama-1B, 1/2/4/8 B200), peak HBM/GPU, % TC roo
 UNIT = "tokens/s"
 
 
+def gemm_traffic():
+    """Per-launch DRAM traffic of the dominant kernel from the committed ncu
+    capture (profiles/r01/ncu_gemm_traffic.json, tools/ncu_traffic.sh)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_gemm_traffic.json")) as f:
+            return json.load(f)["traffic_bytes_per_launch"]
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -304,7 +314,8 @@ def run_ours(args, rank, world, local_rank):
                 "kernel": "tc_gemm (tcgen05 mm2 / adjoint)", "bound": "tensor",
                 "achieved": round(achieved, 1) if achieved else None, "peak": tf_sus,
                 "unit": "TFLOP/s", "frac": round(achieved / tf_sus, 4) if achieved else None,
-                "traffic": None, "launches": cnt.value,
+                "traffic": gemm_traffic(), "traffic_unit": "bytes/launch (ncu dram read+write)",
+                "traffic_source": "profiles/r01/ncu_gemm_traffic.json", "launches": cnt.value,
                 "share_of_step": round(k_share, 4) if k_share else None,
                 "peak_source": src + " sustained (kernel timed inside a long step)",
                 "timing": "CUDA events around every tc_gemm launch on its stream, extra eager profiled pass of the "
