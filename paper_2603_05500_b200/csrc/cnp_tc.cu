@@ -234,7 +234,13 @@ using namespace poetx;
 
 extern "C" {
 
+// Stacks are processed in chunks of at most kChunk blocks, so the scratch
+// stays bounded (Llama-8B has 11,008 blocks of 256: the whole-stack backward
+// scratch would be 8.7 GB) while every launch still covers >= 1024 blocks.
+constexpr int64_t kChunk = 1024;
+
 size_t poetx_cnp_tc_workspace_bytes(int64_t nb, int64_t b) {
+  if (nb > kChunk) nb = kChunk;
   const size_t blk = static_cast<size_t>(nb * b * b);
   // fwd: Q34 [nb,b,2b] bf16 ; bwd: N1 bf16, N2/dQ fp32, N2 bf16, R bf16, P bf16
   size_t fwd = align_up(blk * 4);
@@ -242,10 +248,40 @@ size_t poetx_cnp_tc_workspace_bytes(int64_t nb, int64_t b) {
   return (fwd > bwd ? fwd : bwd) + 4096;
 }
 
+static int cnp_forward_tc_chunk(int64_t nb, int64_t b, const float* packed, void* qq2, void* g_bf16,
+                                float* g_f32, void* ws, size_t ws_bytes, void* stream);
+static int cnp_backward_tc_chunk(int64_t nb, int64_t b, const void* qq2, const float* dg, float* dpacked,
+                                 int accumulate, void* ws, size_t ws_bytes, void* stream);
+
 int poetx_cnp_forward_tc(int64_t nb, int64_t b, const float* packed, void* qq2, void* g_bf16,
                          float* g_f32, void* ws, size_t ws_bytes, void* stream) {
   POETX_TRY(check(nb, b));
   POETX_REQUIRE(packed && qq2 && (g_bf16 || g_f32), POETX_ESHAPE, "cnp_forward_tc: null operand");
+  const int64_t pairs = b * (b - 1) / 2;
+  for (int64_t o = 0; o < nb; o += kChunk) {
+    const int64_t n = nb - o < kChunk ? nb - o : kChunk;
+    POETX_TRY(cnp_forward_tc_chunk(n, b, packed + o * pairs, static_cast<__nv_bfloat16*>(qq2) + o * b * 2 * b,
+                                   g_bf16 ? static_cast<__nv_bfloat16*>(g_bf16) + o * b * b : nullptr,
+                                   g_f32 ? g_f32 + o * b * b : nullptr, ws, ws_bytes, stream));
+  }
+  return POETX_OK;
+}
+
+int poetx_cnp_backward_tc(int64_t nb, int64_t b, const void* qq2, const float* dg, float* dpacked,
+                          int accumulate, void* ws, size_t ws_bytes, void* stream) {
+  POETX_TRY(check(nb, b));
+  POETX_REQUIRE(qq2 && dg && dpacked, POETX_ESHAPE, "cnp_backward_tc: null operand");
+  const int64_t pairs = b * (b - 1) / 2;
+  for (int64_t o = 0; o < nb; o += kChunk) {
+    const int64_t n = nb - o < kChunk ? nb - o : kChunk;
+    POETX_TRY(cnp_backward_tc_chunk(n, b, static_cast<const __nv_bfloat16*>(qq2) + o * b * 2 * b, dg + o * b * b,
+                                    dpacked + o * pairs, accumulate, ws, ws_bytes, stream));
+  }
+  return POETX_OK;
+}
+
+static int cnp_forward_tc_chunk(int64_t nb, int64_t b, const float* packed, void* qq2, void* g_bf16,
+                                float* g_f32, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   Workspace w(ws, ws_bytes);
   auto* q34 = w.take<__nv_bfloat16>(static_cast<size_t>(nb * b * 2 * b));
@@ -270,10 +306,8 @@ int poetx_cnp_forward_tc(int64_t nb, int64_t b, const float* packed, void* qq2, 
   return POETX_OK;
 }
 
-int poetx_cnp_backward_tc(int64_t nb, int64_t b, const void* qq2, const float* dg, float* dpacked,
-                          int accumulate, void* ws, size_t ws_bytes, void* stream) {
-  POETX_TRY(check(nb, b));
-  POETX_REQUIRE(qq2 && dg && dpacked, POETX_ESHAPE, "cnp_backward_tc: null operand");
+static int cnp_backward_tc_chunk(int64_t nb, int64_t b, const void* qq2, const float* dg, float* dpacked,
+                                 int accumulate, void* ws, size_t ws_bytes, void* stream) {
   cudaStream_t st = as_stream(stream);
   const int64_t total = nb * b * b;
   Workspace w(ws, ws_bytes);

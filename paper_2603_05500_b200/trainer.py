@@ -266,10 +266,16 @@ class PoetLinear(torch.nn.Module):
 
 class _PoetRawFn(torch.autograd.Function):
     """POET-X layer core with the caller owning both permutations:
-    u = x[:, pi_in] in, v (before the pi_out scatter) out (csrc/layer.cu flags)."""
+    u = x[:, pi_in] in, v (before the pi_out scatter) out (csrc/layer.cu flags).
+
+    mem variant with ``regen``: like the reference, which caches the layer
+    input x by reference and regathers u = x[:, pi_in] in backward
+    (layer.py:228, 250), the gathered input is not kept: ``regen()`` rebuilds
+    u bit-exactly from tensors the neighbouring ops keep anyway (the RMSNorm
+    input, the attention output, the SwiGLU inputs)."""
 
     @staticmethod
-    def forward(ctx, u, mod):
+    def forward(ctx, u, mod, regen=None):
         T = u.shape[0]
         v = torch.empty((T, mod.n), dtype=torch.bfloat16, device=u.device)
         saved = torch.empty((T, mod.n), dtype=torch.bfloat16, device=u.device) if mod.variant == "fast" else None
@@ -277,15 +283,18 @@ class _PoetRawFn(torch.autograd.Function):
         N.call("poetx_layer_forward_ex", mod.desc, mod.fstruct, T, u.data_ptr(), v.data_ptr(), N.ptr(saved),
                N.IN_GATHERED | N.OUT_UNSCATTERED, ws, wsb, N.stream_ptr(u.device))
         ctx.mod = mod
-        ctx.save_for_backward(u, saved) if saved is not None else ctx.save_for_backward(u)
+        ctx.regen = regen if (regen is not None and mod.variant == "mem") else None
+        kept = [] if ctx.regen is not None else [u]
+        ctx.save_for_backward(*kept, *([saved] if saved is not None else []))
+        ctx.has_u = ctx.regen is None
         return v
 
     @staticmethod
     def backward(ctx, dv):
         mod = ctx.mod
-        saved = ctx.saved_tensors
-        u = saved[0]
-        t = saved[1] if len(saved) > 1 else None
+        saved = list(ctx.saved_tensors)
+        u = saved.pop(0) if ctx.has_u else ctx.regen()
+        t = saved[0] if saved else None
         dv = dv.contiguous()
         T = u.shape[0]
         du = torch.empty_like(u)
@@ -293,7 +302,25 @@ class _PoetRawFn(torch.autograd.Function):
         N.call("poetx_layer_backward_dg", mod.desc, mod.fstruct, T, u.data_ptr(), dv.data_ptr(), N.ptr(t),
                du.data_ptr(), mod.dg_r.data_ptr(), mod.dg_p.data_ptr(), 0,
                N.IN_GATHERED | N.DZ_GATHERED | N.DX_UNSCATTERED, ws, wsb, N.stream_ptr(u.device))
-        return du, None
+        return du, None, None
+
+
+def _rmsnorm_regather(h, w, idx):
+    """u = (rmsnorm(h) * w)[:, idx], recomputed with the forward kernel (bit-exact)."""
+    T, d = h.shape
+    out = torch.empty_like(h)
+    rstd = torch.empty(T, dtype=torch.float32, device=h.device)
+    N.call("poetx_rmsnorm_gather", T, d, h.data_ptr(), w.data_ptr(), 1e-6, 1, _ptrs([idx]), _ptrs([out]),
+           rstd.data_ptr(), N.stream_ptr(h.device))
+    return out
+
+
+def _swiglu_regather(vg, vu, maps):
+    T, f = vg.shape
+    out = torch.empty_like(vg)
+    N.call("poetx_swiglu_gather", T, f, vg.data_ptr(), vu.data_ptr(), maps["cg"].data_ptr(),
+           maps["cu"].data_ptr(), out.data_ptr(), N.stream_ptr(vg.device))
+    return out
 
 
 def _ptrs(ts):
@@ -566,23 +593,33 @@ class PoetLlama(torch.nn.Module):
         gate, up, down = mods["gate"], mods["up"], mods["down"]
         pin = lambda m: m.pin_dev  # noqa: E731
         pout = lambda m: m.pout_dev  # noqa: E731
+        h_in, n1d = h.detach(), n1.detach()
+        rg = lambda mod: (lambda: _rmsnorm_regather(h_in, n1d, pin(mod)[0]))  # noqa: E731
         uq, uk, uv, h = _RMSNormGather.apply(h, n1, [pin(q)[0], pin(k)[0], pin(v)[0]],
                                           [pin(q)[1], pin(k)[1], pin(v)[1]])
         qr, kr, vz = self._branches([
-            lambda: _RopeScatter.apply(_PoetRawFn.apply(uq, q), pout(q)[1], pout(q)[0], self.cos32, self.sin32,
-                                       S, H, hd),
-            lambda: _RopeScatter.apply(_PoetRawFn.apply(uk, k), pout(k)[1], pout(k)[0], self.cos32, self.sin32,
-                                       S, H, hd),
-            lambda: _Permute.apply(_PoetRawFn.apply(uv, v), pout(v)[1], pout(v)[0]),
+            lambda: _RopeScatter.apply(_PoetRawFn.apply(uq, q, rg(q)), pout(q)[1], pout(q)[0], self.cos32,
+                                       self.sin32, S, H, hd),
+            lambda: _RopeScatter.apply(_PoetRawFn.apply(uk, k, rg(k)), pout(k)[1], pout(k)[0], self.cos32,
+                                       self.sin32, S, H, hd),
+            lambda: _Permute.apply(_PoetRawFn.apply(uv, v, rg(v)), pout(v)[1], pout(v)[0]),
         ])
         a = F.scaled_dot_product_attention(qr.view(B, S, H, hd).transpose(1, 2), kr.view(B, S, H, hd).transpose(1, 2),
                                            vz.view(B, S, H, hd).transpose(1, 2), is_causal=True)
+        a_d = a.detach()
         uo = _Permute.apply(a.transpose(1, 2).reshape(B * S, d), pin(o)[0], pin(o)[1])
-        h = _ScatterAdd.apply(h, _PoetRawFn.apply(uo, o), pout(o)[1], pout(o)[0])
+        regen_o = lambda: _permute_cols(a_d.transpose(1, 2).reshape(B * S, d), pin(o)[0])  # noqa: E731
+        h = _ScatterAdd.apply(h, _PoetRawFn.apply(uo, o, regen_o), pout(o)[1], pout(o)[0])
+        h2_in, n2d = h.detach(), n2.detach()
+        rg2 = lambda mod: (lambda: _rmsnorm_regather(h2_in, n2d, pin(mod)[0]))  # noqa: E731
         ug, uu, h = _RMSNormGather.apply(h, n2, [pin(gate)[0], pin(up)[0]], [pin(gate)[1], pin(up)[1]])
-        vg, vu = self._branches([lambda: _PoetRawFn.apply(ug, gate), lambda: _PoetRawFn.apply(uu, up)])
+        vg, vu = self._branches([lambda: _PoetRawFn.apply(ug, gate, rg2(gate)),
+                                 lambda: _PoetRawFn.apply(uu, up, rg2(up))])
         ud = _SwiGLUGather.apply(vg, vu, self.swiglu_maps[i])
-        return _ScatterAdd.apply(h, _PoetRawFn.apply(ud, down), pout(down)[1], pout(down)[0])
+        maps = self.swiglu_maps[i]
+        vg_d, vu_d = vg.detach(), vu.detach()
+        regen_d = lambda: _swiglu_regather(vg_d, vu_d, maps)  # noqa: E731
+        return _ScatterAdd.apply(h, _PoetRawFn.apply(ud, down, regen_d), pout(down)[1], pout(down)[0])
 
     def backward_dense_grads(self, loss):
         """Backprop; dense grads land in the flat dense grad buffer."""
