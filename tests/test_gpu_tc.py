@@ -65,7 +65,8 @@ def test_tc_gemm_pair_and_single_cta(N, M, Nn, K, trans_b, pair):
     assert torch.equal(c, c2)
 
 
-@pytest.mark.parametrize("b,nb,T", [(64, 8, 1024), (128, 6, 300), (256, 8, 8192), (256, 22, 512)])
+@pytest.mark.parametrize("b,nb,T", [(64, 8, 1024), (128, 6, 300), (256, 8, 8192), (256, 22, 512), (256, 3, 300),
+                                    (256, 1, 64)])
 @pytest.mark.parametrize("transpose", [False, True])
 def test_tc_blockdiag_apply(N, b, nb, T, transpose):
     import paper_2603_05500_b200 as P
