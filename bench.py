@@ -255,13 +255,19 @@ def run_ours(args, rank, world, local_rank):
     timed(1, resident=True)
     peak_eager = torch.cuda.max_memory_allocated(dev) / 1e9
 
-    # graph capture of the single-GPU step; with NCCL all-reduces in the step
-    # the eager path is used (collectives are issued by torch.distributed)
-    args.graph = args.graph and pg is None
+    # graph capture of the whole step, NCCL all-reduces included (captured on the
+    # capturing stream's dependency chain); --no-graph launches eagerly
+    graph_error = None
     if args.graph:
         torch.cuda.empty_cache()  # the graph's private pool replaces the eager cache
         tb = dev_batches[0]
-        trainer.capture(tb[:, :-1], tb[:, 1:])
+        try:
+            trainer.capture(tb[:, :-1], tb[:, 1:])
+        except Exception as e:  # keep measuring (eagerly) rather than lose the run
+            graph_error = f"{type(e).__name__}: {e}"[:200]
+            trainer.graph = None
+            args.graph = False
+            torch.cuda.synchronize()
     torch.cuda.reset_peak_memory_stats(dev)
     clocks = ClockSampler(local_rank)
     clocks.start()
@@ -309,6 +315,7 @@ def run_ours(args, rank, world, local_rank):
                 "l2": "working set (2.5 GB frozen weights + activations) far larger than the 126 MB L2",
                 "merge_gap": args.merge_gap,
                 "cuda_graph": bool(args.graph),
+                **({"cuda_graph_error": graph_error} if graph_error else {}),
             },
             "peak_hbm_gb": {"eager_step_allocated": round(peak_eager, 2),
                             "timed_allocated": round(peak_alloc, 2), "timed_reserved": round(peak_res, 2),
