@@ -17,6 +17,7 @@ from .blockdiag import (
     orthogonality_error,
     segmented_outer,
 )
+from .checkpoint import load_checkpoint, save_checkpoint
 from .cnp import (
     CnpCache,
     SkewParams,

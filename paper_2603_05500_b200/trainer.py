@@ -213,6 +213,14 @@ class PoetLinear(torch.nn.Module):
                self.premerged.data_ptr(), N.stream_ptr(self.device))
         self._set_desc()
 
+    def install(self, w: torch.Tensor, perm_in: PermutationMap, perm_out: PermutationMap):
+        """Checkpoint load: new frozen weight W (bf16 [m, n]) and permutations,
+        written into the existing device buffers (fixed addresses)."""
+        self.perm_in, self.perm_out = perm_in, perm_out
+        for dst, src in zip(self.pin_dev + self.pout_dev, perm_in.device(self.device) + perm_out.device(self.device)):
+            dst.copy_(src)
+        self._install(w.to(self.device, torch.bfloat16).contiguous())
+
     def _set_desc(self):
         fi, ii = self.pin_dev
         fo, io = self.pout_dev
@@ -755,6 +763,22 @@ class Trainer:
         self._advance()
         self.graph = g
         return self.static_loss
+
+    def save_checkpoint(self, path: str, config_text: str = "", tokens: int = 0) -> None:
+        """PXK1 file with the reference runner's tensor names (checkpoint.py)."""
+        from .checkpoint import save_checkpoint, trainer_tensors
+
+        save_checkpoint(path, trainer_tensors(self, tokens=tokens), config_text)
+
+    def load_checkpoint(self, path: str):
+        """Resume from a PXK1 file written by ``save_checkpoint``; returns
+        (tokens, config text).  A captured graph stays valid: every buffer it
+        reads is rewritten in place."""
+        from .checkpoint import load_checkpoint, restore_trainer
+
+        tensors, cfg = load_checkpoint(path)
+        tokens = restore_trainer(self, tensors)
+        return tokens, cfg
 
     def merge(self):
         layers = self.model.poet_layers()
