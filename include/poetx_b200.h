@@ -191,6 +191,12 @@ typedef struct {
   const int32_t* perm_out_fwd; /* device int32[n] */
   const int32_t* perm_out_inv;
   const void* premerged;       /* device [m, n] = W[pi_in(i), pi_out(j)] */
+  /* POET-XQ (mem variant only, quant.py): when pm_codes != NULL the frozen
+   * weight is int8 codes [m, n] of the premerged matrix with per-row scales
+   * [m] (F64 for F64 layers, else F32) and premerged is ignored; each call
+   * dequantizes into its workspace right before the mm2 / adjoint GEMM. */
+  const int8_t* pm_codes;
+  const void* pm_scales;
 } poetx_layer_desc;
 
 /* factor state produced by poetx_layer_factors and consumed by fwd/bwd.
@@ -241,6 +247,29 @@ int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_
                       const int32_t* new_in_fwd, const int32_t* new_out_fwd,
                       void* premerged_out, void* w_out, void* ws, size_t ws_bytes,
                       void* stream);
+
+/* POET-XQ merge (layer.py:279-314 with a quantized base): the transformed
+ * base is requantized per row (bit-exact rule of quant.py:41-48) and the
+ * new premerged codes/scales are gathered in the quantized domain. */
+int poetx_layer_merge_quant(const poetx_layer_desc* d, const void* g_r, const void* g_p,
+                            const int32_t* new_in_fwd, const int32_t* new_out_fwd, int8_t* codes_out,
+                            void* scales_out, void* w_out, void* ws, size_t ws_bytes, void* stream);
+
+/* ----------------------------------------------------------------- quant --
+ * Per-row symmetric int8 (quant.py:22-74).  dtype = float type of w / out;
+ * scales are F64 for F64, else F32.  Round half to even, codes in
+ * [-127, 127], all-zero rows get scale 1.0 -- bit-exact with the reference. */
+int poetx_quantize_rows(int dtype, int64_t rows, int64_t cols, const void* w, int8_t* codes, void* scales,
+                        void* stream);
+/* out[i, j] = codes[ri(i), ci(j)] * scales[ri(i)] for an output [rows, cols];
+ * codes rows are src_cols long; row_idx/col_idx may be NULL */
+int poetx_dequantize_rows(int dtype, int64_t rows, int64_t cols, int64_t src_cols, const int8_t* codes,
+                          const void* scales, const int32_t* row_idx, const int32_t* col_idx, void* out,
+                          void* stream);
+/* quantized-domain gather into [rows, cols] (exact: commutes with dequantization) */
+int poetx_quant_gather(int dtype, int64_t rows, int64_t cols, int64_t src_cols, const int32_t* row_idx,
+                       const int32_t* col_idx, const int8_t* codes, const void* scales, int8_t* codes_out,
+                       void* scales_out, void* stream);
 
 /* ------------------------------------------------ fused neighbour kernels --
  * BF16 row-staged kernels that apply the layer permutations inside the

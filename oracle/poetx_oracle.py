@@ -241,10 +241,33 @@ def premerge(w, fwd_in, fwd_out):
 # ---------------------------------------------------------------------------
 
 
-class OracleLayer:
-    """Holds exactly the reference layer state: base W, packed params, perms."""
+def quantize_rows(w):
+    """quant.py:41-48: per-row absmax/127 scale (1.0 for zero rows), codes =
+    clip(rint(w / scale), -127, 127) in float64; scales stored in w's dtype."""
+    w64 = np.asarray(w).astype(np.float64)
+    absmax = np.max(np.abs(w64), axis=1)
+    scales = np.where(absmax > 0.0, absmax / 127.0, 1.0)
+    codes = np.clip(np.rint(w64 / scales[:, None]), -127, 127).astype(np.int8)
+    return codes, scales.astype(np.asarray(w).dtype)
 
-    def __init__(self, base, b, fwd_in, fwd_out, k=3, variant="fast"):
+
+def dequantize_rows(codes, scales):
+    """quant.py:50-61: codes in the scales' float type times the row scale."""
+    return codes.astype(scales.dtype) * scales[:, None]
+
+
+class OracleLayer:
+    """Holds exactly the reference layer state: base W, packed params, perms.
+    ``quantized`` (POET-XQ, mem variant): the base is kept as int8 rows and
+    every product reads the dequantized premerged rows (layer.py:188-210 --
+    the reference's row/column dequantising loops accumulate in the same
+    ascending order as ``matmul``/``matmul_abt`` on the dequantized matrix)."""
+
+    def __init__(self, base, b, fwd_in, fwd_out, k=3, variant="fast", quantized=False):
+        self.quantized = quantized
+        if quantized:
+            self.codes, self.scales = quantize_rows(base)
+            base = dequantize_rows(self.codes, self.scales)
         self.base = np.array(base)
         self.b = b
         self.k = k
@@ -320,6 +343,9 @@ class OracleLayer:
             err_r = orthogonality_error(cnp_forward(q_r, self.k)[0])
             err_p = orthogonality_error(cnp_forward(q_p, self.k)[0])
         self.base = self.transformed_base(exact)
+        if self.quantized:  # requantize the transformed base (layer.py:302-303)
+            self.codes, self.scales = quantize_rows(self.base)
+            self.base = dequantize_rows(self.codes, self.scales)
         self.q_r[...] = 0.0
         self.q_p[...] = 0.0
         self.set_perms(new_fwd_in, new_fwd_out)

@@ -61,6 +61,7 @@ from .permute import (
     premerge_weight,
     sample_permutation,
 )
+from .quant import QuantizedMatrix
 from .rng import Rng
 
 __version__ = "0.1.0"

@@ -53,6 +53,8 @@ class LayerDesc(C.Structure):
         ("perm_out_fwd", VP),
         ("perm_out_inv", VP),
         ("premerged", VP),
+        ("pm_codes", VP),
+        ("pm_scales", VP),
     ]
 
 
@@ -119,6 +121,10 @@ _SIGS = {
     "poetx_layer_backward": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I64, VP, VP, VP,
                                    VP, VP, VP, I32, VP, SZ, VP]),
     "poetx_merge_workspace_bytes": (SZ, [C.POINTER(LayerDesc)]),
+    "poetx_layer_merge_quant": (I32, [C.POINTER(LayerDesc), VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP]),
+    "poetx_quantize_rows": (I32, [I32, I64, I64, VP, VP, VP, VP]),
+    "poetx_dequantize_rows": (I32, [I32, I64, I64, I64, VP, VP, VP, VP, VP, VP]),
+    "poetx_quant_gather": (I32, [I32, I64, I64, I64, VP, VP, VP, VP, VP, VP, VP]),
     "poetx_layer_merge": (I32, [C.POINTER(LayerDesc), VP, VP, VP, VP, VP, VP, VP, SZ, VP]),
     "poetx_sqnorm_workspace_bytes": (SZ, [I32, VP]),
     "poetx_sqnorm": (I32, [I32, I32, VP, VP, VP, VP, VP, SZ, VP]),

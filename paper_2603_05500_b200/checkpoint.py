@@ -153,7 +153,16 @@ def trainer_tensors(trainer, tokens: int = 0, sv_drift: float = 0.0) -> dict:
         t[f"param/{name}"] = model.dense.param[off:off + n]
     for lay in model.poet_layers():
         key = f"layer/{lay.name}"
-        t[f"{key}/base"] = unpermuted_weight(lay.premerged, lay.perm_in, lay.perm_out)
+        if getattr(lay, "quantized", False):  # W's codes / scales (runner.py:159-161)
+            ri, ci = lay.perm_in.device(lay.device)[1], lay.perm_out.device(lay.device)[1]
+            codes = torch.empty_like(lay.codes)
+            scales = torch.empty_like(lay.scales)
+            N.call("poetx_quant_gather", N.BF16, lay.m, lay.n, lay.n, ri.data_ptr(), ci.data_ptr(), lay.codes.data_ptr(),
+                   lay.scales.data_ptr(), codes.data_ptr(), scales.data_ptr(), N.stream_ptr(lay.device))
+            t[f"{key}/base_codes"] = codes
+            t[f"{key}/base_scales"] = scales
+        else:
+            t[f"{key}/base"] = unpermuted_weight(lay.premerged, lay.perm_in, lay.perm_out)
         t[f"{key}/perm_in"] = lay.perm_in.forward.astype(np.uint32)
         t[f"{key}/perm_out"] = lay.perm_out.forward.astype(np.uint32)
         t[f"{key}/merge_count"] = np.array([lay.merge_count], dtype=np.uint32)
@@ -177,13 +186,18 @@ def restore_trainer(trainer, tensors: dict) -> int:
         _restore(model.dense.param[off:off + n], f"param/{name}", tensors)
     for lay in model.poet_layers():
         key = f"layer/{lay.name}"
-        base = _get(tensors, f"{key}/base")
-        if base.shape != (lay.m, lay.n):
-            raise CheckpointError(f"tensor {key}/base mismatch: stored {base.shape}, expected {(lay.m, lay.n)}")
         pin = PermutationMap.from_forward(_get(tensors, f"{key}/perm_in").astype(np.int32))
         pout = PermutationMap.from_forward(_get(tensors, f"{key}/perm_out").astype(np.int32))
-        w = torch.from_numpy(base).to(lay.device).to(torch.bfloat16)
-        lay.install(w, pin, pout)
+        if getattr(lay, "quantized", False):
+            codes, scales = tensors.get(f"{key}/base_codes"), tensors.get(f"{key}/base_scales")
+            if codes is None or scales is None:
+                raise CheckpointError(f"checkpoint missing quantized base for {lay.name}")
+            lay.install_quantized(torch.from_numpy(codes), torch.from_numpy(scales), pin, pout)
+        else:
+            base = _get(tensors, f"{key}/base")
+            if base.shape != (lay.m, lay.n):
+                raise CheckpointError(f"tensor {key}/base mismatch: stored {base.shape}, expected {(lay.m, lay.n)}")
+            lay.install(torch.from_numpy(base).to(lay.device).to(torch.bfloat16), pin, pout)
         lay.merge_count = int(_get(tensors, f"{key}/merge_count")[0])
     model.refresh_maps()
     for tag, grp in (("poet", model.poet), ("dense", model.dense)):

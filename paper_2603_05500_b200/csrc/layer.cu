@@ -17,6 +17,11 @@ int segmented_outer(int dt, int64_t T, int64_t nb, int64_t b, const void* x, con
 size_t cnp_ws_bytes(int dt, int64_t nb, int64_t b, int k);
 size_t outer_ws_bytes(int dt, int64_t T, int64_t nb, int64_t b);
 size_t tc_outer_ws_bytes(int64_t T, int64_t nb, int64_t b);
+int quant_dequant(int dt, int64_t rows, int64_t cols, const int8_t* codes, const void* scales,
+                  const int32_t* ri, const int32_t* ci, void* out, cudaStream_t st, int64_t ld = 0);
+int quant_rows(int dt, int64_t rows, int64_t cols, const void* w, int8_t* codes, void* scales, cudaStream_t st);
+int quant_gather(int dt, int64_t rows, int64_t cols, const int32_t* ri, const int32_t* ci, const int8_t* codes,
+                 const void* scales, int8_t* codes_out, void* scales_out, cudaStream_t st, int64_t ld = 0);
 }  // namespace poetx
 
 using namespace poetx;
@@ -33,7 +38,27 @@ int check_desc(const poetx_layer_desc* d) {
   POETX_REQUIRE(d->variant == POETX_FAST || d->variant == POETX_MEM, POETX_ECONFIG,
                 "variant must be fast or mem");
   POETX_REQUIRE(d->neumann_k >= 1, POETX_ECONFIG, "neumann_k must be >= 1, got %d", d->neumann_k);
+  POETX_REQUIRE(!d->pm_codes || d->variant == POETX_MEM, POETX_ECONFIG,
+                "quantized base requires the mem variant");
+  POETX_REQUIRE(!d->pm_codes || d->pm_scales, POETX_ESHAPE, "layer: quantized base without scales");
   return POETX_OK;
+}
+
+bool quantized(const poetx_layer_desc* d) { return d->pm_codes != nullptr; }
+
+// the premerged weight for a GEMM: the bf16/fp32/fp64 copy, or the int8
+// codes dequantized into a workspace scratch (POET-XQ)
+const void* layer_pm(const poetx_layer_desc* d, Workspace& w, cudaStream_t st, int& rc) {
+  rc = POETX_OK;
+  if (!quantized(d)) return d->premerged;
+  void* s = w.take_bytes(static_cast<size_t>(d->m * d->n) * elt_size(d->dtype));
+  if (!s) {
+    set_error("layer: workspace too small for the dequantized weight");
+    rc = POETX_ESHAPE;
+    return nullptr;
+  }
+  rc = quant_dequant(d->dtype, d->m, d->n, d->pm_codes, d->pm_scales, nullptr, nullptr, s, st);
+  return s;
 }
 
 // G used by the activation path: the bf16 copy for BF16 layers
@@ -109,7 +134,8 @@ size_t poetx_layer_workspace_bytes(const poetx_layer_desc* d, int64_t T) {
     if (t2 > outer) outer = t2;
   }
   size_t cnp = cnp_bwd_ws(d);
-  return 4 * act + grads + (outer > cnp ? outer : cnp) + 8192;
+  const size_t deq = quantized(d) ? align_up(static_cast<size_t>(d->m * d->n) * e) : 0;
+  return 4 * act + grads + deq + (outer > cnp ? outer : cnp) + 8192;
 }
 
 int poetx_layer_factors(const poetx_layer_desc* d, poetx_layer_factors_t* f, void* ws,
@@ -148,6 +174,9 @@ int poetx_layer_forward_ex(const poetx_layer_desc* d, const poetx_layer_factors_
   void* b2 = wsp.take_bytes(T * w * e);
   void* b3 = wsp.take_bytes(T * w * e);
   POETX_REQUIRE(b1 && b2 && b3, POETX_ESHAPE, "layer_forward: workspace too small");
+  int qrc;
+  const void* pm = layer_pm(d, wsp, st, qrc);
+  POETX_TRY(qrc);
   void* t = saved_t ? saved_t : b3;
   // u = x[:, pi_in]  (permute_features 'inverse', layer.py:220) -- or supplied
   const void* u = x;
@@ -158,7 +187,7 @@ int poetx_layer_forward_ex(const poetx_layer_desc* d, const poetx_layer_factors_
   // a = u blockdiag(G_R)  (mm1, layer.py:221)
   POETX_TRY(apply_features(dt, T, d->m / d->b, d->b, act_g(d, f->g_r, f->g_r_lowp), 0, u, b2, st));
   // t = a PM  (mm2, layer.py:222)
-  POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b2, d->m, 0, d->premerged, d->n, 0, t, d->n, 0, stream));
+  POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b2, d->m, 0, pm, d->n, 0, t, d->n, 0, stream));
   // v = t blockdiag(G_P)  (mm3, layer.py:223)
   void* v = out_raw ? z : b1;
   POETX_TRY(apply_features(dt, T, d->n / d->b, d->b, act_g(d, f->g_p, f->g_p_lowp), 0, t, v, st));
@@ -192,6 +221,9 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   void* dgp = dg_mode ? dg_p_out : wsp.take_bytes(nbp * b * b * acc);
   POETX_REQUIRE(b1 && b2 && b3 && b4 && dgr && dgp, POETX_ESHAPE,
                 "layer_backward: workspace too small");
+  int qrc;
+  const void* pm = layer_pm(d, wsp, st, qrc);
+  POETX_TRY(qrc);
   const int dg_acc = dg_mode ? accumulate : 0;
   Workspace tail(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
   const void* gr = act_g(d, f->g_r, f->g_r_lowp);
@@ -213,7 +245,7 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
       u0 = b2;
     }
     POETX_TRY(apply_features(dt, T, nbr, b, gr, 0, u0, b3, st));
-    POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b3, d->m, 0, d->premerged, d->n, 0, b4, d->n, 0, stream));
+    POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b3, d->m, 0, pm, d->n, 0, b4, d->n, 0, stream));
     t = b4;
   }
   // dG_P = segmented_outer(t, dv)  (layer.py:247)
@@ -221,7 +253,7 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   // dt = dv blockdiag(G_P)^T  (layer.py:248)
   POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, dv, b2, st));
   // da = dt PM^T  (layer.py:249)
-  POETX_TRY(poetx_matmul(dt, T, d->m, d->n, b2, d->n, 0, d->premerged, d->n, 1, b3, d->m, 0, stream));
+  POETX_TRY(poetx_matmul(dt, T, d->m, d->n, b2, d->n, 0, pm, d->n, 1, b3, d->m, 0, stream));
   // u = x[:, pi_in]  (layer.py:250) -- or the supplied pre-gathered input
   const void* u = x;
   if (!in_gathered) {
@@ -277,8 +309,9 @@ int poetx_layer_backward_dg(const poetx_layer_desc* d, const poetx_layer_factors
 size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d) {
   if (check_desc(d) != POETX_OK) return 0;
   size_t acc = elt_size(param_dtype(d->dtype));
+  size_t q = quantized(d) ? align_up(static_cast<size_t>(d->m * d->n)) + align_up(static_cast<size_t>(d->m) * acc) : 0;
   return 3 * align_up(static_cast<size_t>(d->m * d->n) * acc) +
-         align_up(static_cast<size_t>(d->m + d->n) * 4) + 4096;
+         align_up(static_cast<size_t>(d->m + d->n) * 4) + q + 4096;
 }
 
 int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_p,
@@ -299,7 +332,10 @@ int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_
   POETX_REQUIRE(pm && mid1 && mid2 && ridx && cidx, POETX_ESHAPE, "layer_merge: workspace too small");
   // mid = blockdiag(G_R) PM blockdiag(G_P) in the parameter type (layer.py:269-271)
   const void* pm_src = d->premerged;
-  if (dt == POETX_BF16) {
+  if (quantized(d)) {
+    POETX_TRY(quant_dequant(pdt, m, n, d->pm_codes, d->pm_scales, nullptr, nullptr, pm, st));
+    pm_src = pm;
+  } else if (dt == POETX_BF16) {
     POETX_TRY(gather_to(POETX_BF16, POETX_F32, m, n, nullptr, nullptr, d->premerged, pm, st));
     pm_src = pm;
   }
@@ -319,6 +355,42 @@ int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_
     POETX_TRY(gather_to(pdt, dt, m, n, ridx, cidx, mid2, premerged_out, st));
   }
   return POETX_OK;
+}
+
+int poetx_layer_merge_quant(const poetx_layer_desc* d, const void* g_r, const void* g_p,
+                            const int32_t* new_in_fwd, const int32_t* new_out_fwd, int8_t* codes_out,
+                            void* scales_out, void* w_out, void* ws, size_t ws_bytes, void* stream) {
+  POETX_TRY(check_desc(d));
+  POETX_REQUIRE(quantized(d), POETX_ESTATE, "layer_merge_quant: layer base is not quantized");
+  POETX_REQUIRE(g_r && g_p && new_in_fwd && new_out_fwd && codes_out && scales_out, POETX_ESHAPE,
+                "layer_merge_quant: missing arguments");
+  cudaStream_t st = as_stream(stream);
+  const int dt = d->dtype, pdt = param_dtype(dt);
+  const int64_t m = d->m, n = d->n, b = d->b;
+  const size_t acc = elt_size(pdt);
+  Workspace wsp(ws, ws_bytes);
+  void* pm = wsp.take_bytes(m * n * acc);
+  void* mid1 = wsp.take_bytes(m * n * acc);
+  void* mid2 = wsp.take_bytes(m * n * acc);
+  int32_t* ridx = wsp.take<int32_t>(m);
+  int32_t* cidx = wsp.take<int32_t>(n);
+  int8_t* qc = wsp.take<int8_t>(static_cast<size_t>(m * n));
+  void* qs = wsp.take_bytes(m * acc);
+  POETX_REQUIRE(pm && mid1 && mid2 && ridx && cidx && qc && qs, POETX_ESHAPE, "layer_merge_quant: workspace too small");
+  // mid = blockdiag(G_R) deq(PM) blockdiag(G_P)  (layer.py:260-271, dequantized premerged)
+  POETX_TRY(quant_dequant(pdt, m, n, d->pm_codes, d->pm_scales, nullptr, nullptr, pm, st));
+  POETX_TRY(apply_weight_rows(pdt, m / b, b, n, g_r, 0, pm, mid1, st));
+  POETX_TRY(apply_features(pdt, m, n / b, b, g_p, 0, mid1, mid2, st));
+  if (w_out) POETX_TRY(gather_to(pdt, dt, m, n, d->perm_in_inv, d->perm_out_inv, mid2, w_out, st));
+  // requantize per row (rows of the new base W are rows of mid, columns only
+  // permuted: absmax and every code are invariant), then gather the codes
+  // into the new premerged order PM'[i,j] = W[new_in(i), new_out(j)]
+  POETX_TRY(quant_rows(pdt, m, n, mid2, qc, qs, st));
+  compose_kernel<<<grid_for(m, 256), 256, 0, st>>>(m, d->perm_in_inv, new_in_fwd, ridx);
+  POETX_LAUNCHED("compose");
+  compose_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, d->perm_out_inv, new_out_fwd, cidx);
+  POETX_LAUNCHED("compose");
+  return quant_gather(dt, m, n, ridx, cidx, qc, qs, codes_out, scales_out, st);
 }
 
 }  // extern "C"

@@ -31,6 +31,7 @@ from . import _native as N
 from .blockdiag import orthogonality_error
 from .cnp import SkewParams, cayley_exact, num_pairs
 from .errors import ConfigError, ShapeError, StateError
+from .quant import QuantizedMatrix
 from .permute import PermutationMap, sample_permutation
 from .rng import Rng
 
@@ -144,7 +145,7 @@ class PoetLinearLayer:
 
     @property
     def quantized(self) -> bool:
-        return False
+        return isinstance(self.premerged, QuantizedMatrix)
 
     def trainable_param_count(self) -> int:
         return int(self.q_r.packed.numel() + self.q_p.packed.numel())
@@ -161,9 +162,12 @@ class PoetLinearLayer:
         return out
 
     @property
-    def base(self) -> torch.Tensor:
+    def base(self):
         """Frozen weight W recovered from the premerged copy:
-        W[r, c] = PM[pi_in^-1(r), pi_out^-1(c)] (exact)."""
+        W[r, c] = PM[pi_in^-1(r), pi_out^-1(c)] (exact; a QuantizedMatrix
+        when the base is quantized, as in the reference)."""
+        if self.quantized:
+            return self.premerged.gather(self.perm_in.inverse, self.perm_out.inverse)
         _, ri = self.perm_in.device(self.device)
         _, ci = self.perm_out.device(self.device)
         out = torch.empty((self.m, self.n), dtype=self.dtype, device=self.device)
@@ -175,6 +179,11 @@ class PoetLinearLayer:
     def base(self, w) -> None:
         if isinstance(w, np.ndarray):
             w = torch.from_numpy(np.ascontiguousarray(w))
+        if isinstance(w, QuantizedMatrix):
+            if w.shape != (self.m, self.n):
+                raise ShapeError(f"base weight shape {w.shape}, expected ({self.m}, {self.n})")
+            self.premerged = w.gather(self.perm_in.forward, self.perm_out.forward)
+            return
         if tuple(w.shape) != (self.m, self.n):
             raise ShapeError(f"base weight shape {tuple(w.shape)}, expected ({self.m}, {self.n})")
         self.premerged = self._premerge(w.to(self.device, self.dtype).contiguous(), self.perm_in, self.perm_out)
@@ -185,13 +194,21 @@ class PoetLinearLayer:
             raise ShapeError("permutation sizes do not match layer dims")
         w = self.base
         self.perm_in, self.perm_out = perm_in, perm_out
-        self.premerged = self._premerge(w, perm_in, perm_out)
+        if isinstance(w, QuantizedMatrix):
+            self.premerged = w.gather(perm_in.forward, perm_out.forward)
+        else:
+            self.premerged = self._premerge(w, perm_in, perm_out)
 
     def quantize_base(self) -> None:
-        """int8 base (POET-XQ) -- mem variant only (layer.py:169-177)."""
+        """Switch the frozen weight to per-row int8 (POET-XQ, layer.py:169-177).
+        Mem variant only: the fast variant's saved mm2 output would defeat
+        the point.  Row quantization commutes with the premerge gathers, so
+        the premerged codes are the quantized base gathered exactly."""
         if self.variant != "mem":
             raise ConfigError("quantized base requires the mem variant")
-        raise ConfigError("int8 premerged base (POET-XQ) is not built in this round")
+        if not self.quantized:
+            self.premerged = QuantizedMatrix.quantize(self.base).gather(self.perm_in.forward,
+                                                                        self.perm_out.forward)
 
     # -- descriptor ----------------------------------------------------------------
 
@@ -205,7 +222,12 @@ class PoetLinearLayer:
         d.m, d.n, d.b = self.m, self.n, self.block_size
         d.perm_in_fwd, d.perm_in_inv = fi.data_ptr(), ii.data_ptr()
         d.perm_out_fwd, d.perm_out_inv = fo.data_ptr(), io.data_ptr()
-        d.premerged = self.premerged.data_ptr()
+        if self.quantized:
+            d.premerged = None
+            d.pm_codes = self.premerged.codes.data_ptr()
+            d.pm_scales = self.premerged.scales.data_ptr()
+        else:
+            d.premerged = self.premerged.data_ptr()
         return d
 
     def compute_factors(self, packed_r=None, packed_p=None) -> Factors:
@@ -282,6 +304,19 @@ class PoetLinearLayer:
     def _merge_call(self, g_r, g_p, new_in=None, new_out=None, want_w=False):
         d = self._desc()
         ws, wsb = N.workspace(N.lib().poetx_merge_workspace_bytes(d), self.device)
+        if self.quantized:
+            w = torch.empty((self.m, self.n), dtype=self.dtype, device=self.device) if want_w else None
+            if new_in is None:  # materialize only: the float transform of the dequantized base
+                N.call("poetx_layer_merge", d, g_r.contiguous().data_ptr(), g_p.contiguous().data_ptr(),
+                       None, None, None, N.ptr(w), ws, wsb, self._stream())
+                return None, w
+            q = self.premerged
+            codes = torch.empty_like(q.codes)
+            scales = torch.empty_like(q.scales)
+            N.call("poetx_layer_merge_quant", d, g_r.contiguous().data_ptr(), g_p.contiguous().data_ptr(),
+                   new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
+                   codes.data_ptr(), scales.data_ptr(), N.ptr(w), ws, wsb, self._stream())
+            return QuantizedMatrix(codes, scales, float_dtype=self.dtype), w
         pm_new = w = None
         ni = no = None
         if new_in is not None:
@@ -314,6 +349,8 @@ class PoetLinearLayer:
         new_out = sample_permutation(self.n, rng)
         drift = float("nan")
         old_base = self.base if compute_sv_drift else None
+        if isinstance(old_base, QuantizedMatrix):
+            old_base = old_base.dequantize()
         pm_new, w_new = self._merge_call(g_r, g_p, new_in, new_out, want_w=compute_sv_drift)
         if compute_sv_drift:
             sv_old = torch.linalg.svdvals(old_base.double())

@@ -29,6 +29,7 @@ import torch.nn.functional as F
 
 from . import _native as N
 from .cnp import num_pairs
+from .errors import ConfigError
 from .optim import ScheduleConfig, adamw_dyn_values, clip_threshold_at, fused_clip_adamw_dyn, lr_at
 from .permute import PermutationMap, sample_permutation
 from .rng import Rng
@@ -46,6 +47,7 @@ class LlamaConfig:
     seq: int = 256
     variant: str = "fast"
     neumann_k: int = 3
+    quantized: bool = False  # POET-XQ int8 frozen weights (mem variant only)
 
     @property
     def head_dim(self) -> int:
@@ -173,8 +175,11 @@ class PoetLinear(torch.nn.Module):
     parameters and its factor/cotangent blocks living in a PoetStack."""
 
     def __init__(self, name, m, n, stack: PoetStack, rng: Rng, *, variant="fast", neumann_k=3,
-                 std=None, device="cuda"):
+                 std=None, device="cuda", quantized=False):
         super().__init__()
+        if quantized and variant != "mem":
+            raise ConfigError("quantized base requires the mem variant")
+        self.quantized = quantized
         b = stack.b
         self.name, self.m, self.n, self.b = name, m, n, b
         self.variant, self.k = variant, neumann_k
@@ -200,6 +205,9 @@ class PoetLinear(torch.nn.Module):
         self.pin_dev = tuple(t.clone() for t in self.perm_in.device(self.device))
         self.pout_dev = tuple(t.clone() for t in self.perm_out.device(self.device))
         self.premerged = torch.empty((m, n), dtype=torch.bfloat16, device=self.device)
+        if quantized:  # int8 premerged codes + per-row fp32 scales (fixed addresses)
+            self.codes = torch.empty((m, n), dtype=torch.int8, device=self.device)
+            self.scales = torch.empty(m, dtype=torch.float32, device=self.device)
         self._install(w)
         del w
         self.fstruct = N.LayerFactors(self.packed_r.data_ptr(), self.packed_p.data_ptr(), None, None,
@@ -211,6 +219,11 @@ class PoetLinear(torch.nn.Module):
         cf, _ = self.perm_out.device(self.device)
         N.call("poetx_gather2d", N.BF16, self.m, self.n, rf.data_ptr(), cf.data_ptr(), w.data_ptr(),
                self.premerged.data_ptr(), N.stream_ptr(self.device))
+        if self.quantized:
+            # row quantization commutes with the premerge gathers (quant.py:63-74)
+            N.call("poetx_quantize_rows", N.BF16, self.m, self.n, self.premerged.data_ptr(), self.codes.data_ptr(),
+                   self.scales.data_ptr(), N.stream_ptr(self.device))
+            self.premerged = None  # the bf16 copy is not kept
         self._set_desc()
 
     def install(self, w: torch.Tensor, perm_in: PermutationMap, perm_out: PermutationMap):
@@ -219,7 +232,22 @@ class PoetLinear(torch.nn.Module):
         self.perm_in, self.perm_out = perm_in, perm_out
         for dst, src in zip(self.pin_dev + self.pout_dev, perm_in.device(self.device) + perm_out.device(self.device)):
             dst.copy_(src)
+        if self.quantized and self.premerged is None:
+            self.premerged = torch.empty((self.m, self.n), dtype=torch.bfloat16, device=self.device)
         self._install(w.to(self.device, torch.bfloat16).contiguous())
+
+    def install_quantized(self, codes: torch.Tensor, scales: torch.Tensor, perm_in: PermutationMap,
+                          perm_out: PermutationMap):
+        """Checkpoint load of a POET-XQ layer: W's int8 codes/scales, gathered
+        into the premerged order in the quantized domain (exact)."""
+        self.perm_in, self.perm_out = perm_in, perm_out
+        for dst, src in zip(self.pin_dev + self.pout_dev, perm_in.device(self.device) + perm_out.device(self.device)):
+            dst.copy_(src)
+        codes, scales = codes.to(self.device).contiguous(), scales.to(self.device, torch.float32).contiguous()
+        N.call("poetx_quant_gather", N.BF16, self.m, self.n, self.n, self.pin_dev[0].data_ptr(), self.pout_dev[0].data_ptr(),
+               codes.data_ptr(), scales.data_ptr(), self.codes.data_ptr(), self.scales.data_ptr(),
+               N.stream_ptr(self.device))
+        self._set_desc()
 
     def _set_desc(self):
         fi, ii = self.pin_dev
@@ -229,7 +257,10 @@ class PoetLinear(torch.nn.Module):
         d.m, d.n, d.b = self.m, self.n, self.b
         d.perm_in_fwd, d.perm_in_inv = fi.data_ptr(), ii.data_ptr()
         d.perm_out_fwd, d.perm_out_inv = fo.data_ptr(), io.data_ptr()
-        d.premerged = self.premerged.data_ptr()
+        if self.quantized:
+            d.pm_codes, d.pm_scales = self.codes.data_ptr(), self.scales.data_ptr()
+        else:
+            d.premerged = self.premerged.data_ptr()
         self.desc = d
 
     def ws_bytes(self, T: int) -> int:
@@ -254,11 +285,19 @@ class PoetLinear(torch.nn.Module):
         new_in = sample_permutation(self.m, rng)
         new_out = sample_permutation(self.n, rng)
         ws, wsb = N.workspace(N.lib().poetx_merge_workspace_bytes(self.desc), self.device)
-        pm_new = torch.empty_like(self.premerged)
-        N.call("poetx_layer_merge", self.desc, g_r.data_ptr(), g_p.data_ptr(),
-               new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
-               pm_new.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
-        self.premerged.copy_(pm_new)
+        if self.quantized:
+            codes, scales = torch.empty_like(self.codes), torch.empty_like(self.scales)
+            N.call("poetx_layer_merge_quant", self.desc, g_r.data_ptr(), g_p.data_ptr(),
+                   new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
+                   codes.data_ptr(), scales.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
+            self.codes.copy_(codes)
+            self.scales.copy_(scales)
+        else:
+            pm_new = torch.empty_like(self.premerged)
+            N.call("poetx_layer_merge", self.desc, g_r.data_ptr(), g_p.data_ptr(),
+                   new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
+                   pm_new.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
+            self.premerged.copy_(pm_new)
         self.perm_in, self.perm_out = new_in, new_out
         for dst, src in zip(self.pin_dev + self.pout_dev, new_in.device(self.device) + new_out.device(self.device)):
             dst.copy_(src)
@@ -496,7 +535,8 @@ class PoetLlama(torch.nn.Module):
             for p in self.PROJ:
                 m, n = shapes[p]
                 mods[p] = PoetLinear(f"{i}.{p}", m, n, self.stack, Rng.keyed(seed, "init", i, p),
-                                     variant=cfg.variant, neumann_k=cfg.neumann_k, device=dev)
+                                     variant=cfg.variant, neumann_k=cfg.neumann_k, device=dev,
+                                     quantized=cfg.quantized)
             self.layers.append(mods)
         hd = cfg.head_dim
         inv = 1.0 / (10000 ** (torch.arange(0, hd, 2, device=dev, dtype=torch.float32) / hd))

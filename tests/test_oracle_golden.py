@@ -140,3 +140,31 @@ def test_optim_transcript_bitwise():
     steps = d["lr_steps"]
     assert np.array_equal([O.lr_at(int(k), 0.08, 3000, 100) for k in steps], d["lr"])
     assert np.array_equal([O.lr_at(int(k), 0.08, 3000, 100, poet=True) for k in steps], d["lr_poet"])
+
+
+# -- POET-XQ (quant.py, quantized layer paths) --------------------------------
+
+
+@pytest.mark.parametrize("tag", ["gauss_f32", "gauss_f64", "ties_f64", "wide_f32"])
+def test_quantize_rows_bitwise(tag):
+    d = load("quant.npz")
+    codes, scales = O.quantize_rows(d[f"q_{tag}_w"])
+    assert codes.dtype == np.int8 and scales.dtype == d[f"q_{tag}_w"].dtype
+    assert np.array_equal(codes, d[f"q_{tag}_codes"])
+    assert np.array_equal(scales, d[f"q_{tag}_scales"])
+
+
+@pytest.mark.parametrize("tag", ["f32", "f64"])
+def test_quantized_layer_bitwise(tag):
+    d = load("quant.npz")
+    lay = O.OracleLayer(d[f"l_{tag}_base"], 8, d[f"l_{tag}_perm_in"], d[f"l_{tag}_perm_out"], variant="mem",
+                        quantized=True)
+    lay.q_r[...] = d[f"l_{tag}_q_r"]
+    lay.q_p[...] = d[f"l_{tag}_q_p"]
+    z, cache = lay.forward(d[f"l_{tag}_x"])
+    gr, gp, dx = lay.backward(cache, d[f"l_{tag}_dz"])
+    for got, key in ((z, "z"), (gr, "gr"), (gp, "gp"), (dx, "dx")):
+        assert np.array_equal(got, d[f"l_{tag}_{key}"]), key
+    lay.merge_and_reinit(d[f"l_{tag}_new_perm_in"], d[f"l_{tag}_new_perm_out"])
+    assert np.array_equal(lay.codes, d[f"l_{tag}_merged_codes"])
+    assert np.array_equal(lay.scales, d[f"l_{tag}_merged_scales"])

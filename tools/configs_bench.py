@@ -29,10 +29,12 @@ CASES = {
     "350m-poetx": dict(kind="poet", model="llama-350m", mb=32),
     "1b-poetx-fast": dict(kind="poet", model="llama-1b", mb=32),
     "1b-poetx-mem": dict(kind="poet", model="llama-1b", mb=32, variant="mem"),
+    "1b-poetxq-mem": dict(kind="poet", model="llama-1b", mb=32, variant="mem", quantized=True),
     "1b-adamw": dict(kind="adamw", model="llama-1b", mb=32),
     "1b-lora": dict(kind="lora", model="llama-1b", mb=32, rank=127),
     "8b-poetx-fast": dict(kind="poet", model="llama-8b", mb=1),
     "8b-poetx-mem": dict(kind="poet", model="llama-8b", mb=1, variant="mem"),
+    "8b-poetxq-mem": dict(kind="poet", model="llama-8b", mb=1, variant="mem", quantized=True),
     "8b-adamw": dict(kind="adamw", model="llama-8b", mb=1),
     "8b-lora": dict(kind="lora", model="llama-8b", mb=1, rank=127),
     "8b-poetx-fast-mb8": dict(kind="poet", model="llama-8b", mb=8),
@@ -100,7 +102,7 @@ def run_model(c):
 
     from paper_2603_05500_b200.trainer import Trainer, llama_config
 
-    cfg = llama_config(c["model"], variant=c.get("variant", "fast"))
+    cfg = llama_config(c["model"], variant=c.get("variant", "fast"), quantized=c.get("quantized", False))
     mb = c["mb"]
     g = torch.Generator().manual_seed(0)
     toks = [torch.randint(0, cfg.vocab, (mb, cfg.seq + 1), generator=g).cuda() for _ in range(2)]
@@ -118,7 +120,8 @@ def run_model(c):
         step = lambda t: tr.step(t[:, :-1], t[:, 1:])  # noqa: E731
     static_gb = torch.cuda.memory_allocated() / 1e9
     ms = timed_steps(step, toks, 3, 10)
-    return {"model": cfg.name, "variant": cfg.variant if c["kind"] == "poet" else None, "micro_batch": mb,
+    return {"model": cfg.name, "variant": cfg.variant if c["kind"] == "poet" else None,
+            "int8_base": bool(c.get("quantized", False)), "micro_batch": mb,
             "seq": cfg.seq, "tokens_per_step": mb * cfg.seq, "tokens_per_s": mb * cfg.seq / (ms / 1e3),
             "ms_per_step": ms, "peak_hbm_gb": torch.cuda.max_memory_allocated() / 1e9,
             "static_hbm_gb": static_gb, "trainable_params": int(trainable),
