@@ -63,10 +63,16 @@ __global__ void __launch_bounds__(256) dequant_rows_kernel(int64_t rows, int64_t
     O* orow = out + r * cols;
     if (!ci && cols % 16 == 0 && ld % 16 == 0) {
       for (int64_t j = threadIdx.x * 16; j < cols; j += blockDim.x * 16) {
-        const int4 v = *reinterpret_cast<const int4*>(crow + j);
+        const int4 v = __ldcs(reinterpret_cast<const int4*>(crow + j));
         const int8_t* c = reinterpret_cast<const int8_t*>(&v);
+        __align__(16) O o[16];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) orow[j + q] = dq<S, O>(c[q], s);
+        for (int q = 0; q < 16; ++q) o[q] = dq<S, O>(c[q], s);
+        // 16 outputs = 32 / 64 / 128 bytes: whole 16-byte vector stores
+        const uint4* src = reinterpret_cast<const uint4*>(o);
+        uint4* dst = reinterpret_cast<uint4*>(orow + j);
+#pragma unroll
+        for (int q = 0; q < static_cast<int>(sizeof(O)) ; ++q) dst[q] = src[q];
       }
     } else {
       for (int64_t j = threadIdx.x; j < cols; j += blockDim.x) orow[j] = dq<S, O>(crow[ci ? ci[j] : j], s);
