@@ -39,7 +39,7 @@ def test_fused_block_matches_unfused_reference_path():
         loss = m(tok[:, :-1], tok[:, 1:])
         m.backward_dense_grads(loss)
         m.stack.backward_factors()
-        out.append((float(loss), m.poet.grad.clone(), m.dense.grad.clone()))
+        out.append((float(loss.detach()), m.poet.grad.clone(), m.dense.grad.clone()))
     (l0, p0, d0), (l1, p1, d1) = out
     assert abs(l0 - l1) <= 1e-2 * abs(l0)
     for a, b in ((p0, p1), (d0, d1)):
@@ -68,3 +68,23 @@ def test_cuda_graph_replay_matches_eager_including_merge():
         assert abs(a - b) <= 1e-3 * abs(a), (a, b)
     assert eager.model.poet_layers()[0].merge_count == graphed.model.poet_layers()[0].merge_count == 2
     assert torch.allclose(eager.model.poet.param, graphed.model.poet.param, atol=1e-5, rtol=1e-3)
+
+
+def test_fast_and_mem_variants_bitwise_equal_in_the_model():
+    """The reference's fast == mem contract (test_layer.py:145-162) at model
+    level: the mem variant recomputes t AND rebuilds every layer input from
+    the neighbours' saved tensors, with the same deterministic kernels, so
+    losses and updated parameters match the fast variant bit for bit."""
+    from paper_2603_05500_b200.trainer import Trainer, llama_config
+
+    toks = [torch.randint(0, 32000, (4, 65), generator=torch.Generator().manual_seed(i)).cuda() for i in range(3)]
+    runs = []
+    for variant in ("fast", "mem"):
+        cfg = llama_config("llama-60m", layers=2, seq=64, variant=variant)
+        tr = Trainer(cfg, 4, seed=7, merge_gap=2, base_lr=3e-3)
+        tr.model.concurrent = False  # same launch order in both runs
+        losses = [float(tr.step(t[:, :-1], t[:, 1:])) for t in toks]
+        runs.append((losses, tr.model.poet.param.clone(), tr.model.dense.param.clone()))
+    (lf, pf, df), (lm, pm, dm) = runs
+    assert lf == lm
+    assert torch.equal(pf, pm) and torch.equal(df, dm)
