@@ -1,6 +1,10 @@
 // PoetLinearLayer orchestration (layer.py:181-314) behind the C ABI:
 // factors (CNP on both sides), forward chain, backward chain, merge.
 // Kernels are stream-ordered; nothing here synchronises the host.
+#include <cstdlib>
+#include <mutex>
+#include <unordered_map>
+
 #include "common.cuh"
 #include "simt_gemm.cuh"
 
@@ -112,6 +116,41 @@ int gather_to(int src_dt, int dst_dt, int64_t rows, int64_t cols, const int32_t*
     return gather_convert<__nv_bfloat16, float>(rows, cols, ridx, cidx, x, y, st);
   set_error("gather_to: unsupported conversion %d -> %d", src_dt, dst_dt);
   return POETX_ESHAPE;
+}
+
+// Side stream per calling stream for the backward's segmented outer
+// products (dG_P = t^T dv, dG_R = u^T da), which only READ buffers the main
+// chain (dt -> adjoint GEMM -> du) reads too: forked and joined with events,
+// so they fill the SMs the main chain's kernel tails leave idle.  Inside a
+// CUDA-graph capture the fork/join become graph edges.
+struct Side {
+  cudaStream_t s = nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
+};
+bool side_enabled() {
+  static int on = [] {
+    const char* e = getenv("POETX_LAYER_SIDE");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return on != 0;
+}
+Side* side_for(cudaStream_t st) {
+  static std::mutex mu;
+  static std::unordered_map<cudaStream_t, Side> sides;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = sides.find(st);
+  if (it != sides.end()) return &it->second;
+  Side sd;
+  int prio = 0;
+  cudaStreamGetPriority(st, &prio);
+  if (cudaStreamCreateWithPriority(&sd.s, cudaStreamNonBlocking, prio) != cudaSuccess ||
+      cudaEventCreateWithFlags(&sd.e0, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&sd.e1, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&sd.e2, cudaEventDisableTiming) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return &sides.emplace(st, sd).first->second;
 }
 
 }  // namespace
@@ -248,8 +287,16 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
     POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b3, d->m, 0, pm, d->n, 0, b4, d->n, 0, stream));
     t = b4;
   }
+  // the two segmented outer products run on a side stream unless the main
+  // chain would overwrite dv's buffer with u (b1) while the first one reads it
+  Side* sd = (side_enabled() && (dz_gathered || in_gathered)) ? side_for(st) : nullptr;
+  cudaStream_t so = sd ? sd->s : st;
+  if (sd) {
+    cudaEventRecord(sd->e0, st);
+    cudaStreamWaitEvent(so, sd->e0, 0);
+  }
   // dG_P = segmented_outer(t, dv)  (layer.py:247)
-  POETX_TRY(segmented_outer(dt, T, nbp, b, t, dv, dgp, dg_acc, tail, st));
+  POETX_TRY(segmented_outer(dt, T, nbp, b, t, dv, dgp, dg_acc, tail, so));
   // dt = dv blockdiag(G_P)^T  (layer.py:248)
   POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, dv, b2, st));
   // da = dt PM^T  (layer.py:249)
@@ -262,7 +309,11 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   }
   // dG_R = segmented_outer(u, da)  (layer.py:251)
   Workspace tail2(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
-  POETX_TRY(segmented_outer(dt, T, nbr, b, u, b3, dgr, dg_acc, tail2, st));
+  if (sd) {
+    cudaEventRecord(sd->e1, st);
+    cudaStreamWaitEvent(so, sd->e1, 0);
+  }
+  POETX_TRY(segmented_outer(dt, T, nbr, b, u, b3, dgr, dg_acc, tail2, so));
   if (dx) {
     // du = da blockdiag(G_R)^T ; dx = du[:, pi_in^-1]  (layer.py:252-253)
     if (dx_raw) {
@@ -271,6 +322,10 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
       POETX_TRY(apply_features(dt, T, nbr, b, gr, 1, b3, b2, st));
       POETX_TRY(gather2d(dt, T, d->m, nullptr, d->perm_in_inv, b2, dx, st));
     }
+  }
+  if (sd) {  // join: everything after this call sees dG_R / dG_P
+    cudaEventRecord(sd->e2, so);
+    cudaStreamWaitEvent(st, sd->e2, 0);
   }
   if (dg_mode) return POETX_OK;
   // packed grads = P(cnp_backward(.))  (layer.py:254-255)
