@@ -133,6 +133,19 @@ class PoetStack:
         N.call("poetx_cnp_backward_tc", self.nb, self.b, self.qq2.data_ptr(), self.dg.data_ptr(),
                self.group.grad.data_ptr(), 0, ws, wsb, N.stream_ptr(self.device))
 
+    # block ranges (one decoder block's seven layers are contiguous in the stack)
+    def forward_factors_range(self, off: int, nb: int):
+        b, pairs = self.b, self.pairs
+        ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(nb, b), self.device)
+        N.call("poetx_cnp_forward_tc", nb, b, self.group.param[off * pairs:].data_ptr(), self.qq2[off].data_ptr(),
+               self.g16[off].data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
+
+    def backward_factors_range(self, off: int, nb: int):
+        b, pairs = self.b, self.pairs
+        ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(nb, b), self.device)
+        N.call("poetx_cnp_backward_tc", nb, b, self.qq2[off].data_ptr(), self.dg[off].data_ptr(),
+               self.group.grad[off * pairs:].data_ptr(), 0, ws, wsb, N.stream_ptr(self.device))
+
 
 # --------------------------------------------------------------------------
 # POET-X linear as an autograd op
@@ -370,6 +383,28 @@ def _swiglu_regather(vg, vu, maps):
     return out
 
 
+class _CnpBackwardHook(torch.autograd.Function):
+    """Identity on the residual stream at a decoder block's input.  Its
+    backward runs once every layer of the block has produced its dG (they
+    all feed the gradient arriving here), so it launches the block's batched
+    CNP backward on the CNP stream, overlapping the backward of the blocks
+    below; the step joins the CNP stream before the optimizer."""
+
+    @staticmethod
+    def forward(ctx, h, model, i):
+        ctx.model, ctx.i = model, i
+        return h.view_as(h)
+
+    @staticmethod
+    def backward(ctx, dh):
+        model = ctx.model
+        cs = model.cnp_stream
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            model.stack.backward_factors_range(*model.block_ranges[ctx.i])
+        return dh, None, None
+
+
 def _ptrs(ts):
     import ctypes as C
     return (C.c_void_p * len(ts))(*[t.data_ptr() for t in ts])
@@ -551,6 +586,15 @@ class PoetLlama(torch.nn.Module):
         # idle; autograd replays the same stream assignment in backward
         self.side = [torch.cuda.Stream(dev), torch.cuda.Stream(dev)] if dev.type == "cuda" else []
         self.concurrent = bool(self.side)
+        # per-decoder-block CNP (forward one block ahead, backward as soon as a
+        # block's dG are complete) on its own stream
+        self.cnp_stream = torch.cuda.Stream(dev) if dev.type == "cuda" else None
+        self.block_ranges = []
+        for i in range(cfg.layers):
+            lo = self.stack.block_off[f"{i}.q.r"]
+            hi = self.stack.block_off[f"{i}.down.p"] + d // b
+            self.block_ranges.append((lo, hi - lo))
+        self.cnp_pipelined = False  # set per step by the trainer
         self.refresh_maps()
 
     def refresh_maps(self):
@@ -586,10 +630,22 @@ class PoetLlama(torch.nn.Module):
         h = F.embedding(tokens.reshape(-1), embed).to(torch.bfloat16)
         cos, sin = self.cos[:S].view(1, S, 1, hd // 2), self.sin[:S].view(1, S, 1, hd // 2)
         leaves = [embed]
+        pipe = self.cnp_pipelined and self.fused
+        main = torch.cuda.current_stream() if pipe else None
+        if pipe:
+            self.cnp_stream.wait_stream(main)  # fork (also joins it into a graph capture)
+            self.stack.forward_factors_range(*self.block_ranges[0])
         for i, mods in enumerate(self.layers):
             n1 = self.dense_param(f"{i}.norm1", (d,)).detach().requires_grad_(True)
             n2 = self.dense_param(f"{i}.norm2", (d,)).detach().requires_grad_(True)
             leaves += [n1, n2]
+            if pipe:
+                main.wait_stream(self.cnp_stream)          # G of block i is ready
+                if i + 1 < len(self.layers):                # block i+1's G overlaps block i
+                    self.cnp_stream.wait_stream(main)
+                    with torch.cuda.stream(self.cnp_stream):
+                        self.stack.forward_factors_range(*self.block_ranges[i + 1])
+                h = _CnpBackwardHook.apply(h, self, i)
             if self.fused:
                 h = self._block_fused(i, mods, h, n1, n2, B, S)
                 continue
@@ -730,10 +786,17 @@ class Trainer:
         optimizer scalars read from ``self.dyn``)."""
         model = self.model
         model.dense.grad.zero_()
-        model.stack.forward_factors()          # CNP of every block, one batched call
-        loss = model(tokens, targets)
-        model.backward_dense_grads(loss)       # layers leave dG in model.stack.dg
-        model.stack.backward_factors()         # batched CNP backward -> packed grads
+        model.cnp_pipelined = model.concurrent and model.fused
+        if model.cnp_pipelined:
+            # per-decoder-block CNP on the CNP stream, overlapped with the layers
+            loss = model(tokens, targets)
+            model.backward_dense_grads(loss)
+            torch.cuda.current_stream().wait_stream(model.cnp_stream)
+        else:
+            model.stack.forward_factors()      # CNP of every block, one batched call
+            loss = model(tokens, targets)
+            model.backward_dense_grads(loss)   # layers leave dG in model.stack.dg
+            model.stack.backward_factors()     # batched CNP backward -> packed grads
         if self.pg is not None:
             average_gradients([model.poet.grad, model.dense.grad], self.pg)
         self.last_sq, self.last_bad = fused_clip_adamw_dyn(
