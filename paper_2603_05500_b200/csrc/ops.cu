@@ -2,6 +2,7 @@
 // of the poetx_b200 C ABI (see include/poetx_b200.h for the contract and
 // the reference functions each one replaces).
 #include <cmath>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -390,6 +391,65 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Feature-major tile gather: a tile of 8 token rows is staged TRANSPOSED in
+// shared memory (one 16-byte slot per feature holding its 8 token values;
+// slots XOR-swizzled within groups of 8 so the transposing stores are
+// conflict-free), so gathering feature idx[j] for all 8 tokens is ONE
+// 16-byte LDS instead of eight conflicted 2-byte LDS: the random accesses
+// that bound the row-major kernel drop ~3x in smem wavefronts.  8x8 bf16
+// transposes are 32 PRMTs in registers on the way in and out.
+__device__ __forceinline__ void tr8x8(const uint4 (&r)[8], uint4 (&c)[8]) {
+  // c[col] word i = {row 2i, row 2i+1} of that column
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t a[4] = {r[2 * i].x, r[2 * i].y, r[2 * i].z, r[2 * i].w};
+    const uint32_t b[4] = {r[2 * i + 1].x, r[2 * i + 1].y, r[2 * i + 1].z, r[2 * i + 1].w};
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      const uint32_t lo = __byte_perm(a[w], b[w], 0x5410), hi = __byte_perm(a[w], b[w], 0x7632);
+      reinterpret_cast<uint32_t*>(&c[2 * w])[i] = lo;
+      reinterpret_cast<uint32_t*>(&c[2 * w + 1])[i] = hi;
+    }
+  }
+}
+__device__ __forceinline__ int fslot(int f) { return (f & ~7) | ((f ^ (f >> 3)) & 7); }
+
+__global__ void __launch_bounds__(256) permute_cols_t8_kernel(int64_t rows, int cols,
+                                                             const int32_t* __restrict__ idx,
+                                                             const __nv_bfloat16* __restrict__ x,
+                                                             __nv_bfloat16* __restrict__ y) {
+  extern __shared__ __align__(16) uint4 slots[];  // [cols] x 16 B
+  const int nv = cols / 8;
+  const int64_t tiles = (rows + 7) / 8;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t r0 = tile * 8;
+    const int nr = static_cast<int>(rows - r0 < 8 ? rows - r0 : 8);
+    for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+      uint4 rr[8], cc[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        rr[r] = r < nr ? __ldcs(reinterpret_cast<const uint4*>(x + (r0 + r) * cols) + c) : make_uint4(0, 0, 0, 0);
+      tr8x8(rr, cc);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) slots[fslot(8 * c + k)] = cc[k];
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < nv; c += blockDim.x) {
+      const int4 i0 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * c);
+      const int4 i1 = __ldg(reinterpret_cast<const int4*>(idx) + 2 * c + 1);
+      const int id[8] = {i0.x, i0.y, i0.z, i0.w, i1.x, i1.y, i1.z, i1.w};
+      uint4 g[8], o[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) g[q] = slots[fslot(id[q])];
+      tr8x8(g, o);  // g[q] = 8 tokens of feature id[q] -> o[r] = token r's 8 outputs
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < nr) __stcs(reinterpret_cast<uint4*>(y + (r0 + r) * cols) + c, o[r]);
+    }
+    __syncthreads();
+  }
+}
+
 // rows are processed in chunks of R rows; chunk i+1 streams into the other
 // smem buffer (cp.async) while chunk i is gathered and written
 __global__ void __launch_bounds__(256) permute_cols_bf16_kernel(int64_t rows, int64_t cols, int R,
@@ -458,6 +518,30 @@ static int gather2d_t(int64_t rows, int64_t cols, const int32_t* ridx, const int
   if (rows <= 0 || cols <= 0) return POETX_OK;
   unsigned grid = static_cast<unsigned>(rows < 148 * 16 ? rows : 148 * 16);
   if constexpr (sizeof(T) == 2) {
+    static const int t8 = [] {
+      const char* e = getenv("POETX_PERMUTE_T8");
+      return e && e[0] == '0' ? 0 : 1;
+    }();
+    const size_t tsm = static_cast<size_t>(cols) * 16;
+    if (t8 && ridx == nullptr && cidx != nullptr && cols % 8 == 0 && tsm <= 200 * 1024 && cols < INT32_MAX &&
+        ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(y) |
+          reinterpret_cast<uintptr_t>(cidx)) & 15) == 0) {
+      static bool attr = false;
+      if (!attr) {
+        cudaFuncSetAttribute(permute_cols_t8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+      }
+      const int64_t tiles = (rows + 7) / 8;
+      int per_sm = static_cast<int>((228 * 1024) / (tsm + 1024));
+      if (per_sm > 8) per_sm = 8;
+      if (per_sm < 1) per_sm = 1;
+      const int64_t cap = 148LL * per_sm;
+      permute_cols_t8_kernel<<<static_cast<unsigned>(tiles < cap ? tiles : cap), 256, tsm, st>>>(
+          rows, static_cast<int>(cols), cidx, reinterpret_cast<const __nv_bfloat16*>(x),
+          reinterpret_cast<__nv_bfloat16*>(y));
+      POETX_LAUNCHED("permute_cols_t8");
+      return POETX_OK;
+    }
     // chunk of R rows ~ 12 KB, two buffers per CTA
     int R = static_cast<int>((12 * 1024) / (cols * 2));
     if (R < 1) R = 1;

@@ -91,7 +91,8 @@ def hbm():
         x = torch.randn((T, cols), device="cuda").bfloat16()
         pm = P.sample_permutation(cols, P.Rng(1))
         ms = timeit(lambda: P.permute_features(x, pm, "inverse"))
-        print(f"permute T x {cols}: {ms * 1e3:.1f} us  {2 * x.numel() * 2 / ms / 1e6:.0f} GB/s")
+        print(f"permute T x {cols}: {ms * 1e3:.1f} us  {2 * x.numel() * 2 / ms / 1e6:.0f} GB/s "
+              f"(env POETX_PERMUTE_T8={os.environ.get('POETX_PERMUTE_T8', '1')})")
         for b in (256, 64):
             G = P.BlockDiagonalFactor((0.1 * torch.randn((cols // b, b, b), device="cuda")).bfloat16())
             for tr in (False, True):
