@@ -108,3 +108,16 @@ def test_error_codes_map_to_reference_exceptions():
     d.dtype, d.variant, d.neumann_k, d.m, d.n, d.b = 0, 0, 3, 10, 8, 4
     with pytest.raises(ConfigError, match="divisible by block_size"):
         N.call("poetx_layer_factors", d, N.LayerFactors(), None, 0, None)
+
+
+def test_quantized_descriptor_requires_mem_variant():
+    """POET-XQ is mem-variant only (layer.py:169-177): the C ABI rejects a
+    quantized descriptor on the fast variant with the reference's error."""
+    from paper_2603_05500_b200 import _native as N
+    from paper_2603_05500_b200.errors import ConfigError
+
+    d = N.LayerDesc()
+    d.dtype, d.variant, d.neumann_k, d.m, d.n, d.b = N.F32, N.FAST, 3, 8, 8, 4
+    d.pm_codes, d.pm_scales = 16, 16  # any non-NULL pointers: validation fails first
+    with pytest.raises(ConfigError, match="quantized base requires the mem variant"):
+        N.call("poetx_layer_factors", d, N.LayerFactors(), None, 0, None)
