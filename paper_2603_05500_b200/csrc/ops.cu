@@ -2,6 +2,7 @@
 // of the poetx_b200 C ABI (see include/poetx_b200.h for the contract and
 // the reference functions each one replaces).
 #include <cmath>
+#include <type_traits>
 #include <cstdlib>
 #include <mutex>
 #include <vector>
@@ -777,21 +778,51 @@ __global__ void adamw_kernel(int64_t n, T* __restrict__ p, T* __restrict__ g, T*
       factor = static_cast<T>(s.thr / norm);
     }
   }
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    T gi = g[i];
-    if (clip) {
-      gi = op_mul(gi, factor);
-      if (write_back) g[i] = gi;
+  auto update = [&](T& pi_, T& gi_, T& mi_, T& vi_) {
+    T gi = gi_;
+    if (clip) gi = op_mul(gi, factor);
+    const T mi = op_add(op_mul(mi_, b1), op_mul(omb1, gi));
+    const T vi = op_add(op_mul(vi_, b2), op_mul(op_mul(omb2, gi), gi));
+    const T mhat = op_div(mi, bc1), vhat = op_div(vi, bc2);
+    T pi = op_mul(pi_, decay);
+    pi_ = op_sub(pi, op_div(op_mul(lr, mhat), op_add(op_sqrt(vhat), eps)));
+    gi_ = gi;
+    mi_ = mi;
+    vi_ = vi;
+  };
+  // 16-byte vectors (same per-element operation order, so bitwise identical)
+  constexpr int V = 16 / sizeof(T);
+  using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  const bool vec_ok = ((reinterpret_cast<uintptr_t>(p) | reinterpret_cast<uintptr_t>(g) |
+                        reinterpret_cast<uintptr_t>(m) | reinterpret_cast<uintptr_t>(v)) & 15) == 0;
+  int64_t done = 0;
+  if (vec_ok) {
+    const int64_t nv = n / V;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nv;
+         i += (int64_t)gridDim.x * blockDim.x) {
+      Vec pv = reinterpret_cast<Vec*>(p)[i], gv = reinterpret_cast<Vec*>(g)[i];
+      Vec mv = reinterpret_cast<Vec*>(m)[i], vv = reinterpret_cast<Vec*>(v)[i];
+      T* pp = reinterpret_cast<T*>(&pv);
+      T* gg = reinterpret_cast<T*>(&gv);
+      T* mm = reinterpret_cast<T*>(&mv);
+      T* ww = reinterpret_cast<T*>(&vv);
+#pragma unroll
+      for (int q = 0; q < V; ++q) update(pp[q], gg[q], mm[q], ww[q]);
+      reinterpret_cast<Vec*>(p)[i] = pv;
+      reinterpret_cast<Vec*>(m)[i] = mv;
+      reinterpret_cast<Vec*>(v)[i] = vv;
+      if (clip && write_back) reinterpret_cast<Vec*>(g)[i] = gv;
     }
-    T mi = op_add(op_mul(m[i], b1), op_mul(omb1, gi));
-    T vi = op_add(op_mul(v[i], b2), op_mul(op_mul(omb2, gi), gi));
+    done = nv * V;
+  }
+  for (int64_t i = done + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    T pi = p[i], gi = g[i], mi = m[i], vi = v[i];
+    update(pi, gi, mi, vi);
+    p[i] = pi;
     m[i] = mi;
     v[i] = vi;
-    T mhat = op_div(mi, bc1), vhat = op_div(vi, bc2);
-    T pi = op_mul(p[i], decay);
-    pi = op_sub(pi, op_div(op_mul(lr, mhat), op_add(op_sqrt(vhat), eps)));
-    p[i] = pi;
+    if (clip && write_back) g[i] = gi;
   }
 }
 
@@ -997,7 +1028,7 @@ static int adamw_launch(int dtype, int ntensors, void* const* p, void* const* g,
                         cudaStream_t st) {
   for (int i = 0; i < ntensors; ++i) {
     if (numel[i] <= 0) continue;
-    unsigned grid = grid_for(numel[i], 256, 148 * 8);
+    unsigned grid = grid_for((numel[i] + 3) / 4, 256, 148 * 16);
     if (dtype == POETX_F32)
       adamw_kernel<float><<<grid, 256, 0, st>>>(numel[i], static_cast<float*>(p[i]),
                                                  static_cast<float*>(g[i]), static_cast<float*>(m[i]),
