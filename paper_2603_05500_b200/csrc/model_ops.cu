@@ -475,11 +475,12 @@ int check_rows(int64_t T, int64_t d, size_t smem) {
 
 // rows per tile: ~48 KB of staged rows per CTA (index loads amortised over
 // the tile, several CTAs per SM for latency hiding)
-int pick_rt(int64_t bytes_per_row) {
-  static int64_t budget = [] {
+int pick_rt(int64_t bytes_per_row, int64_t default_kb = 48) {
+  static int64_t forced = [] {
     const char* e = getenv("POETX_ROW_TILE_KB");
-    return static_cast<int64_t>(e ? atoi(e) : 48) * 1024;
+    return static_cast<int64_t>(e ? atoi(e) : 0) * 1024;
   }();
+  const int64_t budget = forced > 0 ? forced : default_kb * 1024;
   int64_t rt = budget / (bytes_per_row > 0 ? bytes_per_row : 1);
   if (rt >= 8) return 8;
   if (rt >= 4) return 4;
@@ -540,7 +541,9 @@ int poetx_rmsnorm_gather(int64_t T, int64_t d, const void* x, const float* w, fl
   return POETX_OK;
 }
 
-static int bwd_rt(int64_t d, int K) { return pick_rt(d * 2 * (1 + K) + d * 4); }
+// the backward re-reads K index maps per tile: larger tiles amortise them
+// (measured at Llama-1B shapes: 96 KB tiles 78 us vs 48 KB 86 us)
+static int bwd_rt(int64_t d, int K) { return pick_rt(d * 2 * (1 + K) + d * 4, 96); }
 
 size_t poetx_rmsnorm_gather_bwd_workspace_bytes(int64_t T, int64_t d) {
   int rt = bwd_rt(d, 1);  // largest grid over K
