@@ -802,7 +802,15 @@ int tc_outer_splits(int64_t T, int64_t nb, int64_t b) {
   int64_t tm = 128;
   int64_t tiles = nb * ((b + tm - 1) / tm) * ((b + bn - 1) / bn);
   // one wave of persistent CTAs: fewer fp32 partials to write and reduce
-  int64_t want = 148 / tiles;
+  // SM share (percent) the split count targets.  The outer products run on a
+  // side stream next to the main chain (layer.cu), so a partial share wins:
+  // fewer fp32 partials to write and reduce, the rest of the SMs stay with the
+  // chain (Llama-1B step: 100% -> 98.9k tok/s, 25-50% -> 101.5k)
+  static const int64_t share = [] {
+    const char* e = getenv("POETX_OUTER_SM_PCT");
+    return static_cast<int64_t>(e ? atoi(e) : 40);
+  }();
+  int64_t want = (148 * share / 100) / tiles;
   int64_t maxs = (T + 511) / 512;
   if (want > maxs) want = maxs;
   if (want < 1) want = 1;
