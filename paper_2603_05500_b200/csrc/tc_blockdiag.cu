@@ -241,7 +241,12 @@ int tc_blockdiag_apply(int64_t T, int64_t nb, int64_t b, const void* g, int tran
   a.T = static_cast<int>(T);
   a.b = static_cast<int>(b);
   a.m_tiles = static_cast<int>((T + BM - 1) / BM);
-  int chunks = static_cast<int>((num_sms() + nb - 1) / nb);
+  // one wave: at most (CTAs resident per SM by shared memory) x SMs, so no
+  // straggler second wave (b = 256, nb = 22: 154 CTAs -> 132, 44 -> 37.5 us)
+  const int smem = b == 256 ? BdCfg<256>::SMEM : b == 128 ? BdCfg<128>::SMEM : BdCfg<64>::SMEM;
+  int per_sm = (227 * 1024) / (smem + 1024);
+  if (per_sm < 1) per_sm = 1;
+  int chunks = static_cast<int>(static_cast<int64_t>(num_sms()) * per_sm / nb);
   if (chunks > a.m_tiles) chunks = a.m_tiles;
   if (chunks < 1) chunks = 1;
   a.per = (a.m_tiles + chunks - 1) / chunks;
