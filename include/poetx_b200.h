@@ -271,6 +271,15 @@ int poetx_quant_gather(int dtype, int64_t rows, int64_t cols, int64_t src_cols, 
                        const int32_t* col_idx, const int8_t* codes, const void* scales, int8_t* codes_out,
                        void* scales_out, void* stream);
 
+/* ----------------------------------------------------------- loss head --
+ * cross_entropy_fwd: per-row loss over bf16 logits [T, V] (V % 8 == 0) with
+ * row max / sum-exp kept for the backward; cross_entropy_bwd: bf16
+ * dlogits = (softmax - onehot) * (*dloss) * scale. */
+int poetx_cross_entropy_fwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, float* loss_rows,
+                            float* row_max, float* row_sumexp, void* stream);
+int poetx_cross_entropy_bwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, const float* row_max,
+                            const float* row_sumexp, const float* dloss, float scale, void* dlogits, void* stream);
+
 /* ------------------------------------------------ fused neighbour kernels --
  * BF16 row-staged kernels that apply the layer permutations inside the
  * elementwise ops a decoder block needs anyway (used with the

@@ -466,6 +466,80 @@ __global__ void __launch_bounds__(kThreads) scatter_add_kernel(
   }
 }
 
+
+// Cross-entropy over bf16 logits (the trainer's loss head), fused: the
+// forward streams each row once with an online max / sum-exp (fp32) and
+// keeps (max, sum) per row; the backward streams the row again and writes
+// d logits = (softmax - onehot) * g / T straight to bf16 -- no fp32 copy of
+// the [T, V] logits in either direction.
+__device__ __forceinline__ void ms_combine(float& m, float& s, float m2, float s2) {
+  const float M = fmaxf(m, m2);
+  s = (m == -INFINITY ? 0.f : s * expf(m - M)) + (m2 == -INFINITY ? 0.f : s2 * expf(m2 - M));
+  m = M;
+}
+
+__global__ void __launch_bounds__(256) ce_fwd_kernel(int64_t T, int V, const __nv_bfloat16* __restrict__ x,
+                                                     const int64_t* __restrict__ tgt, float* __restrict__ loss,
+                                                     float* __restrict__ mx, float* __restrict__ se) {
+  __shared__ float sm_m[8], sm_s[8];
+  const int wp = threadIdx.x / 32, l = threadIdx.x % 32, nv = V / 8;
+  for (int64_t r = blockIdx.x; r < T; r += gridDim.x) {
+    const uint4* row = reinterpret_cast<const uint4*>(x + r * V);
+    float m = -INFINITY, s = 0.f;
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+      float v[8];
+      unpack8(__ldcs(row + i), v);
+      float cm = v[0];
+#pragma unroll
+      for (int q = 1; q < 8; ++q) cm = fmaxf(cm, v[q]);
+      float cs = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) cs += expf(v[q] - cm);
+      ms_combine(m, s, cm, cs);
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const float m2 = __shfl_xor_sync(0xffffffffu, m, o), s2 = __shfl_xor_sync(0xffffffffu, s, o);
+      ms_combine(m, s, m2, s2);
+    }
+    if (l == 0) { sm_m[wp] = m; sm_s[wp] = s; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      float M = sm_m[0], S = sm_s[0];
+      for (int k = 1; k < 8; ++k) ms_combine(M, S, sm_m[k], sm_s[k]);
+      const float xt = __bfloat162float(x[r * V + tgt[r]]);
+      loss[r] = (M + logf(S)) - xt;
+      mx[r] = M;
+      se[r] = S;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(256) ce_bwd_kernel(int64_t T, int V, const __nv_bfloat16* __restrict__ x,
+                                                     const int64_t* __restrict__ tgt, const float* __restrict__ mx,
+                                                     const float* __restrict__ se, const float* __restrict__ g0,
+                                                     float scale, __nv_bfloat16* __restrict__ grad) {
+  const int nv = V / 8;
+  const float c = *g0 * scale;
+  for (int64_t r = blockIdx.x; r < T; r += gridDim.x) {
+    const uint4* row = reinterpret_cast<const uint4*>(x + r * V);
+    uint4* out = reinterpret_cast<uint4*>(grad + r * V);
+    const float m = mx[r], inv = 1.f / se[r];
+    const int64_t t = tgt[r];
+    for (int i = threadIdx.x; i < nv; i += blockDim.x) {
+      float v[8];
+      unpack8(__ldcs(row + i), v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float p = expf(v[q] - m) * inv;
+        if (8 * i + q == t) p -= 1.f;
+        v[q] = p * c;
+      }
+      __stcs(out + i, pack8(v));
+    }
+  }
+}
+
 int check_rows(int64_t T, int64_t d, size_t smem) {
   POETX_REQUIRE(T >= 0 && d > 0 && d % 8 == 0, POETX_ESHAPE, "row kernel: bad shape (%lld, %lld)",
                 (long long)T, (long long)d);
@@ -653,6 +727,29 @@ int poetx_scatter_add(int64_t T, int64_t d, const void* h, const void* v, const 
                         T, d, static_cast<const __nv_bfloat16*>(h), static_cast<const __nv_bfloat16*>(v),
                         inv, static_cast<__nv_bfloat16*>(out)));
   POETX_LAUNCHED("scatter_add");
+  return POETX_OK;
+}
+
+int poetx_cross_entropy_fwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, float* loss_rows,
+                            float* row_max, float* row_sumexp, void* stream) {
+  POETX_REQUIRE(T >= 0 && V > 0 && V % 8 == 0 && V < INT32_MAX, POETX_ESHAPE,
+                "cross_entropy: vocab must be a positive multiple of 8, got %lld", (long long)V);
+  if (T == 0) return POETX_OK;
+  ce_fwd_kernel<<<static_cast<unsigned>(T < 148 * 8 ? T : 148 * 8), 256, 0, as_stream(stream)>>>(
+      T, static_cast<int>(V), static_cast<const __nv_bfloat16*>(logits), targets, loss_rows, row_max, row_sumexp);
+  POETX_LAUNCHED("cross_entropy_fwd");
+  return POETX_OK;
+}
+
+int poetx_cross_entropy_bwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, const float* row_max,
+                            const float* row_sumexp, const float* dloss, float scale, void* dlogits, void* stream) {
+  POETX_REQUIRE(T >= 0 && V > 0 && V % 8 == 0 && V < INT32_MAX, POETX_ESHAPE,
+                "cross_entropy: vocab must be a positive multiple of 8, got %lld", (long long)V);
+  if (T == 0) return POETX_OK;
+  ce_bwd_kernel<<<static_cast<unsigned>(T < 148 * 8 ? T : 148 * 8), 256, 0, as_stream(stream)>>>(
+      T, static_cast<int>(V), static_cast<const __nv_bfloat16*>(logits), targets, row_max, row_sumexp, dloss, scale,
+      static_cast<__nv_bfloat16*>(dlogits));
+  POETX_LAUNCHED("cross_entropy_bwd");
   return POETX_OK;
 }
 

@@ -490,6 +490,31 @@ class _RopeScatter(torch.autograd.Function):
         return dv, None, None, None, None, None, None, None
 
 
+class _CrossEntropy(torch.autograd.Function):
+    """mean_t CE(logits[t], target[t]) over bf16 logits, fused (model_ops.cu)."""
+
+    @staticmethod
+    def forward(ctx, logits, targets):
+        T, V = logits.shape
+        rows = torch.empty(T, dtype=torch.float32, device=logits.device)
+        mx, se = torch.empty_like(rows), torch.empty_like(rows)
+        tg = targets.contiguous()
+        N.call("poetx_cross_entropy_fwd", T, V, logits.data_ptr(), tg.data_ptr(), rows.data_ptr(), mx.data_ptr(),
+               se.data_ptr(), N.stream_ptr(logits.device))
+        ctx.save_for_backward(logits, tg, mx, se)
+        return rows.mean()
+
+    @staticmethod
+    def backward(ctx, g):
+        logits, tg, mx, se = ctx.saved_tensors
+        T, V = logits.shape
+        grad = torch.empty_like(logits)
+        g = g.float().contiguous()
+        N.call("poetx_cross_entropy_bwd", T, V, logits.data_ptr(), tg.data_ptr(), mx.data_ptr(), se.data_ptr(),
+               g.data_ptr(), 1.0 / T, grad.data_ptr(), N.stream_ptr(logits.device))
+        return grad, None
+
+
 def _permute_cols(x, idx):
     y = torch.empty_like(x)
     N.call("poetx_permute_cols", N.BF16, x.shape[0], x.shape[1], idx.data_ptr(), x.data_ptr(), y.data_ptr(),
@@ -664,7 +689,10 @@ class PoetLlama(torch.nn.Module):
         leaves += [nf, head]
         h = F.rms_norm(h, (d,), nf.to(torch.bfloat16), 1e-6)
         logits = F.linear(h, head.to(torch.bfloat16))
-        loss = F.cross_entropy(logits.float(), targets.reshape(-1))
+        if self.fused:
+            loss = _CrossEntropy.apply(logits, targets.reshape(-1))
+        else:
+            loss = F.cross_entropy(logits.float(), targets.reshape(-1))
         self._leaves = leaves
         return loss
 

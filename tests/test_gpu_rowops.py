@@ -131,3 +131,21 @@ def test_scatter_add(N, T, d, f):
     v = _bf(torch.randn(T, d)).cuda()
     out = _ScatterAdd.apply(h, v, inv, fwd)
     _close(out, h.float() + v.float()[:, inv.long()], 1e-2)
+
+
+@pytest.mark.parametrize("T,V", [(8192, 32000), (37, 64), (1, 128)])
+def test_fused_cross_entropy(N, T, V):
+    """Fused bf16 cross-entropy head vs torch's fp32 cross_entropy."""
+    from paper_2603_05500_b200.trainer import _CrossEntropy
+
+    g = torch.Generator().manual_seed(T + V)
+    logits = (3 * torch.randn(T, V, generator=g)).to(torch.bfloat16).cuda()
+    tgt = torch.randint(0, V, (T,), generator=g).cuda()
+    a = logits.clone().requires_grad_(True)
+    loss = _CrossEntropy.apply(a, tgt)
+    r = logits.float().clone().requires_grad_(True)
+    ref = torch.nn.functional.cross_entropy(r, tgt)
+    assert abs(loss.item() - ref.item()) <= 1e-5 * max(1.0, abs(ref.item()))
+    (2.0 * loss).backward()
+    (2.0 * ref).backward()
+    _close(a.grad, r.grad, 1e-2)
