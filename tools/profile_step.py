@@ -20,6 +20,7 @@ ap.add_argument("--variant", default="fast")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--rows", type=int, default=40)
 ap.add_argument("--graph", action="store_true")
+ap.add_argument("--serial", action="store_true", help="no side streams (per-kernel times undisturbed)")
 args = ap.parse_args()
 
 FAMILIES = [
@@ -34,7 +35,8 @@ FAMILIES = [
     ("to_bf16", "CNP glue"),
     ("adamw", "AdamW+norm"), ("sqdev", "AdamW+norm"),
     ("sdpa", "attention (cuDNN)"), ("cudnn", "attention (cuDNN)"),
-    ("nvjet", "lm_head GEMMs (cuBLAS)"), ("SoftMax", "cross-entropy"),
+    ("nvjet", "lm_head GEMMs (cuBLAS)"), ("SoftMax", "cross-entropy"), ("ce_fwd", "cross-entropy"),
+    ("ce_bwd", "cross-entropy"), ("quantize", "POET-XQ"), ("dequant", "POET-XQ"),
 ]
 
 
@@ -47,6 +49,8 @@ def family(name):
 
 cfg = llama_config(args.model, variant=args.variant)
 tr = Trainer(cfg, args.mb, merge_gap=0)
+if args.serial:
+    tr.model.concurrent = False
 tok = torch.randint(0, cfg.vocab, (args.mb, cfg.seq + 1), device="cuda")
 for _ in range(3):
     tr.step(tok[:, :-1], tok[:, 1:])
