@@ -284,9 +284,11 @@ class PoetLinear(torch.nn.Module):
         z = _PoetFn.apply(x.reshape(-1, self.m).contiguous(), self)
         return z.view(*shp[:-1], self.n)
 
-    def merge_and_reinit(self, rng: Rng):
+    def merge_and_reinit(self, rng: Rng, audit_out: torch.Tensor | None = None):
         """layer.py:279-314 on the device: fold G_R PM G_P (fp32 factors from the
-        CUDA-core CNP for merge accuracy), resample perms, zero packed in place."""
+        CUDA-core CNP for merge accuracy), resample perms, zero packed in place.
+        ``audit_out`` (device float64 [2]) receives ||G^T G - I||_F of both
+        sides (layer.py:287-295), without a host sync."""
         b = self.b
         g_r = torch.empty((self.m // b, b, b), dtype=torch.float32, device=self.device)
         g_p = torch.empty((self.n // b, b, b), dtype=torch.float32, device=self.device)
@@ -295,6 +297,12 @@ class PoetLinear(torch.nn.Module):
         ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(N.F32, max(self.m, self.n) // b, b, self.k),
                               self.device)
         N.call("poetx_layer_factors", self.desc, f, ws, wsb, N.stream_ptr(self.device))
+        if audit_out is not None:
+            for k, g in enumerate((g_r, g_p)):
+                nb = g.shape[0]
+                ws, wsb = N.workspace(nb * b * b * 4 + 512 * 8 + 8192, self.device)
+                N.call("poetx_orthogonality_error", N.F32, nb, b, g.data_ptr(), audit_out[k:].data_ptr(), ws, wsb,
+                       N.stream_ptr(self.device))
         new_in = sample_permutation(self.m, rng)
         new_out = sample_permutation(self.n, rng)
         ws, wsb = N.workspace(N.lib().poetx_merge_workspace_bytes(self.desc), self.device)
@@ -912,9 +920,18 @@ class Trainer:
         return tokens, cfg
 
     def merge(self):
+        """Merge-then-reinitialize every layer (runner.py:302-326): keyed merge
+        RNGs, fresh AdamW moments for the POET group, and a merge audit per
+        layer (orthogonality errors of the folded factors, read back once)."""
         layers = self.model.poet_layers()
-        for lay, rng in zip(layers, merge_rngs(self.seed, self.step_idx, len(layers))):
-            lay.merge_and_reinit(rng)
+        audit = torch.zeros((len(layers), 2), dtype=torch.float64, device=self.device)
+        for i, (lay, rng) in enumerate(zip(layers, merge_rngs(self.seed, self.step_idx, len(layers)))):
+            lay.merge_and_reinit(rng, audit_out=audit[i])
         self.model.refresh_maps()
         self.model.poet.reset_moments()
         self.since_merge = 0
+        errs = audit.cpu().numpy()
+        self.merges = getattr(self, "merges", [])
+        self.merges += [{"step": self.step_idx, "layer": lay.name, "merge_count": lay.merge_count,
+                         "orth_err_r": float(e[0]), "orth_err_p": float(e[1])} for lay, e in zip(layers, errs)]
+        return self.merges[-len(layers):]

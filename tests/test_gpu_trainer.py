@@ -18,6 +18,11 @@ def test_llama60m_step_reduces_loss_and_merges():
     assert losses[-1] < losses[0]
     assert tr.model.poet_layers()[0].merge_count == 2
     assert int(tr.last_bad.item()) == 0
+    # merge audit (runner.py:302-326): one record per layer per merge, orthogonality
+    # error of the folded CNP factors within the reference's small-Q bound
+    assert len(tr.merges) == 2 * len(tr.model.poet_layers())
+    assert all(0.0 <= m["orth_err_r"] <= 1e-2 and 0.0 <= m["orth_err_p"] <= 1e-2 for m in tr.merges)
+    assert any(m["orth_err_r"] > 0 for m in tr.merges)
 
 
 def test_fused_block_matches_unfused_reference_path():
