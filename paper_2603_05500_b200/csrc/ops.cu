@@ -609,6 +609,21 @@ int apply_features(int dt, int64_t T, int64_t nb, int64_t b, const void* g, int 
 int apply_weight_rows(int dt, int64_t nb, int64_t b, int64_t cols, const void* g, int transpose,
                       const void* w, void* y, cudaStream_t st) {
   if (nb <= 0 || cols <= 0) return POETX_OK;
+  if (dt == POETX_BF16 && tc_enabled() && !transpose && b % 64 == 0 && b <= 256 && cols % 256 == 0) {
+    // y[s-rows, :] = g[s] w[s-rows, :] as a grouped tcgen05 product:
+    // A = g[s] (K-major), B = the b rows of w (MN-major), one group per block
+    TcOperand A{g, nb * b, b, b, false};
+    TcOperand B{w, nb * b, cols, cols, true};
+    TcProblem p{};
+    p.M = b; p.N = cols; p.K = b; p.groups = static_cast<int>(nb); p.splits = 1;
+    p.bn = static_cast<int>(b < 256 ? b : 256);
+    p.a_g1 = static_cast<int>(b);
+    p.b_g1 = static_cast<int>(b);
+    p.C = y; p.ldc = cols; p.c_goff = b * cols;
+    p.alpha = 1.0f; p.name = "tc_wfold"; p.tma_epi = 1;
+    int rc = tc_grouped(A, B, p, st);
+    if (rc != POETX_ENOTSUPPORTED) return rc;
+  }
   GemmDesc d{};
   d.M = b; d.N = cols; d.K = b; d.batch = nb;
   d.A = g; d.sAb = b * b; d.sAm = transpose ? 1 : b; d.sAk = transpose ? b : 1;
