@@ -10,6 +10,7 @@
 #include "common.cuh"
 #include "simt_gemm.cuh"
 #include "tc_gemm.cuh"
+#include "tile8.cuh"
 
 namespace poetx {
 
@@ -399,21 +400,6 @@ __device__ __forceinline__ void cp_async_wait() {
 // 16-byte LDS instead of eight conflicted 2-byte LDS: the random accesses
 // that bound the row-major kernel drop ~3x in smem wavefronts.  8x8 bf16
 // transposes are 32 PRMTs in registers on the way in and out.
-__device__ __forceinline__ void tr8x8(const uint4 (&r)[8], uint4 (&c)[8]) {
-  // c[col] word i = {row 2i, row 2i+1} of that column
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t a[4] = {r[2 * i].x, r[2 * i].y, r[2 * i].z, r[2 * i].w};
-    const uint32_t b[4] = {r[2 * i + 1].x, r[2 * i + 1].y, r[2 * i + 1].z, r[2 * i + 1].w};
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const uint32_t lo = __byte_perm(a[w], b[w], 0x5410), hi = __byte_perm(a[w], b[w], 0x7632);
-      reinterpret_cast<uint32_t*>(&c[2 * w])[i] = lo;
-      reinterpret_cast<uint32_t*>(&c[2 * w + 1])[i] = hi;
-    }
-  }
-}
-__device__ __forceinline__ int fslot(int f) { return (f & ~7) | ((f ^ (f >> 3)) & 7); }
 
 __global__ void __launch_bounds__(256) permute_cols_t8_kernel(int64_t rows, int cols,
                                                              const int32_t* __restrict__ idx,
