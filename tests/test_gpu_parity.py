@@ -317,12 +317,21 @@ def test_merge_sv_drift(P):
 # --------------------------------------------------------------- bf16 path ----
 
 
-@pytest.mark.parametrize("m,n,b,T", [(512, 512, 64, 1024), (256, 768, 128, 512), (1024, 512, 256, 384)])
-def test_bf16_layer_vs_oracle(P, m, n, b, T):
-    r = np.random.default_rng(m + n)
+@pytest.mark.parametrize("m,n,b,T,variant,quant", [
+    (512, 512, 64, 1024, "fast", False), (256, 768, 128, 512, "fast", False), (1024, 512, 256, 384, "fast", False),
+    (512, 768, 256, 77, "fast", False), (768, 512, 256, 300, "mem", False), (512, 1024, 256, 130, "mem", True),
+    (256, 256, 64, 33, "mem", True)])
+def test_bf16_layer_vs_oracle(P, m, n, b, T, variant, quant):
+    """bf16 layer (tensor-core path: weight-folded block factors, CTA-pair
+    GEMMs; ragged T; mem variant; int8 base) against the float64 oracle."""
+    r = np.random.default_rng(m + n + T)
     base = (r.standard_normal((m, n)) / np.sqrt(m))
-    layer = P.PoetLinearLayer(torch.from_numpy(base).to(torch.bfloat16), b, P.Rng(5))
-    base_q = layer.base.double().cpu().numpy()  # bf16-rounded weight the GPU really holds
+    layer = P.PoetLinearLayer(torch.from_numpy(base).to(torch.bfloat16), b, P.Rng(5), variant=variant)
+    if quant:
+        layer.quantize_base()
+        base_q = layer.base.dequantize().double().cpu().numpy()  # the int8 weight the GPU holds
+    else:
+        base_q = layer.base.double().cpu().numpy()  # bf16-rounded weight the GPU really holds
     q_r = 0.01 * r.standard_normal(tuple(layer.q_r.packed.shape))
     q_p = 0.01 * r.standard_normal(tuple(layer.q_p.packed.shape))
     layer.q_r.packed.copy_(dev(q_r))
