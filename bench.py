@@ -261,13 +261,21 @@ def run_ours(args, rank, world, local_rank):
     if args.graph:
         torch.cuda.empty_cache()  # the graph's private pool replaces the eager cache
         tb = dev_batches[0]
+        def agree(ok):  # every rank replays a graph, or none does (matched collectives)
+            if pg is None:
+                return ok
+            flag = torch.tensor([1 if ok else 0], device=dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            return bool(flag.item())
+
         try:
-            trainer.capture(tb[:, :-1], tb[:, 1:])
+            trainer.capture(tb[:, :-1], tb[:, 1:], agree=agree)
         except Exception as e:  # keep measuring (eagerly) rather than lose the run
             graph_error = f"{type(e).__name__}: {e}"[:200]
             trainer.graph = None
-            args.graph = False
             torch.cuda.synchronize()
+            torch.cuda.empty_cache()  # release the abandoned graph pool
+        args.graph = trainer.graph is not None
     torch.cuda.reset_peak_memory_stats(dev)
     clocks = ClockSampler(local_rank)
     clocks.start()

@@ -880,10 +880,15 @@ class Trainer:
         self._advance()
         return loss
 
-    def capture(self, tokens: torch.Tensor, targets: torch.Tensor, warmup: int = 2):
+    def capture(self, tokens: torch.Tensor, targets: torch.Tensor, warmup: int = 2, agree=None):
         """Capture one full step (forward, backward, CNP, all-reduce, update) as a
         CUDA graph; later ``step`` calls replay it.  Merges run eagerly between
-        replays and update every buffer the graph reads in place."""
+        replays and update every buffer the graph reads in place.
+
+        ``agree(ok) -> bool`` (data parallel): every rank must replay a graph or
+        none may (the graph holds collectives), so the ranks vote before the
+        first replay.  Raises RuntimeError when the step is not captured; the
+        trainer then keeps stepping eagerly with consistent state."""
         self.static_tokens = tokens.clone()
         self.static_targets = targets.clone()
         side = torch.cuda.Stream(self.device)
@@ -895,8 +900,21 @@ class Trainer:
         self._prepare_scalars()
         g = torch.cuda.CUDAGraph()
         before = N.launch_count()
-        with torch.cuda.graph(g):
-            self.static_loss = self._compute(self.static_tokens, self.static_targets)
+        err = None
+        try:
+            with torch.cuda.graph(g):
+                self.static_loss = self._compute(self.static_tokens, self.static_targets)
+        except Exception as e:  # noqa: BLE001 -- reported to the caller below
+            err = e
+        ok = err is None
+        if agree is not None:
+            ok = bool(agree(ok))
+        if not ok:
+            # the captured step never ran: undo its host-side schedule state
+            self.model.poet.t -= 1
+            self.model.dense.t -= 1
+            torch.cuda.synchronize(self.device)
+            raise RuntimeError(f"step not captured: {err or 'a peer rank could not capture the step'}")
         self.graph_launches = N.launch_count() - before  # library kernels per replayed step
         g.replay()  # capture only records: run the captured step once for real
         self._advance()
