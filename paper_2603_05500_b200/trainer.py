@@ -409,7 +409,15 @@ class _CnpBackwardHook(torch.autograd.Function):
         cs = model.cnp_stream
         cs.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cs):
-            model.stack.backward_factors_range(*model.block_ranges[ctx.i])
+            off, nb = model.block_ranges[ctx.i]
+            model.stack.backward_factors_range(off, nb)
+            if model.dp_group is not None:
+                # data parallel: this block's packed gradients are final -- start
+                # their all-reduce now so it overlaps the blocks below (the step
+                # waits on every handle before the optimizer)
+                pairs = model.stack.pairs
+                model.dp_works.append(_all_reduce_async(model.poet.grad[off * pairs:(off + nb) * pairs],
+                                                        model.dp_group))
         return dh, None, None
 
 
@@ -628,6 +636,7 @@ class PoetLlama(torch.nn.Module):
             hi = self.stack.block_off[f"{i}.down.p"] + d // b
             self.block_ranges.append((lo, hi - lo))
         self.cnp_pipelined = False  # set per step by the trainer
+        self.dp_group, self.dp_works = None, []
         self.refresh_maps()
 
     def refresh_maps(self):
@@ -784,6 +793,23 @@ def average_gradients(buffers, group) -> None:
             buf.div_(dist.get_world_size(group))
 
 
+def _all_reduce_async(buf, group):
+    """Start an averaging all-reduce of ``buf``; returns (work, buf, scale)
+    for ``_finish_all_reduce`` (NCCL averages itself, gloo sums)."""
+    import torch.distributed as dist
+
+    if dist.get_backend(group) == "nccl":
+        return dist.all_reduce(buf, op=dist.ReduceOp.AVG, group=group, async_op=True), buf, None
+    return dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=group, async_op=True), buf, dist.get_world_size(group)
+
+
+def _finish_all_reduce(works) -> None:
+    for work, buf, scale in works:
+        work.wait()  # the current stream waits for the collective
+        if scale is not None:
+            buf.div_(scale)
+
+
 def merge_rngs(seed: int, step: int, n_layers: int):
     """Per-layer merge streams Rng.keyed(seed, "merge", step, idx)
     (runner.py:304-307): identical on every rank, so merges need no
@@ -824,17 +850,22 @@ class Trainer:
         model.dense.grad.zero_()
         model.cnp_pipelined = model.concurrent and model.fused
         if model.cnp_pipelined:
-            # per-decoder-block CNP on the CNP stream, overlapped with the layers
+            # per-decoder-block CNP on the CNP stream, overlapped with the layers;
+            # with DP each block's packed-gradient all-reduce starts right after
+            model.dp_group, model.dp_works = self.pg, []
             loss = model(tokens, targets)
             model.backward_dense_grads(loss)
             torch.cuda.current_stream().wait_stream(model.cnp_stream)
+            if self.pg is not None:
+                _finish_all_reduce(model.dp_works + [_all_reduce_async(model.dense.grad, self.pg)])
+                model.dp_works = []
         else:
             model.stack.forward_factors()      # CNP of every block, one batched call
             loss = model(tokens, targets)
             model.backward_dense_grads(loss)   # layers leave dG in model.stack.dg
             model.stack.backward_factors()     # batched CNP backward -> packed grads
-        if self.pg is not None:
-            average_gradients([model.poet.grad, model.dense.grad], self.pg)
+            if self.pg is not None:
+                average_gradients([model.poet.grad, model.dense.grad], self.pg)
         self.last_sq, self.last_bad = fused_clip_adamw_dyn(
             [([model.poet.param], [model.poet.grad], [model.poet.m], [model.poet.v], self.dyn[0]),
              ([model.dense.param], [model.dense.grad], [model.dense.m], [model.dense.v], self.dyn[1])],
