@@ -210,9 +210,18 @@ typedef struct {
   void* g_p_lowp;
   void* q2_r;            /* Q^2 caches (k == 3), may be NULL */
   void* q2_p;
+  /* optional precomputed weight folds of a BF16 layer (else built per call):
+   * w_in_fold = bd(G_R) PM, w_out_fold = PM bd(G_P), both [m, n] bf16 */
+  const void* w_in_fold;
+  const void* w_out_fold;
 } poetx_layer_factors_t;
 
 size_t poetx_layer_workspace_bytes(const poetx_layer_desc* d, int64_t T);
+/* BF16 weight folds: which = 0 -> out = bd(G_R) PM, 1 -> out =
+ * PM bd(G_P), from the factors' bf16 G (and the dequantized int8 base);
+ * out is [m, n] bf16.  ws >= poetx_layer_workspace_bytes(d, 0). */
+int poetx_layer_weight_fold(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int which, void* out,
+                            void* ws, size_t ws_bytes, void* stream);
 int poetx_layer_factors(const poetx_layer_desc* d, poetx_layer_factors_t* f, void* ws,
                         size_t ws_bytes, void* stream);
 /* z[T,n] = layer(x[T,m]); saved_t[T,n] written when non-NULL (fast). */

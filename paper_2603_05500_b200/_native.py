@@ -68,6 +68,8 @@ class LayerFactors(C.Structure):
         ("g_p_lowp", VP),
         ("q2_r", VP),
         ("q2_p", VP),
+        ("w_in_fold", VP),
+        ("w_out_fold", VP),
     ]
 
 
@@ -123,6 +125,7 @@ _SIGS = {
     "poetx_layer_backward": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I64, VP, VP, VP,
                                    VP, VP, VP, I32, VP, SZ, VP]),
     "poetx_merge_workspace_bytes": (SZ, [C.POINTER(LayerDesc)]),
+    "poetx_layer_weight_fold": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I32, VP, VP, SZ, VP]),
     "poetx_layer_merge_quant": (I32, [C.POINTER(LayerDesc), VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP]),
     "poetx_quantize_rows": (I32, [I32, I64, I64, VP, VP, VP, VP]),
     "poetx_dequantize_rows": (I32, [I32, I64, I64, I64, VP, VP, VP, VP, VP, VP]),

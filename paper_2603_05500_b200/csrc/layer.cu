@@ -241,9 +241,13 @@ int poetx_layer_forward_ex(const poetx_layer_desc* d, const poetx_layer_factors_
   }
   if (reassoc(d)) {
     // t = u (bd(G_R) PM)  (mm1 folded into the weight, layer.py:221-222)
-    void* w2 = wsp.take_bytes(d->m * d->n * e);
-    POETX_REQUIRE(w2, POETX_ESHAPE, "layer_forward: workspace too small");
-    POETX_TRY(apply_weight_rows(dt, d->m / d->b, d->b, d->n, act_g(d, f->g_r, f->g_r_lowp), 0, pm, w2, st));
+    const void* w2 = f->w_in_fold;
+    if (!w2) {
+      void* w = wsp.take_bytes(d->m * d->n * e);
+      POETX_REQUIRE(w, POETX_ESHAPE, "layer_forward: workspace too small");
+      POETX_TRY(apply_weight_rows(dt, d->m / d->b, d->b, d->n, act_g(d, f->g_r, f->g_r_lowp), 0, pm, w, st));
+      w2 = w;
+    }
     POETX_TRY(poetx_matmul(dt, T, d->n, d->m, u, d->m, 0, w2, d->n, 0, t, d->n, 0, stream));
   } else {
     // a = u blockdiag(G_R)  (mm1, layer.py:221)
@@ -299,9 +303,10 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
     dv = b1;
   }
   const bool ra = reassoc(d);
-  void* w1 = ra ? wsp.take_bytes(d->m * d->n * e) : nullptr;  // PM bd(G_P)
-  void* w2 = ra && !saved_t ? wsp.take_bytes(d->m * d->n * e) : nullptr;  // bd(G_R) PM
-  POETX_REQUIRE(!ra || (w1 && (saved_t || w2)), POETX_ESHAPE, "layer_backward: workspace too small");
+  const bool own_w1 = ra && !f->w_out_fold, own_w2 = ra && !saved_t && !f->w_in_fold;
+  void* w1 = own_w1 ? wsp.take_bytes(d->m * d->n * e) : nullptr;  // PM bd(G_P)
+  void* w2 = own_w2 ? wsp.take_bytes(d->m * d->n * e) : nullptr;  // bd(G_R) PM
+  POETX_REQUIRE((!own_w1 || w1) && (!own_w2 || w2), POETX_ESHAPE, "layer_backward: workspace too small");
   Workspace tail(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
   const void* t = saved_t;
   if (!t) {
@@ -312,8 +317,9 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
       u0 = b2;
     }
     if (ra) {
-      POETX_TRY(apply_weight_rows(dt, nbr, b, d->n, gr, 0, pm, w2, st));
-      POETX_TRY(poetx_matmul(dt, T, d->n, d->m, u0, d->m, 0, w2, d->n, 0, b4, d->n, 0, stream));
+      if (own_w2) POETX_TRY(apply_weight_rows(dt, nbr, b, d->n, gr, 0, pm, w2, st));
+      const void* wi = own_w2 ? w2 : f->w_in_fold;
+      POETX_TRY(poetx_matmul(dt, T, d->n, d->m, u0, d->m, 0, wi, d->n, 0, b4, d->n, 0, stream));
     } else {
       POETX_TRY(apply_features(dt, T, nbr, b, gr, 0, u0, b3, st));
       POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b3, d->m, 0, pm, d->n, 0, b4, d->n, 0, stream));
@@ -332,8 +338,9 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   POETX_TRY(segmented_outer(dt, T, nbp, b, t, dv, dgp, dg_acc, tail, so));
   if (ra) {
     // da = dv (PM bd(G_P))^T  (layer.py:248-249 with dt folded into the weight)
-    POETX_TRY(apply_features(dt, d->m, nbp, b, gp, 0, pm, w1, st));
-    POETX_TRY(poetx_matmul(dt, T, d->m, d->n, dv, d->n, 0, w1, d->n, 1, b3, d->m, 0, stream));
+    if (own_w1) POETX_TRY(apply_features(dt, d->m, nbp, b, gp, 0, pm, w1, st));
+    const void* wo = own_w1 ? w1 : f->w_out_fold;
+    POETX_TRY(poetx_matmul(dt, T, d->m, d->n, dv, d->n, 0, wo, d->n, 1, b3, d->m, 0, stream));
   } else {
     // dt = dv blockdiag(G_P)^T  (layer.py:248)
     POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, dv, b2, st));
@@ -398,6 +405,21 @@ int poetx_layer_backward_dg(const poetx_layer_desc* d, const poetx_layer_factors
                 "layer_backward_dg: bad arguments");
   return layer_backward_impl(d, f, T, x, dz, saved_t, dx, nullptr, nullptr, dg_r, dg_p,
                              accumulate, flags, ws, ws_bytes, stream);
+}
+
+int poetx_layer_weight_fold(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int which, void* out,
+                            void* ws, size_t ws_bytes, void* stream) {
+  POETX_TRY(check_desc(d));
+  POETX_REQUIRE(d->dtype == POETX_BF16 && f && out && (which == 0 || which == 1), POETX_ESHAPE,
+                "layer_weight_fold: BF16 layer, factors and output required");
+  POETX_REQUIRE(f->g_r_lowp && f->g_p_lowp, POETX_ESHAPE, "layer_weight_fold: bf16 factors required");
+  cudaStream_t st = as_stream(stream);
+  Workspace wsp(ws, ws_bytes);
+  int qrc;
+  const void* pm = layer_pm(d, wsp, st, qrc);
+  POETX_TRY(qrc);
+  if (which == 0) return apply_weight_rows(d->dtype, d->m / d->b, d->b, d->n, f->g_r_lowp, 0, pm, out, st);
+  return apply_features(d->dtype, d->m, d->n / d->b, d->b, f->g_p_lowp, 0, pm, out, st);
 }
 
 size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d) {

@@ -21,6 +21,7 @@ all-reduce are one launch each over contiguous HBM.  Dense trainables
 from __future__ import annotations
 
 import math
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -223,8 +224,10 @@ class PoetLinear(torch.nn.Module):
             self.scales = torch.empty(m, dtype=torch.float32, device=self.device)
         self._install(w)
         del w
-        self.fstruct = N.LayerFactors(self.packed_r.data_ptr(), self.packed_p.data_ptr(), None, None,
-                                      self.g_r16.data_ptr(), self.g_p16.data_ptr(), None, None)
+        self.fstruct_plain = N.LayerFactors(self.packed_r.data_ptr(), self.packed_p.data_ptr(), None, None,
+                                            self.g_r16.data_ptr(), self.g_p16.data_ptr(), None, None)
+        self.fstruct = self.fstruct_bwd = self.fstruct_plain
+        self.fstruct_folded = None  # (forward, backward) structs when weight folds are pipelined
         self.merge_count = 0
 
     def _install(self, w: torch.Tensor):
@@ -278,6 +281,13 @@ class PoetLinear(torch.nn.Module):
 
     def ws_bytes(self, T: int) -> int:
         return int(N.lib().poetx_layer_workspace_bytes(self.desc, T))
+
+    def weight_fold(self, which: int, out: torch.Tensor):
+        """out = bd(G_R) PM (which 0) or PM bd(G_P) (which 1), bf16 [m, n],
+        on the current stream (poetx_layer_weight_fold)."""
+        ws, wsb = N.workspace(self.ws_bytes(0), self.device)
+        N.call("poetx_layer_weight_fold", self.desc, self.fstruct_plain, which, out.data_ptr(), ws, wsb,
+               N.stream_ptr(self.device))
 
     def forward(self, x):
         shp = x.shape
@@ -367,7 +377,7 @@ class _PoetRawFn(torch.autograd.Function):
         T = u.shape[0]
         du = torch.empty_like(u)
         ws, wsb = N.workspace(mod.ws_bytes(T), u.device)
-        N.call("poetx_layer_backward_dg", mod.desc, mod.fstruct, T, u.data_ptr(), dv.data_ptr(), N.ptr(t),
+        N.call("poetx_layer_backward_dg", mod.desc, mod.fstruct_bwd, T, u.data_ptr(), dv.data_ptr(), N.ptr(t),
                du.data_ptr(), mod.dg_r.data_ptr(), mod.dg_p.data_ptr(), 0,
                N.IN_GATHERED | N.DZ_GATHERED | N.DX_UNSCATTERED, ws, wsb, N.stream_ptr(u.device))
         return du, None, None
@@ -418,6 +428,28 @@ class _CnpBackwardHook(torch.autograd.Function):
                 pairs = model.stack.pairs
                 model.dp_works.append(_all_reduce_async(model.poet.grad[off * pairs:(off + nb) * pairs],
                                                         model.dp_group))
+        return dh, None, None
+
+
+class _FoldPrefetchHook(torch.autograd.Function):
+    """Identity on a decoder block's OUTPUT.  Its backward fires when the
+    block's backward is about to start: the block's backward weight folds
+    (PM bd(G_P), launched one block earlier on the CNP stream) must be
+    complete, and the folds of the block below are launched now, so they are
+    built while this block runs its backward."""
+
+    @staticmethod
+    def forward(ctx, h, model, i):
+        ctx.model, ctx.i = model, i
+        return h.view_as(h)
+
+    @staticmethod
+    def backward(ctx, dh):
+        model, i = ctx.model, ctx.i
+        cur = torch.cuda.current_stream()
+        cur.wait_event(model.fold_events[i])
+        if i > 0:
+            model.launch_out_folds(i - 1)
         return dh, None, None
 
 
@@ -636,6 +668,31 @@ class PoetLlama(torch.nn.Module):
             hi = self.stack.block_off[f"{i}.down.p"] + d // b
             self.block_ranges.append((lo, hi - lo))
         self.cnp_pipelined = False  # set per step by the trainer
+        # bf16 weight folds of one decoder block (forward bd(G_R) PM, backward
+        # PM bd(G_P)), double-buffered by block parity and built on the CNP
+        # stream one block ahead of their use
+        per_block = sum(m * n for m, n in shapes.values())
+        self.fold_in = [torch.empty(per_block, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        self.fold_out = [torch.empty(per_block, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+        self.fold_events = [torch.cuda.Event() for _ in range(cfg.layers)] if dev.type == "cuda" else []
+        self.fold_views = []
+        for i, mods in enumerate(self.layers):
+            off, views = 0, {}
+            for p in self.PROJ:
+                mod = mods[p]
+                sz = mod.m * mod.n
+                wi = self.fold_in[i % 2][off:off + sz].view(mod.m, mod.n)
+                wo = self.fold_out[i % 2][off:off + sz].view(mod.m, mod.n)
+                views[p] = (wi, wo)
+                # the forward reads bd(G_R) PM; the backward reads PM bd(G_P) (the
+                # forward fold's slot belongs to block i+2 by then: not passed)
+                mod.fstruct_folded = (
+                    N.LayerFactors(mod.packed_r.data_ptr(), mod.packed_p.data_ptr(), None, None,
+                                   mod.g_r16.data_ptr(), mod.g_p16.data_ptr(), None, None, wi.data_ptr(), None),
+                    N.LayerFactors(mod.packed_r.data_ptr(), mod.packed_p.data_ptr(), None, None,
+                                   mod.g_r16.data_ptr(), mod.g_p16.data_ptr(), None, None, None, wo.data_ptr()))
+                off += sz
+            self.fold_views.append(views)
         self.dp_group, self.dp_works = None, []
         self.refresh_maps()
 
@@ -661,6 +718,35 @@ class PoetLlama(torch.nn.Module):
     def poet_layers(self):
         return [mods[p] for mods in self.layers for p in self.PROJ]
 
+    def _use_folds(self, on: bool):
+        for mods in self.layers:
+            for p in self.PROJ:
+                mod = mods[p]
+                mod.fstruct, mod.fstruct_bwd = mod.fstruct_folded if on else (mod.fstruct_plain, mod.fstruct_plain)
+
+    def folds_supported(self) -> bool:
+        """Weight folds apply to BF16 layers on the reassociated path
+        (csrc/layer.cu reassoc(): b in {64, 128, 256}, n % 256 == 0)."""
+        if os.environ.get("POETX_FOLD_PIPELINE", "1") == "0":
+            return False
+        return all(m.desc.dtype == N.BF16 and m.b % 64 == 0 and m.b <= 256 and m.n % 256 == 0
+                   for m in self.poet_layers())
+
+    def launch_in_folds(self, i: int):
+        """Forward folds bd(G_R) PM of block i, on the current stream."""
+        for p in self.PROJ:
+            self.layers[i][p].weight_fold(0, self.fold_views[i][p][0])
+
+    def launch_out_folds(self, i: int):
+        """Backward folds PM bd(G_P) of block i on the CNP stream (after the
+        work already queued on the current stream); records fold_events[i]."""
+        cs = self.cnp_stream
+        cs.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(cs):
+            for p in self.PROJ:
+                self.layers[i][p].weight_fold(1, self.fold_views[i][p][1])
+            self.fold_events[i].record(cs)
+
     def dense_param(self, name, shape):
         return self.dense.view(self.dense.param, name, shape)
 
@@ -674,22 +760,30 @@ class PoetLlama(torch.nn.Module):
         leaves = [embed]
         pipe = self.cnp_pipelined and self.fused
         main = torch.cuda.current_stream() if pipe else None
+        folds = pipe and self.folds_supported()
+        self._use_folds(folds)
         if pipe:
             self.cnp_stream.wait_stream(main)  # fork (also joins it into a graph capture)
             self.stack.forward_factors_range(*self.block_ranges[0])
+            if folds:
+                self.launch_in_folds(0)
         for i, mods in enumerate(self.layers):
             n1 = self.dense_param(f"{i}.norm1", (d,)).detach().requires_grad_(True)
             n2 = self.dense_param(f"{i}.norm2", (d,)).detach().requires_grad_(True)
             leaves += [n1, n2]
             if pipe:
-                main.wait_stream(self.cnp_stream)          # G of block i is ready
+                main.wait_stream(self.cnp_stream)          # G (and folds) of block i are ready
                 if i + 1 < len(self.layers):                # block i+1's G overlaps block i
                     self.cnp_stream.wait_stream(main)
                     with torch.cuda.stream(self.cnp_stream):
                         self.stack.forward_factors_range(*self.block_ranges[i + 1])
+                        if folds:
+                            self.launch_in_folds(i + 1)
                 h = _CnpBackwardHook.apply(h, self, i)
             if self.fused:
                 h = self._block_fused(i, mods, h, n1, n2, B, S)
+                if folds:
+                    h = _FoldPrefetchHook.apply(h, self, i)
                 continue
             x = F.rms_norm(h, (d,), n1.to(torch.bfloat16), 1e-6)
             q = mods["q"](x).view(B, S, H, hd)
@@ -701,6 +795,8 @@ class PoetLlama(torch.nn.Module):
             h = h + mods["o"](a.transpose(1, 2).reshape(B * S, d))
             x = F.rms_norm(h, (d,), n2.to(torch.bfloat16), 1e-6)
             h = h + mods["down"](F.silu(mods["gate"](x)) * mods["up"](x))
+        if folds:  # backward folds of the top block, built while the loss head runs
+            self.launch_out_folds(len(self.layers) - 1)
         nf = self.dense_param("norm_f", (d,)).detach().requires_grad_(True)
         head = self.dense_param("head", (cfg.vocab, d)).detach().requires_grad_(True)
         leaves += [nf, head]
