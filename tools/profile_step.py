@@ -21,6 +21,7 @@ ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--rows", type=int, default=40)
 ap.add_argument("--graph", action="store_true")
 ap.add_argument("--serial", action="store_true", help="no side streams (per-kernel times undisturbed)")
+ap.add_argument("--timeline", action="store_true", help="per-stream occupancy: idle gaps, time with one kernel alone")
 args = ap.parse_args()
 
 FAMILIES = [
@@ -80,3 +81,55 @@ for f, ms in sorted(fams.items(), key=lambda x: -x[1]):
 print("top kernels:")
 for k, (ms, n) in sorted(kern.items(), key=lambda x: -x[1][0])[: args.rows]:
     print(f"  {ms:8.3f} ms {100 * ms / wall:5.1f}% x{n // args.steps:<5d} {k[:110]}")
+
+
+if args.timeline:
+    # kernel intervals per stream from the chrome trace (tid = stream)
+    import json
+    import tempfile
+
+    path = os.path.join(tempfile.mkdtemp(), "trace.json")
+    prof.export_chrome_trace(path)
+    with open(path) as fh:
+        evs = [ev for ev in json.load(fh)["traceEvents"] if ev.get("cat") == "kernel" and ev.get("dur", 0) > 0]
+    t0 = min(ev["ts"] for ev in evs)
+    t1 = max(ev["ts"] + ev["dur"] for ev in evs)
+    edges = []
+    for ev in evs:
+        edges.append((ev["ts"], 1, ev))
+        edges.append((ev["ts"] + ev["dur"], -1, ev))
+    edges.sort(key=lambda x: (x[0], x[1]))
+    active = {}
+    idle = 0.0
+    alone = collections.defaultdict(float)
+    overl = collections.defaultdict(float)
+    by_stream = collections.defaultdict(float)
+    last = t0
+    for ts, kind, ev in edges:
+        dt = ts - last
+        if dt > 0:
+            if not active:
+                idle += dt
+            elif len(active) == 1:
+                alone[family(next(iter(active.values()))["name"])] += dt
+            else:
+                for e2 in active.values():
+                    overl[family(e2["name"])] += dt / len(active)
+        last = ts
+        if kind > 0:
+            active[id(ev)] = ev
+            by_stream[ev.get("tid")] += ev["dur"]
+        else:
+            active.pop(id(ev), None)
+    span = (t1 - t0) / 1e3 / args.steps
+    print(f"\ntimeline over {args.steps} steps: span {span:.2f} ms/step, idle (no kernel) {idle / 1e3 / args.steps:.2f} ms/step")
+    print("time with ONE kernel running, by family (ms/step):")
+    for f, us in sorted(alone.items(), key=lambda x: -x[1]):
+        print(f"  {us / 1e3 / args.steps:8.3f}  {f}")
+    print(f"  {sum(alone.values()) / 1e3 / args.steps:8.3f}  total")
+    print("overlapped time, shared equally among running kernels (ms/step):")
+    for f, us in sorted(overl.items(), key=lambda x: -x[1]):
+        print(f"  {us / 1e3 / args.steps:8.3f}  {f}")
+    print("busy time per stream (ms/step):")
+    for sid, us in sorted(by_stream.items(), key=lambda x: -x[1]):
+        print(f"  stream {sid}: {us / 1e3 / args.steps:8.3f}")
