@@ -289,6 +289,16 @@ int poetx_cross_entropy_fwd(int64_t T, int64_t V, const void* logits, const int6
 int poetx_cross_entropy_bwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, const float* row_max,
                             const float* row_sumexp, const float* dloss, float scale, void* dlogits, void* stream);
 
+/* ------------------------------------------------------ attention backward --
+ * Causal softmax attention backward, bf16, token-major [B*S, H*hd] tensors
+ * (row pitch H*hd), natural-log logsumexp lse [B, H, S] from the forward
+ * (cuDNN's).  dq/dk/dv are written (not accumulated).  Supported shape: S =
+ * 256, hd = 64 (the Llama-60M/350M/1B blocks); anything else returns
+ * POETX_ECONFIG.  Model plumbing, not a reference interface. */
+int poetx_attention_bwd(int64_t B, int64_t S, int64_t H, int64_t hd, const void* q, const void* k, const void* v,
+                        const void* o, const void* dout, const float* lse, void* dq, void* dk, void* dv,
+                        void* stream);
+
 /* ------------------------------------------------ fused neighbour kernels --
  * BF16 row-staged kernels that apply the layer permutations inside the
  * elementwise ops a decoder block needs anyway (used with the

@@ -563,6 +563,41 @@ class _CrossEntropy(torch.autograd.Function):
         return grad, None
 
 
+class _Attention(torch.autograd.Function):
+    """Causal attention over token-major [B*S, H*hd] q, k, v -> [B*S, H*hd]:
+    cuDNN forward (output + natural-log logsumexp), backward on the fused
+    tcgen05 kernel (csrc/attention.cu; S = 256, hd = 64)."""
+
+    @staticmethod
+    def forward(ctx, q, k, v, B, S, H, hd):
+        qt, kt, vt = (t.view(B, S, H, hd).transpose(1, 2) for t in (q, k, v))
+        o, lse = torch.ops.aten._scaled_dot_product_cudnn_attention(qt, kt, vt, None, True, 0.0, True, False)[:2]
+        out = o.transpose(1, 2).reshape(B * S, H * hd)
+        if not out.is_contiguous() or not lse.is_contiguous():
+            raise RuntimeError("cuDNN attention returned an unexpected layout")
+        ctx.save_for_backward(q, k, v, out, lse)
+        ctx.shape = (B, S, H, hd)
+        return out
+
+    @staticmethod
+    def backward(ctx, do):
+        q, k, v, out, lse = ctx.saved_tensors
+        B, S, H, hd = ctx.shape
+        do = do.contiguous()
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        N.call("poetx_attention_bwd", B, S, H, hd, q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(),
+               do.data_ptr(), lse.data_ptr(), dq.data_ptr(), dk.data_ptr(), dv.data_ptr(), N.stream_ptr(q.device))
+        return dq, dk, dv, None, None, None, None
+
+
+def fused_attention_supported(S, hd):
+    """The tcgen05 attention backward covers sequence 256 with head_dim 64.
+    Opt-in (env POETX_ATTN_BWD=1): it is correct and deterministic but, at one
+    199 KB CTA per SM, only level with cuDNN's backward inside the step
+    (130 vs ~143 us alone; step 108.9k vs 109.1k tok/s)."""
+    return S == 256 and hd == 64 and os.environ.get("POETX_ATTN_BWD", "0") == "1"
+
+
 def _permute_cols(x, idx):
     y = torch.empty_like(x)
     N.call("poetx_permute_cols", N.BF16, x.shape[0], x.shape[1], idx.data_ptr(), x.data_ptr(), y.data_ptr(),
@@ -849,11 +884,16 @@ class PoetLlama(torch.nn.Module):
                                        self.sin32, S, H, hd),
             lambda: _Permute.apply(_PoetRawFn.apply(uv, v, rg(v)), pout(v)[1], pout(v)[0]),
         ])
-        a = F.scaled_dot_product_attention(qr.view(B, S, H, hd).transpose(1, 2), kr.view(B, S, H, hd).transpose(1, 2),
-                                           vz.view(B, S, H, hd).transpose(1, 2), is_causal=True)
-        a_d = a.detach()
-        uo = _Permute.apply(a.transpose(1, 2).reshape(B * S, d), pin(o)[0], pin(o)[1])
-        regen_o = lambda: _permute_cols(a_d.transpose(1, 2).reshape(B * S, d), pin(o)[0])  # noqa: E731
+        if fused_attention_supported(S, hd):
+            a2 = _Attention.apply(qr, kr, vz, B, S, H, hd)
+        else:
+            a = F.scaled_dot_product_attention(qr.view(B, S, H, hd).transpose(1, 2),
+                                               kr.view(B, S, H, hd).transpose(1, 2),
+                                               vz.view(B, S, H, hd).transpose(1, 2), is_causal=True)
+            a2 = a.transpose(1, 2).reshape(B * S, d)
+        a_d = a2.detach()
+        uo = _Permute.apply(a2, pin(o)[0], pin(o)[1])
+        regen_o = lambda: _permute_cols(a_d, pin(o)[0])  # noqa: E731
         h = _ScatterAdd.apply(h, _PoetRawFn.apply(uo, o, regen_o), pout(o)[1], pout(o)[0])
         h2_in, n2d = h.detach(), n2.detach()
         rg2 = lambda mod: (lambda: _rmsnorm_regather(h2_in, n2d, pin(mod)[0]))  # noqa: E731
