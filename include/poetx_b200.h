@@ -197,6 +197,10 @@ typedef struct {
    * dequantizes into its workspace right before the mm2 / adjoint GEMM. */
   const int8_t* pm_codes;
   const void* pm_scales;
+  /* BF16 layers: nonzero -> reassociated products, the block factors folded
+   * into the frozen weight (bd(G_R) PM, PM bd(G_P)) -- fewer bytes
+   * when T is large against n*b; zero -> factors applied to the activations. */
+  int fold_weight;
 } poetx_layer_desc;
 
 /* factor state produced by poetx_layer_factors and consumed by fwd/bwd.

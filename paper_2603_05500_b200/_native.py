@@ -55,6 +55,7 @@ class LayerDesc(C.Structure):
         ("premerged", VP),
         ("pm_codes", VP),
         ("pm_scales", VP),
+        ("fold_weight", C.c_int),
     ]
 
 

@@ -62,7 +62,7 @@ bool reassoc(const poetx_layer_desc* d) {
     const char* e = getenv("POETX_REASSOC");
     return e && e[0] == '0' ? 0 : 1;
   }();
-  return on && d->dtype == POETX_BF16 && d->b % 64 == 0 && d->b <= 256 && d->n % 256 == 0;
+  return on && d->fold_weight && d->dtype == POETX_BF16 && d->b % 64 == 0 && d->b <= 256 && d->n % 256 == 0;
 }
 
 // the premerged weight for a GEMM: the bf16/fp32/fp64 copy, or the int8

@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--model", default="llama-1b")
 ap.add_argument("--mb", type=int, default=32)
 ap.add_argument("--variant", default="fast")
+ap.add_argument("--quantized", action="store_true")
 ap.add_argument("--steps", type=int, default=2)
 ap.add_argument("--rows", type=int, default=40)
 ap.add_argument("--graph", action="store_true")
@@ -48,7 +49,7 @@ def family(name):
     return "other torch"
 
 
-cfg = llama_config(args.model, variant=args.variant)
+cfg = llama_config(args.model, variant=args.variant, quantized=args.quantized)
 tr = Trainer(cfg, args.mb, merge_gap=0)
 if args.serial:
     tr.model.concurrent = False
@@ -92,6 +93,15 @@ if args.timeline:
     prof.export_chrome_trace(path)
     with open(path) as fh:
         evs = [ev for ev in json.load(fh)["traceEvents"] if ev.get("cat") == "kernel" and ev.get("dur", 0) > 0]
+
+    def tfam(ev):
+        # split the pair-GEMM family by grid: full-width launches (mm2 / adjoint /
+        # folds / CNP) vs the SM-share-sized segmented outer products
+        f = family(ev["name"])
+        if "tc2_kernel" in ev["name"]:
+            grid = ev.get("args", {}).get("grid", [0])
+            f += " [outer, partial grid]" if grid and grid[0] < 140 else " [full grid]"
+        return f
     t0 = min(ev["ts"] for ev in evs)
     t1 = max(ev["ts"] + ev["dur"] for ev in evs)
     edges = []
@@ -111,10 +121,10 @@ if args.timeline:
             if not active:
                 idle += dt
             elif len(active) == 1:
-                alone[family(next(iter(active.values()))["name"])] += dt
+                alone[tfam(next(iter(active.values())))] += dt
             else:
                 for e2 in active.values():
-                    overl[family(e2["name"])] += dt / len(active)
+                    overl[tfam(e2)] += dt / len(active)
         last = ts
         if kind > 0:
             active[id(ev)] = ev
