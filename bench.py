@@ -302,7 +302,10 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         achieved = (flops.value / (tot_ms.value / 1e3) / 1e12) if tot_ms.value > 0 else None
         if cnt.value:
-            k_share = tot_ms.value / prof_ms  # share of the (eager) profiled steps
+            # the kernel's device time per step (its own launches, events on its
+            # stream, measured in the eager pass) over the timed step's time; the
+            # eager pass itself is slower (one event pair per launch, serialised)
+            k_share = tot_ms.value / ms
         out = {
             "metric": METRIC,
             "value": round(value, 1),
@@ -338,6 +341,7 @@ def run_ours(args, rank, world, local_rank):
                 "traffic": gemm_traffic(), "traffic_unit": "bytes/launch (ncu dram read+write)",
                 "traffic_source": "profiles/r01/ncu_gemm_traffic.json", "launches": cnt.value,
                 "share_of_step": round(k_share, 4) if k_share else None,
+                "kernel_ms_per_step": round(tot_ms.value / args.steps, 3) if cnt.value else None,
                 "peak_source": src + " sustained (kernel timed inside a long step)",
                 "timing": "CUDA events around every tc_gemm launch on its stream, extra eager profiled pass of the "
                           "same steps with the q/k/v and gate/up chains serialised",

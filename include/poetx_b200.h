@@ -293,6 +293,19 @@ int poetx_cross_entropy_fwd(int64_t T, int64_t V, const void* logits, const int6
 int poetx_cross_entropy_bwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, const float* row_max,
                             const float* row_sumexp, const float* dloss, float scale, void* dlogits, void* stream);
 
+/* ---------------------------------------------------- singular values --
+ * svd_singular_values (linalg.py:166-218): one-sided Jacobi in float64,
+ * same rotation and stopping rule (tol relative to sqrt(alpha beta), stop
+ * after a rotation-free sweep), round-robin pair order, one CTA per matrix.
+ * a: batch row-major [rows, cols] float64; sv: batch x min(rows, cols),
+ * descending.  residual / sweeps (optional, per matrix): worst relative
+ * off-diagonal of the last sweep (0 when converged) and the sweeps used, -1
+ * when max_sweeps ran out (the caller raises ConvergenceError).
+ * min(rows, cols) <= 4096. */
+size_t poetx_singular_values_workspace_bytes(int64_t batch, int64_t rows, int64_t cols);
+int poetx_singular_values(int64_t batch, int64_t rows, int64_t cols, const double* a, double* sv, double tol,
+                          int max_sweeps, double* residual, int* sweeps, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------ attention backward --
  * Causal softmax attention backward, bf16, token-major [B*S, H*hd] tensors
  * (row pitch H*hd), natural-log logsumexp lse [B, H, S] from the forward

@@ -215,6 +215,47 @@ def orthogonality_error(g):
 # ---------------------------------------------------------------------------
 
 
+def svd_singular_values(a, tol=1e-10, max_sweeps=100):
+    """One-sided Jacobi singular values, float64, lexicographic pair order and
+    the same rotation / stopping rule (linalg.py:166-218).  Returns
+    (descending singular values, converged flag, worst residual of the last
+    sweep)."""
+    w = np.array(a, dtype=np.float64)
+    if w.shape[0] < w.shape[1]:
+        w = w.T.copy()
+    n = w.shape[1]
+    if n == 0:
+        return np.zeros(0), True, 0.0
+    norms = np.einsum("ij,ij->j", w, w)
+    worst = 0.0
+    for _ in range(max_sweeps):
+        rotated = False
+        worst = 0.0
+        for p in range(n - 1):
+            for q in range(p + 1, n):
+                alpha, beta = norms[p], norms[q]
+                gamma = float(w[:, p] @ w[:, q])
+                scale = np.sqrt(alpha * beta)
+                if scale <= 0.0 or abs(gamma) <= tol * scale:
+                    continue
+                worst = max(worst, abs(gamma) / scale)
+                rotated = True
+                zeta = (beta - alpha) / (2.0 * gamma)
+                t = np.copysign(1.0, zeta) / (abs(zeta) + np.sqrt(1.0 + zeta * zeta))
+                c = 1.0 / np.sqrt(1.0 + t * t)
+                s = c * t
+                cp = w[:, p].copy()
+                w[:, p] = c * cp - s * w[:, q]
+                w[:, q] = s * cp + c * w[:, q]
+                norms[p] = float(w[:, p] @ w[:, p])
+                norms[q] = float(w[:, q] @ w[:, q])
+        if not rotated:
+            sv = np.sort(np.sqrt(np.maximum(norms, 0.0)))[::-1].copy()
+            return sv, True, 0.0
+    sv = np.sort(np.sqrt(np.maximum(norms, 0.0)))[::-1].copy()
+    return sv, False, worst
+
+
 def invert(fwd):
     inv = np.empty_like(fwd)
     inv[fwd] = np.arange(fwd.shape[0], dtype=fwd.dtype)

@@ -8,6 +8,7 @@ sm_100a kernels in libpoetx_b200.so reached through a C ABI
 (include/poetx_b200.h).  There is no CPU fallback.
 """
 
+from .audit import singular_values, spectral_norm, spectrum_audit
 from .blockdiag import (
     BlockDiagonalFactor,
     apply_to_features,

@@ -354,8 +354,14 @@ class PoetLinearLayer:
             old_base = old_base.dequantize()
         pm_new, w_new = self._merge_call(g_r, g_p, new_in, new_out, want_w=compute_sv_drift)
         if compute_sv_drift:
-            sv_old = torch.linalg.svdvals(old_base.double())
-            sv_new = torch.linalg.svdvals(w_new.double())
+            # the reference's Jacobi singular values (audit.py / csrc/svd.cu) up to
+            # a million entries; cuSOLVER's svdvals beyond (one CTA per matrix)
+            if self.m * self.n <= (1 << 20):
+                from .audit import singular_values
+                sv_old, sv_new = singular_values(old_base), singular_values(w_new)
+            else:
+                sv_old = torch.linalg.svdvals(old_base.double())
+                sv_new = torch.linalg.svdvals(w_new.double())
             denom = torch.clamp(sv_old, min=np.finfo(np.float64).tiny)
             drift = float(torch.max(torch.abs(sv_new - sv_old) / denom))
         self.premerged = pm_new

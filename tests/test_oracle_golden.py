@@ -168,3 +168,12 @@ def test_quantized_layer_bitwise(tag):
     lay.merge_and_reinit(d[f"l_{tag}_new_perm_in"], d[f"l_{tag}_new_perm_out"])
     assert np.array_equal(lay.codes, d[f"l_{tag}_merged_codes"])
     assert np.array_equal(lay.scales, d[f"l_{tag}_merged_scales"])
+
+
+@pytest.mark.parametrize("tag", ["square", "tall", "wide", "rank6", "single", "graded"])
+def test_jacobi_singular_values_bitwise(tag):
+    """linalg.svd_singular_values restated: bitwise against the reference."""
+    g = load("spectrum.npz")
+    sv, ok, _ = O.svd_singular_values(g[f"a_{tag}"])
+    assert ok
+    assert np.array_equal(sv, g[f"sv_{tag}"])

@@ -1,6 +1,3 @@
 mkdir -p gpurun_out
-( for c in 1b-poetxq-mem 1b-poetxq-mem 1b-poetx-mem 1b-poetxq-mem 8b-poetx-mem 8b-poetx-mem; do
-    echo "$c: $(timeout 600 python tools/configs_bench.py --one $c 2>/dev/null | python -c "import json,sys; d=json.loads(sys.stdin.readlines()[-1]); print(round(d.get('tokens_per_s',0)), round(d.get('ms_per_step',0),1), round(d.get('peak_hbm_gb',0),1))")"
-  done
-  nvidia-smi --query-gpu=clocks.sm,clocks_throttle_reasons.active,temperature.gpu,power.draw --format=csv
-) > gpurun_out/ab_cfg.txt 2>&1
+( for i in 1 2 3 4 5; do date +%T; timeout 200 python tools/hangprobe.py llama-8b 1 mem 30 2>&1 | tail -30; echo "rc=$?"; done
+) > gpurun_out/hang.txt 2>&1
