@@ -16,7 +16,10 @@ import torch
 
 from .errors import ConfigError, NumericsError, PoetxError, ShapeError, StateError
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpoetx_b200.so")
+# POETX_LIB_PATH: load another build of the same library (same-box A/B runs,
+# tools/ab_build.sh); the default is the in-tree build
+LIB_PATH = os.environ.get("POETX_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                           "libpoetx_b200.so")
 
 F32, F64, BF16 = 0, 1, 2
 FAST, MEM = 0, 1

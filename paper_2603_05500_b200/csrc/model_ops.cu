@@ -367,27 +367,30 @@ __global__ void __launch_bounds__(kThreads) rope_scatter_kernel(
     stage_rows(vs, v + r0 * d, nr, d);
     cp_wait_all();
     __syncthreads();
-    for (int i = threadIdx.x; i < nvec; i += kThreads) {
-      const int c0 = 8 * i, wi = c0 & (hd - 1);
-      const bool first = wi < half;
-      const int pc0 = first ? c0 + half : c0 - half;
-      const int f0 = first ? wi : wi - half;
+    // one thread: 8 outputs of a head's first half and their 8 partners in
+    // the second half -- the 16 gathers feed 16 outputs
+    for (int i = threadIdx.x; i < nvec / 2; i += kThreads) {
+      const int head = (8 * i) / half, f0 = (8 * i) % half;
+      const int c0 = head * hd + f0, c1 = c0 + half;
       int me[8], pa[8];
       load_idx8(inv, c0, me);
-      load_idx8(inv, pc0, pa);
+      load_idx8(inv, c1, pa);
       for (int r = 0; r < nr; ++r) {
         const int s = static_cast<int>((r0 + r) % S);
         float cs[8], sn[8];
         load_f8(cosb + s * half + f0, cs);
         load_f8(sinb + s * half + f0, sn);
         const __nv_bfloat16* row = vs + r * d;
-        float o[8];
+        float o0[8], o1[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
           const float zm = bf(row[me[q]]), zp = bf(row[pa[q]]);
-          o[q] = first ? zm * cs[q] - zp * sn[q] : zm * cs[q] + zp * sn[q];
+          o0[q] = zm * cs[q] - zp * sn[q];
+          o1[q] = zp * cs[q] + zm * sn[q];
         }
-        __stcs(reinterpret_cast<uint4*>(out + (r0 + r) * d) + i, pack8(o));
+        __nv_bfloat16* orow = out + (r0 + r) * d;
+        __stcs(reinterpret_cast<uint4*>(orow + c0), pack8(o0));
+        __stcs(reinterpret_cast<uint4*>(orow + c1), pack8(o1));
       }
     }
     __syncthreads();
@@ -408,29 +411,39 @@ __global__ void __launch_bounds__(kThreads) rope_scatter_bwd_kernel(
     stage_rows(os, dout + r0 * d, nr, d);
     cp_wait_all();
     __syncthreads();
-    for (int i = threadIdx.x; i < nvec; i += kThreads) {
-      int cc[8], pp[8], ff[8];
-      bool first[8];
-      load_idx8(fwd, 8 * i, cc);
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        const int wi = cc[q] & (hd - 1);
-        first[q] = wi < half;
-        ff[q] = first[q] ? wi : wi - half;
-        pp[q] = first[q] ? cc[q] + half : cc[q] - half;
-      }
+    // dz = RoPE^T(dout) in place, pairs of contiguous 8-vectors (no gathers)
+    for (int i = threadIdx.x; i < nvec / 2; i += kThreads) {
+      const int head = (8 * i) / half, f0 = (8 * i) % half;
+      const int c0 = head * hd + f0, c1 = c0 + half;
       for (int r = 0; r < nr; ++r) {
         const int s = static_cast<int>((r0 + r) % S);
-        const float* cr = cosb + s * half;
-        const float* sr = sinb + s * half;
+        float cs[8], sn[8], g0[8], g1[8];
+        load_f8(cosb + s * half + f0, cs);
+        load_f8(sinb + s * half + f0, sn);
+        uint4* p0 = reinterpret_cast<uint4*>(os + r * d + c0);
+        uint4* p1 = reinterpret_cast<uint4*>(os + r * d + c1);
+        unpack8(*p0, g0);
+        unpack8(*p1, g1);
+        float d0[8], d1[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          d0[q] = g0[q] * cs[q] + g1[q] * sn[q];
+          d1[q] = g1[q] * cs[q] - g0[q] * sn[q];
+        }
+        *p0 = pack8(d0);
+        *p1 = pack8(d1);
+      }
+    }
+    __syncthreads();
+    // dv[j] = dz[fwd[j]]: one gather per output
+    for (int i = threadIdx.x; i < nvec; i += kThreads) {
+      int cc[8];
+      load_idx8(fwd, 8 * i, cc);
+      for (int r = 0; r < nr; ++r) {
         const __nv_bfloat16* row = os + r * d;
         float o[8];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float cs = __ldg(cr + ff[q]), sn = __ldg(sr + ff[q]);
-          const float g = bf(row[cc[q]]), gp = bf(row[pp[q]]);
-          o[q] = first[q] ? g * cs + gp * sn : g * cs - gp * sn;
-        }
+        for (int q = 0; q < 8; ++q) o[q] = bf(row[cc[q]]);
         __stcs(reinterpret_cast<uint4*>(dv + (r0 + r) * d) + i, pack8(o));
       }
     }
