@@ -336,7 +336,9 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
 /* out[:, j] = silu(vg[:, cg[j]]) * vu[:, cu[j]] */
 int poetx_swiglu_gather(int64_t T, int64_t f, const void* vg, const void* vu, const int32_t* cg,
                         const int32_t* cu, void* out, void* stream);
-/* dvg[:, j] = du[:, A[j]] silu'(vg[:, j]) vu[:, B[j]];  dvu[:, j] = du[:, C[j]] silu(vg[:, D[j]]) */
+/* dvg[:, j] = du[:, A[j]] silu'(vg[:, j]) vu[:, B[j]];  dvu[:, j] = du[:, C[j]] silu(vg[:, D[j]]).
+ * The maps of one SwiGLU satisfy C = A o D (C[j] = A[D[j]]); the kernel uses
+ * that (dvu formed in gate order, then gathered through D) and does not read C. */
 int poetx_swiglu_gather_bwd(int64_t T, int64_t f, const void* vg, const void* vu, const void* du,
                             const int32_t* A, const int32_t* B, const int32_t* C, const int32_t* D,
                             void* dvg, void* dvu, void* stream);

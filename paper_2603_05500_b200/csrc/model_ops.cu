@@ -309,6 +309,51 @@ __global__ void __launch_bounds__(kThreads) swiglu_gather_kernel(
 }
 
 // dv_g[j] = du[A[j]] * silu'(v_g[j]) * v_u[B[j]] ; dv_u[j] = du[C[j]] * silu(v_g[D[j]])
+// on a staged tile of nr rows (gs, us, ds: RT rows each).  C[j] = A[D[j]], so
+// dv_u is first formed in gate order (du[A[k]] silu(v_g[k]), no extra gather)
+// over the thread's own v_g vector in place, then gathered through D: three
+// gathers per element instead of four.
+template <int RT>
+__device__ __forceinline__ void swiglu_bwd_tile(int64_t r0, int nr, int f, __nv_bfloat16* gs,
+                                                const __nv_bfloat16* us, const __nv_bfloat16* ds,
+                                                const int32_t* __restrict__ A, const int32_t* __restrict__ B,
+                                                const int32_t* __restrict__ D, __nv_bfloat16* __restrict__ dvg,
+                                                __nv_bfloat16* __restrict__ dvu) {
+  const int nvec = f / 8;
+  for (int i = threadIdx.x; i < nvec; i += kThreads) {
+    int ia[8], ib[8];
+    load_idx8(A, 8 * i, ia);
+    load_idx8(B, 8 * i, ib);
+    for (int r = 0; r < nr; ++r) {
+      const int o = r * f;
+      float gself[8], g[8], ug[8];
+      uint4* gv = reinterpret_cast<uint4*>(gs + o) + i;
+      unpack8(*gv, gself);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float sg = sigmoid_f(gself[q]);
+        const float dh = bf(ds[o + ia[q]]);
+        g[q] = dh * (sg * (1.f + gself[q] * (1.f - sg))) * bf(us[o + ib[q]]);
+        ug[q] = dh * gself[q] * sg;
+      }
+      __stcs(reinterpret_cast<uint4*>(dvg + (r0 + r) * f) + i, pack8(g));
+      *gv = pack8(ug);  // only this thread reads this v_g vector
+    }
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nvec; i += kThreads) {
+    int id[8];
+    load_idx8(D, 8 * i, id);
+    for (int r = 0; r < nr; ++r) {
+      const __nv_bfloat16* row = gs + r * f;
+      float u[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) u[q] = bf(row[id[q]]);
+      __stcs(reinterpret_cast<uint4*>(dvu + (r0 + r) * f) + i, pack8(u));
+    }
+  }
+}
+
 template <int RT>
 __global__ void __launch_bounds__(kThreads) swiglu_gather_bwd_kernel(
     int64_t T, int f, const __nv_bfloat16* __restrict__ vg, const __nv_bfloat16* __restrict__ vu,
@@ -319,7 +364,7 @@ __global__ void __launch_bounds__(kThreads) swiglu_gather_bwd_kernel(
   __nv_bfloat16* gs = reinterpret_cast<__nv_bfloat16*>(sm);
   __nv_bfloat16* us = gs + RT * f;
   __nv_bfloat16* ds = us + RT * f;
-  const int nvec = f / 8;
+  (void)Cc;  // C = A o D: dv_u is gathered through D from the gate-order values
   for (int64_t r0 = static_cast<int64_t>(blockIdx.x) * RT; r0 < T; r0 += static_cast<int64_t>(gridDim.x) * RT) {
     const int nr = static_cast<int>(T - r0 < RT ? T - r0 : RT);
     stage_rows(gs, vg + r0 * f, nr, f);
@@ -327,27 +372,7 @@ __global__ void __launch_bounds__(kThreads) swiglu_gather_bwd_kernel(
     stage_rows(ds, du + r0 * f, nr, f);
     cp_wait_all();
     __syncthreads();
-    for (int i = threadIdx.x; i < nvec; i += kThreads) {
-      int ia[8], ib[8], ic[8], id[8];
-      load_idx8(A, 8 * i, ia);
-      load_idx8(B, 8 * i, ib);
-      load_idx8(Cc, 8 * i, ic);
-      load_idx8(D, 8 * i, id);
-      for (int r = 0; r < nr; ++r) {
-        const int o = r * f;
-        float gself[8], g[8], u[8];
-        unpack8(reinterpret_cast<const uint4*>(gs + o)[i], gself);
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float sg = sigmoid_f(gself[q]);
-          g[q] = bf(ds[o + ia[q]]) * (sg * (1.f + gself[q] * (1.f - sg))) * bf(us[o + ib[q]]);
-          const float gd = bf(gs[o + id[q]]);
-          u[q] = bf(ds[o + ic[q]]) * gd * sigmoid_f(gd);
-        }
-        __stcs(reinterpret_cast<uint4*>(dvg + (r0 + r) * f) + i, pack8(g));
-        __stcs(reinterpret_cast<uint4*>(dvu + (r0 + r) * f) + i, pack8(u));
-      }
-    }
+    swiglu_bwd_tile<RT>(r0, nr, f, gs, us, ds, A, B, D, dvg, dvu);
     __syncthreads();
   }
 }

@@ -37,4 +37,4 @@ if "--time" in sys.argv:
     e.record()
     torch.cuda.synchronize()
     us = s.elapsed_time(e) / 50 * 1e3
-    print(f"{op} ROW_DB={os.environ.get('POETX_ROW_DB', '1')}: {us:.1f} us, {nbytes / us / 1e3:.0f} GB/s")
+    print(f"{op}: {us:.1f} us, {nbytes / us / 1e3:.0f} GB/s")
