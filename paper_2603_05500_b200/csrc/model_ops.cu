@@ -17,6 +17,7 @@
 #include <cstdlib>
 
 #include "common.cuh"
+#include "tile8.cuh"
 
 namespace poetx {
 namespace {
@@ -250,6 +251,169 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
     dst[0] = make_float4(dwacc[slot][0], dwacc[slot][1], dwacc[slot][2], dwacc[slot][3]);
     dst[1] = make_float4(dwacc[slot][4], dwacc[slot][5], dwacc[slot][6], dwacc[slot][7]);
   }
+}
+
+// ---------------------------------------------------------------------------
+// Feature-major 8-token variants (tile8.cuh) of the RMSNorm kernels: one
+// thread per 8-column vector (blockDim = d / 8), tiles of 8 tokens.  The
+// gathered rows are staged as d 16-byte slots, each holding one feature of
+// all 8 tokens, so a gather is one 16-byte LDS serving 8 tokens instead of
+// eight bank-conflicted 2-byte LDS; 8x8 transposes (PRMT) turn slots back
+// into row vectors for coalesced stores.  Same fp32 expressions and
+// reduction order as the row-staged kernels at d = 2048.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float block_row_sum(float v, float* red, int r, int nw) {
+  // one value per thread for row r -> sum over the block (warp shuffles, then warps in order)
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (threadIdx.x % 32 == 0) red[r * 32 + threadIdx.x / 32] = v;
+  return v;
+}
+
+template <int K>
+__global__ void __launch_bounds__(256) rmsnorm_gather_t8_kernel(int64_t T, int d, const __nv_bfloat16* __restrict__ x,
+                                                                const float* __restrict__ w, float eps, IdxList outs,
+                                                                float* __restrict__ rstd_out) {
+  extern __shared__ __align__(16) uint4 slots[];  // d slots
+  __shared__ float red[8 * 32];
+  __shared__ float rs_s[8];
+  const int c = threadIdx.x, nw = blockDim.x / 32;
+  float wv[8];
+  load_f8(w + 8 * c, wv);
+  const int64_t tiles = (T + 7) / 8;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t r0 = tile * 8;
+    const int nr = static_cast<int>(T - r0 < 8 ? T - r0 : 8);
+    uint4 rr[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      rr[r] = r < nr ? __ldcs(reinterpret_cast<const uint4*>(x + (r0 + r) * d) + c) : make_uint4(0, 0, 0, 0);
+      float v[8];
+      unpack8(rr[r], v);
+      float ss = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) ss += v[q] * v[q];
+      block_row_sum(ss, red, r, nw);
+    }
+    __syncthreads();
+    if (threadIdx.x < 8) {
+      float tot = 0.f;
+      for (int k = 0; k < nw; ++k) tot += red[threadIdx.x * 32 + k];
+      const float rs = rsqrtf(tot / static_cast<float>(d) + eps);
+      rs_s[threadIdx.x] = rs;
+      if (threadIdx.x < nr) rstd_out[r0 + threadIdx.x] = rs;
+    }
+    __syncthreads();
+    uint4 yy[8], cc[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      float v[8];
+      unpack8(rr[r], v);
+      const float rs = rs_s[r];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = v[q] * rs * wv[q];
+      yy[r] = pack8(v);
+    }
+    tr8x8(yy, cc);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) slots[fslot(8 * c + q)] = cc[q];
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      int id[8];
+      load_idx8(outs.idx[k], 8 * c, id);
+      uint4 g[8], o[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) g[q] = slots[fslot(id[q])];
+      tr8x8(g, o);
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(outs.ptr[k]);
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < nr) __stcs(reinterpret_cast<uint4*>(dst + (r0 + r) * d) + c, o[r]);
+    }
+    __syncthreads();
+  }
+}
+
+template <int K>
+__global__ void __launch_bounds__(256, 2) rmsnorm_gather_bwd_t8_kernel(
+    int64_t T, int d, const __nv_bfloat16* __restrict__ x, const float* __restrict__ w,
+    const float* __restrict__ rstd_in, IdxList dus, const __nv_bfloat16* __restrict__ dres,
+    __nv_bfloat16* __restrict__ dx, float* __restrict__ dw_part) {
+  extern __shared__ __align__(16) uint4 slots[];
+  __shared__ float red[8 * 32];
+  const int c = threadIdx.x, nw = blockDim.x / 32;
+  float wv[8], dwacc[8];
+  load_f8(w + 8 * c, wv);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) dwacc[q] = 0.f;
+  const int64_t tiles = (T + 7) / 8;
+  for (int64_t tile = blockIdx.x; tile < tiles; tile += gridDim.x) {
+    const int64_t r0 = tile * 8;
+    const int nr = static_cast<int>(T - r0 < 8 ? T - r0 : 8);
+    float dy[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r)
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dy[r][q] = 0.f;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {  // dy = sum_k du_k[:, inv_k], k ascending
+      const __nv_bfloat16* src = static_cast<const __nv_bfloat16*>(dus.ptr[k]);
+      uint4 rr[8], cc[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        rr[r] = r < nr ? __ldcs(reinterpret_cast<const uint4*>(src + (r0 + r) * d) + c) : make_uint4(0, 0, 0, 0);
+      tr8x8(rr, cc);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) slots[fslot(8 * c + q)] = cc[q];
+      __syncthreads();
+      int id[8];
+      load_idx8(dus.idx[k], 8 * c, id);
+      uint4 g[8], o[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) g[q] = slots[fslot(id[q])];
+      tr8x8(g, o);
+#pragma unroll
+      for (int r = 0; r < 8; ++r) {
+        float v[8];
+        unpack8(o[r], v);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) dy[r][q] += v[q];
+      }
+      __syncthreads();
+    }
+    float xv[8][8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const uint4 xr = r < nr ? __ldcs(reinterpret_cast<const uint4*>(x + (r0 + r) * d) + c) : make_uint4(0, 0, 0, 0);
+      unpack8(xr, xv[r]);
+      float dot = 0.f;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) dot += dy[r][q] * wv[q] * xv[r][q];
+      block_row_sum(dot, red, r, nw);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      if (r >= nr) break;
+      float tot = 0.f;
+      for (int k = 0; k < nw; ++k) tot += red[r * 32 + k];
+      const float rs = rstd_in[r0 + r];
+      const float coef = rs * rs * rs * tot / static_cast<float>(d);
+      float o[8], res[8];
+      if (dres) unpack8(__ldcs(reinterpret_cast<const uint4*>(dres + (r0 + r) * d) + c), res);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        o[q] = rs * dy[r][q] * wv[q] - coef * xv[r][q];
+        if (dres) o[q] += res[q];
+        dwacc[q] += dy[r][q] * xv[r][q] * rs;
+      }
+      __stcs(reinterpret_cast<uint4*>(dx + (r0 + r) * d) + c, pack8(o));
+    }
+    __syncthreads();
+  }
+  float4* dst = reinterpret_cast<float4*>(dw_part + static_cast<int64_t>(blockIdx.x) * d + 8 * c);
+  dst[0] = make_float4(dwacc[0], dwacc[1], dwacc[2], dwacc[3]);
+  dst[1] = make_float4(dwacc[4], dwacc[5], dwacc[6], dwacc[7]);
 }
 
 // column sums of a [rows, d] partial matrix: 8 warps split the rows of a
@@ -629,6 +793,33 @@ void set_smem(K kernel, size_t smem) {
   if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
+// feature-major 8-token RMSNorm kernels: one thread per 8-column vector, so
+// d / 8 must be a whole number of warps within a CTA (env POETX_ROW_T8=0 off)
+bool use_t8(int64_t d) {
+  static const bool on = [] {
+    const char* e = getenv("POETX_ROW_T8");
+    return e ? atoi(e) != 0 : true;
+  }();
+  return on && d % 256 == 0 && d / 8 <= 256;
+}
+// the backward's T8 variant measured slower (K = 3: 84 vs 74 us at d = 2048;
+// 128-register cap, K restagings per tile): opt-in with POETX_ROW_T8_BWD=1
+bool use_t8_bwd(int64_t d) {
+  static const bool on = [] {
+    const char* e = getenv("POETX_ROW_T8_BWD");
+    return e && atoi(e) != 0;
+  }();
+  return on && use_t8(d);
+}
+unsigned t8_grid(int64_t T, size_t smem) {
+  const int64_t tiles = (T + 7) / 8;
+  int64_t per_sm = static_cast<int64_t>((228 * 1024) / (smem + 2048));
+  if (per_sm > 8) per_sm = 8;
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = 148 * per_sm;
+  return static_cast<unsigned>(tiles < cap ? (tiles > 0 ? tiles : 1) : cap);
+}
+
 
 }  // namespace
 }  // namespace poetx
@@ -646,6 +837,21 @@ int poetx_rmsnorm_gather(int64_t T, int64_t d, const void* x, const float* w, fl
   if (T == 0) return POETX_OK;
   IdxList L{};
   for (int k = 0; k < K; ++k) { L.idx[k] = idx[k]; L.ptr[k] = out[k]; }
+  if (use_t8(d)) {
+    const size_t tsm = static_cast<size_t>(d) * 16;
+    const unsigned grid = t8_grid(T, tsm);
+    cudaStream_t st = as_stream(stream);
+    switch (K) {
+      case 1: set_smem(rmsnorm_gather_t8_kernel<1>, tsm);
+              rmsnorm_gather_t8_kernel<1><<<grid, d / 8, tsm, st>>>(T, d, static_cast<const __nv_bfloat16*>(x), w, eps, L, rstd); break;
+      case 2: set_smem(rmsnorm_gather_t8_kernel<2>, tsm);
+              rmsnorm_gather_t8_kernel<2><<<grid, d / 8, tsm, st>>>(T, d, static_cast<const __nv_bfloat16*>(x), w, eps, L, rstd); break;
+      default: set_smem(rmsnorm_gather_t8_kernel<3>, tsm);
+               rmsnorm_gather_t8_kernel<3><<<grid, d / 8, tsm, st>>>(T, d, static_cast<const __nv_bfloat16*>(x), w, eps, L, rstd); break;
+    }
+    POETX_LAUNCHED("rmsnorm_gather_t8");
+    return POETX_OK;
+  }
   POETX_K_DISPATCH(K, rt, rmsnorm_gather_kernel, set_smem(k, smem);
                    k<<<row_grid(T, rt), kThreads, smem, as_stream(stream)>>>(
                        T, d, static_cast<const __nv_bfloat16*>(x), w, eps, L, rstd);)
@@ -659,7 +865,10 @@ static int bwd_rt(int64_t d, int K) { return pick_rt(d * 2 * (1 + K) + d * 4, 96
 
 size_t poetx_rmsnorm_gather_bwd_workspace_bytes(int64_t T, int64_t d) {
   int rt = bwd_rt(d, 1);  // largest grid over K
-  return static_cast<size_t>(row_grid(T, rt)) * d * 4 + 256;
+  size_t g = row_grid(T, rt);
+  const size_t g8 = t8_grid(T, static_cast<size_t>(d) * 16);
+  if (g8 > g) g = g8;
+  return g * d * 4 + 256;
 }
 
 int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w, const float* rstd,
@@ -673,6 +882,30 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
   const size_t smem = rt * d * 2 * (1 + K) + rt * d * 4 + rt * 8 * 4;
   POETX_TRY(check_rows(T, d, smem));
   if (T == 0) return POETX_OK;
+  if (use_t8_bwd(d)) {
+    const size_t tsm = static_cast<size_t>(d) * 16;
+    const unsigned g8 = t8_grid(T, tsm);
+    POETX_REQUIRE(ws_bytes >= static_cast<size_t>(g8) * d * 4, POETX_ESHAPE, "rmsnorm_gather_bwd: workspace too small");
+    cudaStream_t st = as_stream(stream);
+    float* part = static_cast<float*>(ws);
+    IdxList L{};
+    for (int k = 0; k < K; ++k) { L.idx[k] = inv[k]; L.ptr[k] = const_cast<void*>(du[k]); }
+    const auto* xb = static_cast<const __nv_bfloat16*>(x);
+    const auto* rb = static_cast<const __nv_bfloat16*>(dres);
+    auto* db = static_cast<__nv_bfloat16*>(dx);
+    switch (K) {
+      case 1: set_smem(rmsnorm_gather_bwd_t8_kernel<1>, tsm);
+              rmsnorm_gather_bwd_t8_kernel<1><<<g8, d / 8, tsm, st>>>(T, d, xb, w, rstd, L, rb, db, part); break;
+      case 2: set_smem(rmsnorm_gather_bwd_t8_kernel<2>, tsm);
+              rmsnorm_gather_bwd_t8_kernel<2><<<g8, d / 8, tsm, st>>>(T, d, xb, w, rstd, L, rb, db, part); break;
+      default: set_smem(rmsnorm_gather_bwd_t8_kernel<3>, tsm);
+               rmsnorm_gather_bwd_t8_kernel<3><<<g8, d / 8, tsm, st>>>(T, d, xb, w, rstd, L, rb, db, part); break;
+    }
+    POETX_LAUNCHED("rmsnorm_gather_bwd_t8");
+    colsum_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(g8, d, part, dw, accumulate_dw);
+    POETX_LAUNCHED("colsum");
+    return POETX_OK;
+  }
   const unsigned grid = row_grid(T, rt);
   POETX_REQUIRE(ws_bytes >= static_cast<size_t>(grid) * d * 4, POETX_ESHAPE,
                 "rmsnorm_gather_bwd: workspace too small");
