@@ -42,18 +42,28 @@ CASES = {
 
 
 def timed_steps(step, toks, warmup, steps):
+    """Median per-step device time (CUDA events around each eager step, Python
+    GC paused): eager host-side stalls (allocator, GC) show up as isolated
+    slow steps, which the median ignores."""
+    import gc
+    import statistics
+
     import torch
 
     for i in range(warmup):
         step(toks[i % len(toks)])
     torch.cuda.synchronize()
-    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    s.record()
-    for i in range(steps):
-        step(toks[i % len(toks)])
-    e.record()
-    torch.cuda.synchronize()
-    return s.elapsed_time(e) / steps
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    gc.disable()
+    try:
+        for i in range(steps):
+            ev[i][0].record()
+            step(toks[i % len(toks)])
+            ev[i][1].record()
+        torch.cuda.synchronize()
+    finally:
+        gc.enable()
+    return statistics.median(a.elapsed_time(b) for a, b in ev)
 
 
 def run_layer():
@@ -119,7 +129,7 @@ def run_model(c):
         trainable = tr.trainable
         step = lambda t: tr.step(t[:, :-1], t[:, 1:])  # noqa: E731
     static_gb = torch.cuda.memory_allocated() / 1e9
-    ms = timed_steps(step, toks, 3, 10)
+    ms = timed_steps(step, toks, 3, 15)
     return {"model": cfg.name, "variant": cfg.variant if c["kind"] == "poet" else None,
             "int8_base": bool(c.get("quantized", False)), "micro_batch": mb,
             "seq": cfg.seq, "tokens_per_step": mb * cfg.seq, "tokens_per_s": mb * cfg.seq / (ms / 1e3),
