@@ -28,9 +28,16 @@ namespace tc {
 namespace {
 
 constexpr int BD_THREADS = 256;
-constexpr int BD_STAGES = 4;
+#ifndef POETX_BD_STAGES
+#define POETX_BD_STAGES 4
+#endif
+#ifndef POETX_BD_EPI_BUFS
+#define POETX_BD_EPI_BUFS 2
+#endif
+constexpr int BD_STAGES = POETX_BD_STAGES;
+constexpr int BD_EPI_BUFS = POETX_BD_EPI_BUFS;
 constexpr int BD_A_BYTES = BM * BK * 2;          // 16 KB x tile
-constexpr int BD_EPI_BYTES = 4 * 2 * 32 * 128;   // 4 warps x 2 buffers x (32 rows x 128 B)
+constexpr int BD_EPI_BYTES = 4 * BD_EPI_BUFS * 32 * 128;  // 4 warps x buffers x (32 rows x 128 B)
 
 template <int BN> struct BdCfg {
   static constexpr int B_BYTES = BN * BN * 2;  // resident G[s]
@@ -150,7 +157,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
     }
   } else if (warp >= 4) {
     const int ew = warp - 4;
-    uint8_t* stg = epi + ew * (2 * 32 * 128);
+    uint8_t* stg = epi + ew * (BD_EPI_BUFS * 32 * 128);
     int acc = 0, buf = 0;
     uint32_t acc_phase = 0;
     for (int t = t0; t < t1; ++t) {
@@ -162,7 +169,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
         const uint32_t taddr = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * BN + c;
         tmem_ld32(taddr, r0);
         tmem_ld32(taddr + 32, r1);
-        if (lane == 0) bulk_wait_read<1>();  // staging buffer `buf` free again
+        if (lane == 0) bulk_wait_read<BD_EPI_BUFS - 1>();  // staging buffer `buf` free again
         __syncwarp();
         uint8_t* row = stg + buf * (32 * 128) + lane * 128;
 #pragma unroll
@@ -181,7 +188,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
           tma_store_2d(&map_y, stg + buf * (32 * 128), s * BN + c, t * BM + ew * 32);
           bulk_commit();
         }
-        buf ^= 1;
+        if (++buf == BD_EPI_BUFS) buf = 0;
       }
       fence_before();
       __syncwarp();

@@ -14,9 +14,22 @@ T, b = 8192, 256
 x = torch.randn((T, dim), device="cuda").bfloat16()
 y = torch.randn_like(x)
 G = P.BlockDiagonalFactor((0.1 * torch.randn((dim // b, b, b), device="cuda")).bfloat16())
-for _ in range(3):
+def run():
     if op == "apply":
         P.apply_to_features(G, x, transpose=tr)
     else:
         P.segmented_outer(x, y, b)
+
+
+for _ in range(3):
+    run()
 torch.cuda.synchronize()
+if "--time" in sys.argv:
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(50):
+        run()
+    e.record()
+    torch.cuda.synchronize()
+    us = s.elapsed_time(e) / 50 * 1e3
+    print(f"{op} dim={dim} transpose={int(tr)}: {us:.1f} us, {4 * T * dim / us / 1e3:.0f} GB/s")

@@ -42,9 +42,10 @@ CASES = {
 
 
 def timed_steps(step, toks, warmup, steps):
-    """Median per-step device time (CUDA events around each eager step, Python
-    GC paused): eager host-side stalls (allocator, GC) show up as isolated
-    slow steps, which the median ignores."""
+    """(mean, median) per-step time (CUDA events around each eager step, Python
+    GC paused).  The mean includes everything (merge steps too); eager
+    host-side stalls (allocator) show up as isolated slow steps, which the
+    median ignores."""
     import gc
     import statistics
 
@@ -63,7 +64,8 @@ def timed_steps(step, toks, warmup, steps):
         torch.cuda.synchronize()
     finally:
         gc.enable()
-    return statistics.median(a.elapsed_time(b) for a, b in ev)
+    ts = [a.elapsed_time(b) for a, b in ev]
+    return sum(ts) / len(ts), statistics.median(ts)
 
 
 def run_layer():
@@ -94,7 +96,7 @@ def run_layer():
         g = lay.backward(c, dz)
         P.adamw_step(params, {"q_r": g.q_r, "q_p": g.q_p}, st, 1e-3, sched)
 
-    ms = timed_steps(step, [None], 5, 50)
+    ms, _ = timed_steps(step, [None], 5, 50)
     ref = O.OracleLayer(base, b, lay.perm_in.forward, lay.perm_out.forward)
     xn, dzn = x.cpu().numpy(), dz.cpu().numpy()
     t0 = time.perf_counter()
@@ -129,12 +131,12 @@ def run_model(c):
         trainable = tr.trainable
         step = lambda t: tr.step(t[:, :-1], t[:, 1:])  # noqa: E731
     static_gb = torch.cuda.memory_allocated() / 1e9
-    ms = timed_steps(step, toks, 3, 15)
+    ms, med = timed_steps(step, toks, 3, 15)
     return {"model": cfg.name, "variant": cfg.variant if c["kind"] == "poet" else None,
             "int8_base": bool(c.get("quantized", False)), "micro_batch": mb,
             "seq": cfg.seq, "tokens_per_step": mb * cfg.seq, "tokens_per_s": mb * cfg.seq / (ms / 1e3),
-            "ms_per_step": ms, "peak_hbm_gb": torch.cuda.max_memory_allocated() / 1e9,
-            "static_hbm_gb": static_gb, "trainable_params": int(trainable),
+            "ms_per_step": ms, "tokens_per_s_median_step": mb * cfg.seq / (med / 1e3),
+            "peak_hbm_gb": torch.cuda.max_memory_allocated() / 1e9, "static_hbm_gb": static_gb, "trainable_params": int(trainable),
             "merge_gap": c.get("merge_gap", 0), "lora_rank": c.get("rank")}
 
 
