@@ -115,11 +115,14 @@ if args.timeline:
     overl = collections.defaultdict(float)
     by_stream = collections.defaultdict(float)
     last = t0
+    gaps = []
+    prev_end = None
     for ts, kind, ev in edges:
         dt = ts - last
         if dt > 0:
             if not active:
                 idle += dt
+                gaps.append((dt, prev_end["name"][:60] if prev_end else "-", ev["name"][:60]))
             elif len(active) == 1:
                 alone[tfam(next(iter(active.values())))] += dt
             else:
@@ -131,8 +134,13 @@ if args.timeline:
             by_stream[ev.get("tid")] += ev["dur"]
         else:
             active.pop(id(ev), None)
+            prev_end = ev
     span = (t1 - t0) / 1e3 / args.steps
     print(f"\ntimeline over {args.steps} steps: span {span:.2f} ms/step, idle (no kernel) {idle / 1e3 / args.steps:.2f} ms/step")
+    print("largest idle gaps (us: after -> before):")
+    for dt, a, b in sorted(gaps, reverse=True)[:12]:
+        print(f"  {dt:8.1f}  {a}  ->  {b}")
+    print(f"  idle gaps: {len(gaps) / args.steps:.0f} per step, median {sorted(g[0] for g in gaps)[len(gaps) // 2] if gaps else 0:.1f} us")
     print("time with ONE kernel running, by family (ms/step):")
     for f, us in sorted(alone.items(), key=lambda x: -x[1]):
         print(f"  {us / 1e3 / args.steps:8.3f}  {f}")
