@@ -23,6 +23,7 @@ namespace poetx {
 namespace {
 
 constexpr int kThreads = 256;
+constexpr int kColsumSplits = 16;  // stage-1 row splits of the RMSNorm dw column sum
 constexpr int kMaxK = 3;
 
 struct IdxList {
@@ -438,6 +439,31 @@ __global__ void __launch_bounds__(256) colsum_kernel(int64_t rows, int64_t d, co
   }
 }
 
+// stage 1 of a two-stage column sum: CTA (strip, split) sums its contiguous
+// range of rows for 32 columns into mid[split, :] (fixed order)
+__global__ void __launch_bounds__(256) colsum_split_kernel(int64_t rows, int64_t d, const float* __restrict__ part,
+                                                           float* __restrict__ mid) {
+  __shared__ float red[8][33];
+  const int wp = threadIdx.x / 32, l = threadIdx.x % 32;
+  const int64_t c = static_cast<int64_t>(blockIdx.x) * 32 + l;
+  const int64_t per = (rows + gridDim.y - 1) / gridDim.y;
+  const int64_t r0 = blockIdx.y * per, r1 = r0 + per < rows ? r0 + per : rows;
+  float acc = 0.f;
+  if (c < d)
+    for (int64_t r = r0 + wp; r < r1; r += 8) acc += part[r * d + c];
+  red[wp][l] = acc;
+  __syncthreads();
+  if (wp == 0 && c < d) {
+    float t = 0.f;
+    for (int k = 0; k < 8; ++k) t += red[k][l];
+    mid[static_cast<int64_t>(blockIdx.y) * d + c] = t;
+  }
+}
+
+// dw (+)= column sums of the [rows, d] per-CTA partials: two stages so the
+// reduction spreads over (d / 32) x kColsumSplits CTAs
+int colsum2(int64_t rows, int64_t d, const float* part, float* mid, float* out, int accumulate, cudaStream_t st);
+
 template <int RT>
 __global__ void __launch_bounds__(kThreads) swiglu_gather_kernel(
     int64_t T, int f, const __nv_bfloat16* __restrict__ vg, const __nv_bfloat16* __restrict__ vu,
@@ -793,6 +819,16 @@ void set_smem(K kernel, size_t smem) {
   if (smem > 48 * 1024) cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
 }
 
+int colsum2(int64_t rows, int64_t d, const float* part, float* mid, float* out, int accumulate, cudaStream_t st) {
+  const int splits = static_cast<int>(rows < kColsumSplits ? (rows > 0 ? rows : 1) : kColsumSplits);
+  const unsigned strips = static_cast<unsigned>((d + 31) / 32);
+  colsum_split_kernel<<<dim3(strips, splits), 256, 0, st>>>(rows, d, part, mid);
+  POETX_LAUNCHED("colsum_split");
+  colsum_kernel<<<strips, 256, 0, st>>>(splits, d, mid, out, accumulate);
+  POETX_LAUNCHED("colsum");
+  return POETX_OK;
+}
+
 // feature-major 8-token RMSNorm kernels: one thread per 8-column vector, so
 // d / 8 must be a whole number of warps within a CTA (env POETX_ROW_T8=0 off)
 bool use_t8(int64_t d) {
@@ -868,7 +904,7 @@ size_t poetx_rmsnorm_gather_bwd_workspace_bytes(int64_t T, int64_t d) {
   size_t g = row_grid(T, rt);
   const size_t g8 = t8_grid(T, static_cast<size_t>(d) * 16);
   if (g8 > g) g = g8;
-  return g * d * 4 + 256;
+  return (g + kColsumSplits) * d * 4 + 256;
 }
 
 int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w, const float* rstd,
@@ -885,7 +921,8 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
   if (use_t8_bwd(d)) {
     const size_t tsm = static_cast<size_t>(d) * 16;
     const unsigned g8 = t8_grid(T, tsm);
-    POETX_REQUIRE(ws_bytes >= static_cast<size_t>(g8) * d * 4, POETX_ESHAPE, "rmsnorm_gather_bwd: workspace too small");
+    POETX_REQUIRE(ws_bytes >= static_cast<size_t>(g8 + kColsumSplits) * d * 4, POETX_ESHAPE,
+                  "rmsnorm_gather_bwd: workspace too small");
     cudaStream_t st = as_stream(stream);
     float* part = static_cast<float*>(ws);
     IdxList L{};
@@ -902,12 +939,11 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
                rmsnorm_gather_bwd_t8_kernel<3><<<g8, d / 8, tsm, st>>>(T, d, xb, w, rstd, L, rb, db, part); break;
     }
     POETX_LAUNCHED("rmsnorm_gather_bwd_t8");
-    colsum_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(g8, d, part, dw, accumulate_dw);
-    POETX_LAUNCHED("colsum");
+    POETX_TRY(colsum2(g8, d, part, part + static_cast<size_t>(g8) * d, dw, accumulate_dw, st));
     return POETX_OK;
   }
   const unsigned grid = row_grid(T, rt);
-  POETX_REQUIRE(ws_bytes >= static_cast<size_t>(grid) * d * 4, POETX_ESHAPE,
+  POETX_REQUIRE(ws_bytes >= static_cast<size_t>(grid + kColsumSplits) * d * 4, POETX_ESHAPE,
                 "rmsnorm_gather_bwd: workspace too small");
   cudaStream_t st = as_stream(stream);
   float* part = static_cast<float*>(ws);
@@ -918,8 +954,7 @@ int poetx_rmsnorm_gather_bwd(int64_t T, int64_t d, const void* x, const float* w
                                                    L, static_cast<const __nv_bfloat16*>(dres),
                                                    static_cast<__nv_bfloat16*>(dx), part);)
   POETX_LAUNCHED("rmsnorm_gather_bwd");
-  colsum_kernel<<<static_cast<unsigned>((d + 31) / 32), 256, 0, st>>>(grid, d, part, dw, accumulate_dw);
-  POETX_LAUNCHED("colsum");
+  POETX_TRY(colsum2(grid, d, part, part + static_cast<size_t>(grid) * d, dw, accumulate_dw, st));
   return POETX_OK;
 }
 
