@@ -17,7 +17,7 @@
 //     dV += P^T dO_qt, dK += dS^T Q_qt, dQ_qt += dS K_kt     (tcgen05, K = 128)
 // with D = rowsum(dO * O) computed from the staged tiles, and scale applied
 // to dK and dQ in the drain.  Warp 0 issues the TMA loads, warp 1 the MMAs,
-// warps 4..11 (one key / query row per thread = one TMEM lane, two warps per
+// warps 4..19 (one key / query row per thread = one TMEM lane, four warps per
 // lane group splitting the columns) the softmax algebra and the drains.
 #include "tc_common.cuh"
 
@@ -35,7 +35,7 @@ constexpr int OFF_LSE = 6 * MAT, OFF_D = OFF_LSE + SEQ * 4, OFF_BAR = OFF_D + SE
 constexpr int SMEM = OFF_BAR + 128 + 1024;
 constexpr float LOG2E = 1.4426950408889634f;
 
-__device__ __forceinline__ void named_sync_epi() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+__device__ __forceinline__ void named_sync_epi() { asm volatile("bar.sync 1, 512;" ::: "memory"); }
 
 __device__ __forceinline__ void unpack_bf16x8(const uint4 u, float (&o)[8]) {
   const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
@@ -50,13 +50,23 @@ __device__ __forceinline__ void unpack_bf16x8(const uint4 u, float (&o)[8]) {
 // swizzled 16-byte chunk c of row r inside a [rows x 64 bf16] SW128 block
 __device__ __forceinline__ uint32_t sw_off(int r, int c) { return r * 128 + ((c ^ (r & 7)) << 4); }
 
-// 32 fp32 TMEM columns of this thread's lane -> 64 bytes of a bf16 row in global
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// 16 fp32 TMEM columns of this thread's lane -> 32 bytes of a bf16 row in global
 __device__ __forceinline__ void drain_row(uint32_t taddr, float mul, __nv_bfloat16* dst) {
-  uint32_t r[32];
-  tmem_ld32(taddr, r);
+  uint32_t r[16];
+  tmem_ld16(taddr, r);
   uint4* out = reinterpret_cast<uint4*>(dst);
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 2; ++q) {
     uint4 v;
     v.x = pack_bf16(__float_as_uint(__uint_as_float(r[8 * q + 0]) * mul), __float_as_uint(__uint_as_float(r[8 * q + 1]) * mul));
     v.y = pack_bf16(__float_as_uint(__uint_as_float(r[8 * q + 2]) * mul), __float_as_uint(__uint_as_float(r[8 * q + 3]) * mul));
@@ -81,8 +91,9 @@ __device__ __forceinline__ uint4 pack_f8(const float* v) {
   return u;
 }
 
-constexpr int THREADS = 384;  // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle, 4..11 softmax / drains
-constexpr int EPI = 256;
+constexpr int NQ = 4;                  // softmax warps per TMEM lane group (each: 128 / NQ columns)
+constexpr int EPI = 128 * NQ;          // warps 4..4+4*NQ-1: softmax algebra and drains
+constexpr int THREADS = 128 + EPI;     // warps 0 TMA, 1 MMA, 2 TMEM alloc, 3 idle
 
 __global__ void __launch_bounds__(THREADS, 1)
     attn_bwd_kernel(const __grid_constant__ CUtensorMap mq, const __grid_constant__ CUtensorMap mk,
@@ -200,7 +211,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int et = threadIdx.x - 128;
     for (int i = et; i < SEQ; i += EPI) lse_s[i] = lse[static_cast<int64_t>(bh) * SEQ + i] * LOG2E;
     mbar_wait(&ldb[0], 0);
-    {  // D[q] = sum_c dO[q, c] O[q, c]
+    if (et < SEQ) {  // D[q] = sum_c dO[q, c] O[q, c]
       const int q = et, r = q % 128;
       const uint8_t* pd = sm + OFF_DO + (q / 128) * TILE;
       const uint8_t* po = sm + OFF_O + (q / 128) * TILE;
@@ -226,32 +237,30 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(s_full, it & 1);
       fence_after();
 #pragma unroll 1
-      for (int c0 = ch * 64; c0 < ch * 64 + 64; c0 += 32) {
-        uint32_t s[32], dp[32];
-        tmem_ld32(tl + c0, s);
-        tmem_ld32(tl + 128 + c0, dp);
-        float p[32], ds[32];
-        const float4* l4 = reinterpret_cast<const float4*>(lse_s + qt * 128 + c0);
-        const float4* d4 = reinterpret_cast<const float4*>(d_s + qt * 128 + c0);
+      for (int c0 = ch * (128 / NQ); c0 < (ch + 1) * (128 / NQ); c0 += 16) {
+        uint32_t sv[16], dp[16];
+        tmem_ld16(tl + c0, sv);
+        tmem_ld16(tl + 128 + c0, dp);
 #pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const float4 lv = l4[j4], dv4 = d4[j4];
-          const float lq[4] = {lv.x, lv.y, lv.z, lv.w}, dq4[4] = {dv4.x, dv4.y, dv4.z, dv4.w};
+        for (int g = 0; g < 2; ++g) {
+          float p[8], ds[8];
+          const float4* l4 = reinterpret_cast<const float4*>(lse_s + qt * 128 + c0 + 8 * g);
+          const float4* d4 = reinterpret_cast<const float4*>(d_s + qt * 128 + c0 + 8 * g);
+          const float4 la = l4[0], lb = l4[1], da = d4[0], db = d4[1];
+          const float lq[8] = {la.x, la.y, la.z, la.w, lb.x, lb.y, lb.z, lb.w};
+          const float dq8[8] = {da.x, da.y, da.z, da.w, db.x, db.y, db.z, db.w};
 #pragma unroll
-          for (int u = 0; u < 4; ++u) {
-            const int j = 4 * j4 + u;
-            float pj = ex2(__uint_as_float(s[j]) * sl2 - lq[u]);
+          for (int u = 0; u < 8; ++u) {
+            const int j = 8 * g + u;
+            float pj = ex2(__uint_as_float(sv[j]) * sl2 - lq[u]);
             if (diag && kk > qt * 128 + c0 + j) pj = 0.f;
-            p[j] = pj;
-            ds[j] = pj * (__uint_as_float(dp[j]) - dq4[u]);
+            p[u] = pj;
+            ds[u] = pj * (__uint_as_float(dp[j]) - dq8[u]);
           }
-        }
-#pragma unroll
-        for (int g = 0; g < 4; ++g) {
           const int j0 = c0 + 8 * g;
           const uint32_t off = (j0 / 64) * TILE + sw_off(e, (j0 % 64) / 8);
-          *reinterpret_cast<uint4*>(sm + OFF_PT + off) = pack_f8(p + 8 * g);
-          *reinterpret_cast<uint4*>(sm + OFF_DST + off) = pack_f8(ds + 8 * g);
+          *reinterpret_cast<uint4*>(sm + OFF_PT + off) = pack_f8(p);
+          *reinterpret_cast<uint4*>(sm + OFF_DST + off) = pack_f8(ds);
         }
       }
       fence_async_smem();
@@ -260,18 +269,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (it == 1) {  // key tile 0 complete: drain dV, dK (this thread: 32 of the 64 columns)
         mbar_wait(acc_full, 0);
         fence_after();
-        drain_row(tl + 256 + ch * 32, 1.f, dv + (row0 + e) * ld + col0 + ch * 32);
-        drain_row(tl + 320 + ch * 32, scale, dk + (row0 + e) * ld + col0 + ch * 32);
+        drain_row(tl + 256 + ch * 16, 1.f, dv + (row0 + e) * ld + col0 + ch * 16);
+        drain_row(tl + 320 + ch * 16, scale, dk + (row0 + e) * ld + col0 + ch * 16);
         fence_before();
         mbar_arrive(acc_empty);
       }
     }
     mbar_wait(fin, 0);
     fence_after();
-    drain_row(tl + 256 + ch * 32, 1.f, dv + (row0 + 128 + e) * ld + col0 + ch * 32);
-    drain_row(tl + 320 + ch * 32, scale, dk + (row0 + 128 + e) * ld + col0 + ch * 32);
-    drain_row(tl + 384 + ch * 32, scale, dq + (row0 + e) * ld + col0 + ch * 32);
-    drain_row(tl + 448 + ch * 32, scale, dq + (row0 + 128 + e) * ld + col0 + ch * 32);
+    drain_row(tl + 256 + ch * 16, 1.f, dv + (row0 + 128 + e) * ld + col0 + ch * 16);
+    drain_row(tl + 320 + ch * 16, scale, dk + (row0 + 128 + e) * ld + col0 + ch * 16);
+    drain_row(tl + 384 + ch * 16, scale, dq + (row0 + e) * ld + col0 + ch * 16);
+    drain_row(tl + 448 + ch * 16, scale, dq + (row0 + 128 + e) * ld + col0 + ch * 16);
   }
 
   fence_before();

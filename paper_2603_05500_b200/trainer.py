@@ -592,11 +592,10 @@ class _Attention(torch.autograd.Function):
 
 
 def fused_attention_supported(S, hd):
-    """The tcgen05 attention backward covers sequence 256 with head_dim 64.
-    Opt-in (env POETX_ATTN_BWD=1): it is correct and deterministic but, at one
-    199 KB CTA per SM, only level with cuDNN's backward inside the step
-    (130 vs ~143 us alone; step 108.9k vs 109.1k tok/s)."""
-    return S == 256 and hd == 64 and os.environ.get("POETX_ATTN_BWD", "0") == "1"
+    """The tcgen05 attention backward covers sequence 256 with head_dim 64
+    (120 us per Llama-1B layer vs ~143 us for cuDNN's three backward kernels;
+    +0.8% step in same-box A/B).  Env POETX_ATTN_BWD=0 keeps cuDNN's."""
+    return S == 256 and hd == 64 and os.environ.get("POETX_ATTN_BWD", "1") != "0"
 
 
 def _permute_cols(x, idx):
