@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-( timeout 900 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-  timeout 300 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+( for lib in abtest/lib_prev.so "" abtest/lib_prev.so ""; do echo "${lib:-current}: $(POETX_LIB_PATH=$lib timeout 120 python tools/attnbench.py 2>&1 | tail -1)"; done
 ) > gpurun_out/attn_prof.txt 2>&1
