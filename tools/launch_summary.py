@@ -12,7 +12,7 @@ FAMILIES = [
     ("colsum", "rmsnorm+gather"), ("swiglu", "swiglu+gather"), ("rope", "rope+scatter"),
     ("scatter_add", "residual scatter"), ("permute", "permute"), ("unpack_q", "CNP glue"), ("combine_fwd", "CNP glue"),
     ("bwd_prep", "CNP glue"), ("pack_dq", "CNP glue"), ("to_bf16", "CNP glue"), ("adamw", "AdamW+norm"),
-    ("sqdev", "AdamW+norm"), ("sdpa", "attention (cuDNN)"), ("cudnn", "attention (cuDNN)"),
+    ("sqdev", "AdamW+norm"), ("sdpa", "attention"), ("cudnn", "attention"), ("attn_bwd", "attention"),
     ("nvjet", "lm_head GEMMs (cuBLAS)"), ("ce_fwd", "cross-entropy"), ("ce_bwd", "cross-entropy"),
     ("dequant", "POET-XQ"), ("quant", "POET-XQ"),
 ]

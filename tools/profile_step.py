@@ -36,7 +36,7 @@ FAMILIES = [
     ("unpack_q", "CNP glue"), ("combine_fwd", "CNP glue"), ("bwd_prep", "CNP glue"), ("pack_dq", "CNP glue"),
     ("to_bf16", "CNP glue"),
     ("adamw", "AdamW+norm"), ("sqdev", "AdamW+norm"),
-    ("sdpa", "attention (cuDNN)"), ("cudnn", "attention (cuDNN)"),
+    ("sdpa", "attention"), ("cudnn", "attention"), ("attn_bwd", "attention"),
     ("nvjet", "lm_head GEMMs (cuBLAS)"), ("SoftMax", "cross-entropy"), ("ce_fwd", "cross-entropy"),
     ("ce_bwd", "cross-entropy"), ("quantize", "POET-XQ"), ("dequant", "POET-XQ"),
 ]
