@@ -222,7 +222,7 @@ class PoetLinearLayer:
         d.m, d.n, d.b = self.m, self.n, self.block_size
         d.perm_in_fwd, d.perm_in_inv = fi.data_ptr(), ii.data_ptr()
         d.perm_out_fwd, d.perm_out_inv = fo.data_ptr(), io.data_ptr()
-        d.fold_weight = 1
+        d.fold_weight = int(getattr(self, "fold_weight", True))
         if self.quantized:
             d.premerged = None
             d.pm_codes = self.premerged.codes.data_ptr()

@@ -321,12 +321,15 @@ def test_merge_sv_drift(P):
     (512, 512, 64, 1024, "fast", False), (256, 768, 128, 512, "fast", False), (1024, 512, 256, 384, "fast", False),
     (512, 768, 256, 77, "fast", False), (768, 512, 256, 300, "mem", False), (512, 1024, 256, 130, "mem", True),
     (256, 256, 64, 33, "mem", True)])
-def test_bf16_layer_vs_oracle(P, m, n, b, T, variant, quant):
-    """bf16 layer (tensor-core path: weight-folded block factors, CTA-pair
-    GEMMs; ragged T; mem variant; int8 base) against the float64 oracle."""
+@pytest.mark.parametrize("fold", [True, False], ids=["weight_folded", "activation_side"])
+def test_bf16_layer_vs_oracle(P, m, n, b, T, variant, quant, fold):
+    """bf16 layer (tensor-core path: block factors folded into the weight or
+    applied to the activations, CTA-pair GEMMs; ragged T; mem variant; int8
+    base) against the float64 oracle."""
     r = np.random.default_rng(m + n + T)
     base = (r.standard_normal((m, n)) / np.sqrt(m))
     layer = P.PoetLinearLayer(torch.from_numpy(base).to(torch.bfloat16), b, P.Rng(5), variant=variant)
+    layer.fold_weight = fold
     if quant:
         layer.quantize_base()
         base_q = layer.base.dequantize().double().cpu().numpy()  # the int8 weight the GPU holds
