@@ -293,6 +293,16 @@ int poetx_cross_entropy_fwd(int64_t T, int64_t V, const void* logits, const int6
 int poetx_cross_entropy_bwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, const float* row_max,
                             const float* row_sumexp, const float* dloss, float scale, void* dlogits, void* stream);
 
+/* ------------------------------------------------------------ embedding --
+ * The trainer's token embedding (model plumbing): out[t] = bf16(table[tok[t]])
+ * (fp32 table [V, d]); backward: dtable[v] += sum_{tok[t] = v} dh[t] over the
+ * tokens sorted stably by id (sorted_tokens, order = the sort's permutation),
+ * one warp per id in ascending position order -- deterministic, no atomics. */
+int poetx_embedding_fwd(int64_t T, int64_t V, int64_t d, const int64_t* tokens, const float* table, void* out,
+                        void* stream);
+int poetx_embedding_bwd(int64_t T, int64_t d, const int64_t* sorted_tokens, const int64_t* order, const void* dh,
+                        float* dtable, void* stream);
+
 /* ---------------------------------------------------- singular values --
  * svd_singular_values (linalg.py:166-218): one-sided Jacobi in float64,
  * same rotation and stopping rule (tol relative to sqrt(alpha beta), stop

@@ -115,6 +115,8 @@ _SIGS = {
     "poetx_cross_entropy_bwd": (I32, [I64, I64, VP, VP, VP, VP, VP, C.c_float, VP, VP]),
     "poetx_attention_bwd": (I32, [I64, I64, I64, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP]),
     "poetx_singular_values_workspace_bytes": (SZ, [I64, I64, I64]),
+    "poetx_embedding_fwd": (I32, [I64, I64, I64, VP, VP, VP, VP]),
+    "poetx_embedding_bwd": (I32, [I64, I64, VP, VP, VP, VP, VP]),
     "poetx_singular_values": (I32, [I64, I64, I64, VP, VP, C.c_double, I32, VP, VP, VP, SZ, VP]),
     "poetx_orthogonality_error": (I32, [I32, I64, I64, VP, VP, VP, SZ, VP]),
     "poetx_permute_cols": (I32, [I32, I64, I64, VP, VP, VP, VP]),

@@ -695,6 +695,55 @@ __global__ void __launch_bounds__(kThreads) scatter_add_kernel(
 }
 
 
+// Token embedding of the trainer (fp32 table, bf16 activations):
+//   forward   out[t, :] = bf16(table[tok[t], :])            (gather + cast in one pass)
+//   backward  dtable[v, :] += sum over t with tok[t] = v of dh[t, :]
+// The backward walks the tokens sorted by id (stable, so positions ascend
+// within an id): one warp per run of equal ids sums its rows in fp32 in that
+// fixed order and adds the total into the table gradient -- every row is
+// written by exactly one warp, no atomics, deterministic.
+__global__ void __launch_bounds__(256) embedding_fwd_kernel(int64_t T, int64_t d, const int64_t* __restrict__ tok,
+                                                            const float* __restrict__ table,
+                                                            __nv_bfloat16* __restrict__ out) {
+  const int64_t nv = d / 8;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < T * nv;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t t = i / nv, c = i % nv;
+    const float4* src = reinterpret_cast<const float4*>(table + tok[t] * d) + 2 * c;
+    const float4 a = __ldg(src), b = __ldg(src + 1);
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    reinterpret_cast<uint4*>(out + t * d)[c] = pack8(v);
+  }
+}
+
+__global__ void __launch_bounds__(256) embedding_bwd_kernel(int64_t T, int64_t d, const int64_t* __restrict__ sorted_tok,
+                                                            const int64_t* __restrict__ order,
+                                                            const __nv_bfloat16* __restrict__ dh,
+                                                            float* __restrict__ dtable) {
+  const int lane = threadIdx.x % 32;
+  const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32;
+  if (j >= T) return;
+  const int64_t id = sorted_tok[j];
+  if (j > 0 && sorted_tok[j - 1] == id) return;  // not the start of a run
+  int64_t end = j + 1;
+  while (end < T && sorted_tok[end] == id) ++end;
+  for (int64_t c0 = 8 * lane; c0 < d; c0 += 256) {  // 8 columns per lane per chunk
+    float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    for (int64_t k = j; k < end; ++k) {
+      float v[8];
+      unpack8(__ldg(reinterpret_cast<const uint4*>(dh + order[k] * d + c0)), v);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] += v[q];
+    }
+    float4* dst = reinterpret_cast<float4*>(dtable + id * d + c0);
+    float4 a = dst[0], b = dst[1];
+    a.x += acc[0]; a.y += acc[1]; a.z += acc[2]; a.w += acc[3];
+    b.x += acc[4]; b.y += acc[5]; b.z += acc[6]; b.w += acc[7];
+    dst[0] = a;
+    dst[1] = b;
+  }
+}
+
 // Cross-entropy over bf16 logits (the trainer's loss head), fused: the
 // forward streams each row once with an online max / sum-exp (fp32) and
 // keeps (max, sum) per row; the backward streams the row again and writes
@@ -1056,6 +1105,32 @@ int poetx_cross_entropy_bwd(int64_t T, int64_t V, const void* logits, const int6
       T, static_cast<int>(V), static_cast<const __nv_bfloat16*>(logits), targets, row_max, row_sumexp, dloss, scale,
       static_cast<__nv_bfloat16*>(dlogits));
   POETX_LAUNCHED("cross_entropy_bwd");
+  return POETX_OK;
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int poetx_embedding_fwd(int64_t T, int64_t V, int64_t d, const int64_t* tokens, const float* table, void* out,
+                        void* stream) {
+  POETX_REQUIRE(T >= 0 && V > 0 && d > 0 && d % 8 == 0, POETX_ESHAPE, "embedding_fwd: d %% 8 == 0 required");
+  if (T == 0) return POETX_OK;
+  const int64_t work = T * (d / 8);
+  const unsigned grid = static_cast<unsigned>(work / 256 + 1 < 148 * 16 ? work / 256 + 1 : 148 * 16);
+  embedding_fwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(T, d, tokens, table, static_cast<__nv_bfloat16*>(out));
+  POETX_LAUNCHED("embedding_fwd");
+  return POETX_OK;
+}
+
+int poetx_embedding_bwd(int64_t T, int64_t d, const int64_t* sorted_tokens, const int64_t* order, const void* dh,
+                        float* dtable, void* stream) {
+  POETX_REQUIRE(T >= 0 && d > 0 && d % 8 == 0, POETX_ESHAPE, "embedding_bwd: d %% 8 == 0 required");
+  if (T == 0) return POETX_OK;
+  const unsigned grid = static_cast<unsigned>((T + 7) / 8);
+  embedding_bwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(T, d, sorted_tokens, order,
+                                                            static_cast<const __nv_bfloat16*>(dh), dtable);
+  POETX_LAUNCHED("embedding_bwd");
   return POETX_OK;
 }
 

@@ -539,6 +539,32 @@ class _RopeScatter(torch.autograd.Function):
         return dv, None, None, None, None, None, None, None
 
 
+class _Embedding(torch.autograd.Function):
+    """h = bf16(table[tokens]) (fp32 table); the backward adds the table
+    gradient straight into ``grad_view`` (the flat dense grad buffer) with the
+    deterministic sorted-run kernel and returns no gradient for the table."""
+
+    @staticmethod
+    def forward(ctx, tokens, table, grad_view):
+        T, (V, d) = tokens.numel(), table.shape
+        tok = tokens.reshape(-1).contiguous()
+        out = torch.empty((T, d), dtype=torch.bfloat16, device=table.device)
+        N.call("poetx_embedding_fwd", T, V, d, tok.data_ptr(), table.data_ptr(), out.data_ptr(),
+               N.stream_ptr(table.device))
+        ctx.save_for_backward(tok)
+        ctx.grad_view = grad_view
+        return out
+
+    @staticmethod
+    def backward(ctx, dh):
+        (tok,) = ctx.saved_tensors
+        dh = dh.contiguous()
+        srt, order = torch.sort(tok, stable=True)
+        N.call("poetx_embedding_bwd", tok.numel(), dh.shape[1], srt.data_ptr(), order.data_ptr(), dh.data_ptr(),
+               ctx.grad_view.data_ptr(), N.stream_ptr(dh.device))
+        return None, None, None
+
+
 class _CrossEntropy(torch.autograd.Function):
     """mean_t CE(logits[t], target[t]) over bf16 logits, fused (model_ops.cu)."""
 
@@ -797,7 +823,10 @@ class PoetLlama(torch.nn.Module):
         B, S = tokens.shape
         d, H, hd = cfg.d, cfg.heads, cfg.head_dim
         embed = self.dense_param("embed", (cfg.vocab, d)).detach().requires_grad_(True)
-        h = F.embedding(tokens.reshape(-1), embed).to(torch.bfloat16)
+        if self.fused and os.environ.get("POETX_FUSED_EMBED", "1") != "0":  # table grad added in place
+            h = _Embedding.apply(tokens, embed, self.dense.view(self.dense.grad, "embed", (cfg.vocab, d)))
+        else:
+            h = F.embedding(tokens.reshape(-1), embed).to(torch.bfloat16)
         cos, sin = self.cos[:S].view(1, S, 1, hd // 2), self.sin[:S].view(1, S, 1, hd // 2)
         leaves = [embed]
         pipe = self.cnp_pipelined and self.fused
@@ -916,9 +945,10 @@ class PoetLlama(torch.nn.Module):
     def backward_dense_grads(self, loss):
         """Backprop; dense grads land in the flat dense grad buffer."""
         names = ["embed"] + [f"{i}.norm{j}" for i in range(self.cfg.layers) for j in (1, 2)] + ["norm_f", "head"]
-        grads = torch.autograd.grad(loss, self._leaves)
+        grads = torch.autograd.grad(loss, self._leaves, allow_unused=True)
         for name, g in zip(names, grads):
-            self.dense.view(self.dense.grad, name, g.shape).add_(g)
+            if g is not None:  # None: written in place by its backward (the fused embedding)
+                self.dense.view(self.dense.grad, name, g.shape).add_(g)
 
 
 def weight_folding_pays(cfg: LlamaConfig, micro_batch: int) -> bool:

@@ -149,3 +149,29 @@ def test_fused_cross_entropy(N, T, V):
     (2.0 * loss).backward()
     (2.0 * ref).backward()
     _close(a.grad, r.grad, 1e-2)
+
+
+@pytest.mark.parametrize("T,V,d", [(8192, 32000, 2048), (300, 50, 512), (7, 3, 256)])
+def test_embedding_fwd_bwd(N, T, V, d):
+    """Fused embedding (gather + bf16 cast; sorted-run table gradient added in
+    place) against F.embedding in fp32; repeated tokens included."""
+    from paper_2603_05500_b200.trainer import _Embedding
+
+    g = torch.Generator().manual_seed(T + V)
+    tok = torch.randint(0, V, (T,), generator=g).cuda()
+    table = torch.randn(V, d, generator=g).cuda()
+    gbuf = torch.randn(V, d, generator=g).cuda()  # accumulates onto existing content
+    base = gbuf.clone()
+    t = table.clone().requires_grad_(True)
+    out = _Embedding.apply(tok, t, gbuf)
+    ref = torch.nn.functional.embedding(tok, table)
+    assert torch.equal(out, ref.to(torch.bfloat16))
+    dh = _bf(torch.randn(T, d, generator=g)).cuda()
+    out.backward(dh)
+    tr = table.clone().requires_grad_(True)
+    torch.nn.functional.embedding(tok, tr).backward(dh.float())
+    _close(gbuf - base, tr.grad, 1e-5)
+    first = gbuf.clone()
+    gbuf.copy_(base)
+    _Embedding.apply(tok, t, gbuf).backward(dh)
+    assert torch.equal(gbuf, first)  # deterministic: bitwise the same result again
