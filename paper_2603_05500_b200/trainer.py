@@ -463,13 +463,14 @@ class _RMSNormGather(torch.autograd.Function):
     """y = rmsnorm(h) * w, then u_k = y[:, pi_in_k] for each consumer."""
 
     @staticmethod
-    def forward(ctx, h, w, fwds, invs):
+    def forward(ctx, h, w, fwds, invs, dw_into=None):
         T, d = h.shape
         outs = [torch.empty_like(h) for _ in fwds]
         rstd = torch.empty(T, dtype=torch.float32, device=h.device)
         N.call("poetx_rmsnorm_gather", T, d, h.data_ptr(), w.data_ptr(), 1e-6, len(fwds), _ptrs(fwds),
                _ptrs(outs), rstd.data_ptr(), N.stream_ptr(h.device))
         ctx.invs = invs
+        ctx.dw_into = dw_into  # the gain's gradient is accumulated here in-kernel (else returned)
         ctx.save_for_backward(h, w, rstd)
         # h is also passed through (the residual stream), so its gradient comes
         # back here and is added inside the fused backward kernel
@@ -483,12 +484,13 @@ class _RMSNormGather(torch.autograd.Function):
         dus = [g.contiguous() for g in dus]
         dres = None if dres is None else dres.contiguous()
         dx = torch.empty_like(h)
-        dw = torch.empty_like(w)
+        into = ctx.dw_into is not None
+        dw = ctx.dw_into if into else torch.empty_like(w)
         ws, wsb = N.workspace(N.lib().poetx_rmsnorm_gather_bwd_workspace_bytes(T, d), h.device)
         N.call("poetx_rmsnorm_gather_bwd", T, d, h.data_ptr(), w.data_ptr(), rstd.data_ptr(), len(dus),
-               _ptrs(ctx.invs), _ptrs(dus), N.ptr(dres), dx.data_ptr(), dw.data_ptr(), 0, ws, wsb,
+               _ptrs(ctx.invs), _ptrs(dus), N.ptr(dres), dx.data_ptr(), dw.data_ptr(), int(into), ws, wsb,
                N.stream_ptr(h.device))
-        return dx, dw, None, None
+        return dx, (None if into else dw), None, None, None
 
 
 class _SwiGLUGather(torch.autograd.Function):
@@ -818,6 +820,13 @@ class PoetLlama(torch.nn.Module):
     def dense_param(self, name, shape):
         return self.dense.view(self.dense.param, name, shape)
 
+    def dense_grad_view(self, name, d):
+        """A gain's slice of the flat dense grad buffer, for kernels that
+        accumulate into it in place (env POETX_FUSED_EMBED=0 returns grads)."""
+        if os.environ.get("POETX_FUSED_EMBED", "1") == "0":
+            return None
+        return self.dense.view(self.dense.grad, name, (d,))
+
     def forward(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
         cfg = self.cfg
         B, S = tokens.shape
@@ -912,7 +921,7 @@ class PoetLlama(torch.nn.Module):
         h_in, n1d = h.detach(), n1.detach()
         rg = lambda mod: (lambda: _rmsnorm_regather(h_in, n1d, pin(mod)[0]))  # noqa: E731
         uq, uk, uv, h = _RMSNormGather.apply(h, n1, [pin(q)[0], pin(k)[0], pin(v)[0]],
-                                          [pin(q)[1], pin(k)[1], pin(v)[1]])
+                                          [pin(q)[1], pin(k)[1], pin(v)[1]], self.dense_grad_view(f"{i}.norm1", d))
         qr, kr, vz = self._branches([
             lambda: _RopeScatter.apply(_PoetRawFn.apply(uq, q, rg(q)), pout(q)[1], pout(q)[0], self.cos32,
                                        self.sin32, S, H, hd),
@@ -933,7 +942,8 @@ class PoetLlama(torch.nn.Module):
         h = _ScatterAdd.apply(h, _PoetRawFn.apply(uo, o, regen_o), pout(o)[1], pout(o)[0])
         h2_in, n2d = h.detach(), n2.detach()
         rg2 = lambda mod: (lambda: _rmsnorm_regather(h2_in, n2d, pin(mod)[0]))  # noqa: E731
-        ug, uu, h = _RMSNormGather.apply(h, n2, [pin(gate)[0], pin(up)[0]], [pin(gate)[1], pin(up)[1]])
+        ug, uu, h = _RMSNormGather.apply(h, n2, [pin(gate)[0], pin(up)[0]], [pin(gate)[1], pin(up)[1]],
+                                         self.dense_grad_view(f"{i}.norm2", d))
         vg, vu = self._branches([lambda: _PoetRawFn.apply(ug, gate, rg2(gate)),
                                  lambda: _PoetRawFn.apply(uu, up, rg2(up))])
         ud = _SwiGLUGather.apply(vg, vu, self.swiglu_maps[i])
