@@ -357,7 +357,11 @@ constexpr int A_B = HALF * BK * 2;              // 16 KB
 constexpr int B_B = HALF * BK * 2;              // 16 KB
 constexpr int STAGE = A_B + B_B;
 constexpr int EPI = 4 * 2 * 32 * 128;
-constexpr int STAGES = (227 * 1024 - EPI - 2048) / STAGE > 8 ? 8 : (227 * 1024 - EPI - 2048) / STAGE;
+#ifndef POETX_PAIR_STAGES
+#define POETX_PAIR_STAGES 8
+#endif
+constexpr int STAGES_FIT = (227 * 1024 - EPI - 2048) / STAGE;
+constexpr int STAGES = STAGES_FIT > POETX_PAIR_STAGES ? POETX_PAIR_STAGES : STAGES_FIT;  // 6 by default
 constexpr int SMEM = STAGES * STAGE + EPI + 1024 + 256;
 template <bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
