@@ -576,9 +576,24 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   return fn;
 }
 
+// cuTensorMapEncodeTiled is a driver call: make sure the calling thread has
+// the device's primary context current (autograd's backward worker threads
+// may not have touched the runtime yet; tools such as ncu / compute-sanitizer
+// then reject the encode with CUDA_ERROR_INVALID_CONTEXT)
+static void ensure_context() {
+  thread_local bool done = false;
+  if (!done) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaSetDevice(dev);
+    done = true;
+  }
+}
+
 // 2-D bf16 tensor map over a row-major [rows, cols] view with row pitch
 int make_map(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
              uint32_t box_cols, uint32_t box_rows) {
+  ensure_context();
   auto fn = encode_fn();
   POETX_REQUIRE(fn != nullptr, POETX_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};
@@ -594,6 +609,7 @@ int make_map(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, u
 
 int make_map_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
                  uint32_t box_cols, uint32_t box_rows) {
+  ensure_context();
   auto fn = encode_fn();
   POETX_REQUIRE(fn != nullptr, POETX_ECUDA, "cuTensorMapEncodeTiled unavailable");
   cuuint64_t dims[2] = {cols, rows};

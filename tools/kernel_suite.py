@@ -3,6 +3,11 @@ tokens, b = 256), each preceded by NVTX-free warm-up, as an ncu target:
 
     ncu --set full -o gpurun_out/suite python tools/kernel_suite.py
     python tools/kernel_suite.py --summary gpurun_out/suite.ncu-rep > profiles/r01/ncu_kernels.md
+or, without a (large) report file:
+    ncu --csv --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,\
+        sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed --log-file suite.csv \
+        python tools/kernel_suite.py
+    python tools/kernel_suite.py --summary suite.csv
 
 The summary converts each kernel's ncu duration into achieved TFLOP/s or
 GB/s from its ALGORITHMIC work and divides by the measured
@@ -40,6 +45,9 @@ PLAN = [
     ("adamw_kernel", "AdamW + clip (120.6M params)", "bytes", 120.64e6 * 28),
     ("swiglu_gather_bwd", "SwiGLU+gathers backward (T x 5632)", "bytes", 5.0 * T * f * 2),
     ("rmsnorm_gather_bwd", "RMSNorm+3 gathers backward (T x 2048)", "bytes", 6.0 * T * d * 2),
+    ("rmsnorm_gather_t8", "RMSNorm+3 gathers forward, 8-token tiles (T x 2048)", "bytes", 4.0 * T * d * 2),
+    ("rope_scatter_kernel", "RoPE + output scatter (T x 2048)", "bytes", 2.0 * T * d * 2),
+    ("attn_bwd", "causal attention backward (B=32, S=256, H=32, hd=64)", "flop", 32 * 32 * 3 * 10.0 * 128 * 128 * 64),
 ]
 
 
@@ -88,20 +96,52 @@ def run():
     ws, wsb = N.workspace(N.lib().poetx_rmsnorm_gather_bwd_workspace_bytes(T, d))
     N.call("poetx_rmsnorm_gather_bwd", T, d, x.data_ptr(), w.data_ptr(), rstd.data_ptr(), 3, _ptrs(invs), _ptrs(dus),
            None, dx.data_ptr(), dw.data_ptr(), 0, ws, wsb, st)
+    fwds = [torch.argsort(i.long()).int() for i in invs]
+    outs = [torch.empty_like(x) for _ in range(3)]
+    N.call("poetx_rmsnorm_gather", T, d, x.data_ptr(), w.data_ptr(), 1e-6, 3, _ptrs(fwds), _ptrs(outs), rstd.data_ptr(), st)
+    S_, H_, hd_ = 256, 32, 64
+    ang = torch.outer(torch.arange(S_, device=dev).float(), 1.0 / (10000 ** (torch.arange(0, hd_, 2, device=dev).float() / hd_)))
+    cs, sn = ang.cos().contiguous(), ang.sin().contiguous()
+    ro = torch.empty_like(x)
+    N.call("poetx_rope_scatter", T, S_, H_, hd_, x.data_ptr(), invs[0].data_ptr(), cs.data_ptr(), sn.data_ptr(),
+           ro.data_ptr(), st)
+    from paper_2603_05500_b200.trainer import _Attention
+    q_, k_, v_ = (torch.randn((T, d), device=dev).bfloat16().requires_grad_(True) for _ in range(3))
+    o_ = _Attention.apply(q_, k_, v_, T // S_, S_, H_, hd_)
+    torch.autograd.grad(o_, (q_, k_, v_), torch.randn_like(o_))
     torch.cuda.synchronize()
+
+
+def _long_csv_to_wide(path):
+    """`ncu --csv --metrics ... --log-file x.csv` (one row per metric) ->
+    the raw page's layout: header, units, one row per kernel launch."""
+    rows = [r for r in csv.reader(open(path)) if len(r) > 10]
+    h = rows[0]
+    ki, ni, ui, vi, ii = (h.index(k) for k in ("Kernel Name", "Metric Name", "Metric Unit", "Metric Value", "ID"))
+    launches, units = {}, {}
+    for r in rows[1:]:
+        e = launches.setdefault(r[ii], {"Kernel Name": r[ki]})
+        e[r[ni]] = r[vi].replace(",", "")
+        units[r[ni]] = r[ui]
+    names = ["Kernel Name"] + sorted(units)
+    data = [[launches[k].get(n, "0") for n in names] for k in sorted(launches, key=int)]
+    return names, [""] + [units[n] for n in names[1:]], data
 
 
 def summary(rep):
     with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
         peaks = json.load(fh)
     hbm, tf = peaks["hbm_gbs"], peaks["bf16_tflops"]
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
-                          "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
-                          "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,"
-                          "dram__throughput.avg.pct_of_peak_sustained_elapsed"],
-                         capture_output=True, text=True).stdout
-    rows = list(csv.reader(io.StringIO(out)))
-    h, units, data = rows[0], rows[1], rows[2:]
+    if rep.endswith(".csv"):
+        h, units, data = _long_csv_to_wide(rep)
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv", "--metrics",
+                              "gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,"
+                              "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,"
+                              "dram__throughput.avg.pct_of_peak_sustained_elapsed"],
+                             capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(out)))
+        h, units, data = rows[0], rows[1], rows[2:]
     col = {k: h.index(k) for k in h}
     scale = {"us": 1e-6, "ms": 1e-3, "ns": 1e-9, "msecond": 1e-3, "usecond": 1e-6, "nsecond": 1e-9}
     byte_scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
@@ -109,16 +149,17 @@ def summary(rep):
     print("|---|---|---|---|---|---|")
     i = 0
     for sub, label, kind, work in PLAN:
-        while i < len(data) and sub not in data[i][col["Kernel Name"]]:
-            i += 1
-        if i >= len(data):
-            break
-        r = data[i]
-        i += 1
+        j = i
+        while j < len(data) and sub not in data[j][col["Kernel Name"]]:
+            j += 1
+        if j >= len(data):  # not launched at this shape (e.g. no split-T reduce): skip the row
+            continue
+        r = data[j]
+        i = j + 1
         tsec = float(r[col["gpu__time_duration.sum"]]) * scale.get(units[col["gpu__time_duration.sum"]], 1e-6)
         rd = float(r[col["dram__bytes_read.sum"]]) * byte_scale.get(units[col["dram__bytes_read.sum"]], 1)
         wr = float(r[col["dram__bytes_write.sum"]]) * byte_scale.get(units[col["dram__bytes_write.sum"]], 1)
-        tp = r[col["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]]
+        tp = r[col["sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"]] or "0"
         if kind == "flop":
             ach = work / tsec / 1e12
             txt, frac = f"{ach:.0f} TFLOP/s", ach / tf
