@@ -121,3 +121,20 @@ def test_quantized_descriptor_requires_mem_variant():
     d.pm_codes, d.pm_scales = 16, 16  # any non-NULL pointers: validation fails first
     with pytest.raises(ConfigError, match="quantized base requires the mem variant"):
         N.call("poetx_layer_factors", d, N.LayerFactors(), None, 0, None)
+
+
+def test_weight_folding_rule(monkeypatch):
+    """Reassociated products only where they measured faster:
+    Llama-1B at 8192 tokens; not Llama-350M, not Llama-8B at 1024 tokens;
+    POETX_REASSOC forces either way."""
+    from paper_2603_05500_b200.trainer import llama_config, weight_folding_pays
+
+    monkeypatch.delenv("POETX_REASSOC", raising=False)
+    assert weight_folding_pays(llama_config("llama-1b"), 32)
+    assert not weight_folding_pays(llama_config("llama-350m"), 32)
+    assert not weight_folding_pays(llama_config("llama-8b"), 1)
+    assert weight_folding_pays(llama_config("llama-8b"), 8)
+    monkeypatch.setenv("POETX_REASSOC", "0")
+    assert not weight_folding_pays(llama_config("llama-1b"), 32)
+    monkeypatch.setenv("POETX_REASSOC", "1")
+    assert weight_folding_pays(llama_config("llama-350m"), 32)
