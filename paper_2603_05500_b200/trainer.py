@@ -880,6 +880,12 @@ class PoetLlama(torch.nn.Module):
         nf = self.dense_param("norm_f", (d,)).detach().requires_grad_(True)
         head = self.dense_param("head", (cfg.vocab, d)).detach().requires_grad_(True)
         leaves += [nf, head]
+        self._early_dense = set()
+        if self.dp_group is not None and self.cnp_pipelined:
+            # the head's gradient is final right after the loss head's backward:
+            # add it into the flat buffer and start its all-reduce then, under
+            # the whole decoder backward (SURVEY §8e bucketed overlap)
+            head.register_hook(self._head_grad_hook)
         h = F.rms_norm(h, (d,), nf.to(torch.bfloat16), 1e-6)
         logits = F.linear(h, head.to(torch.bfloat16))
         if self.fused:
@@ -952,12 +958,31 @@ class PoetLlama(torch.nn.Module):
         regen_d = lambda: _swiglu_regather(vg_d, vu_d, maps)  # noqa: E731
         return _ScatterAdd.apply(h, _PoetRawFn.apply(ud, down, regen_d), pout(down)[1], pout(down)[0])
 
+    def _head_grad_hook(self, g):
+        view = self.dense.view(self.dense.grad, "head", g.shape)
+        view.add_(g)
+        self.dp_works.append(_all_reduce_async(view.view(-1), self.dp_group))
+        self._early_dense.add("head")
+        return g
+
+    def dense_grad_rest(self):
+        """Contiguous slices of the flat dense grad buffer NOT already
+        all-reduced early (everything but the head when its hook fired)."""
+        flat = self.dense.grad
+        if "head" not in getattr(self, "_early_dense", ()):
+            return [flat]
+        off, size = self.dense.offsets["head"]
+        return [t for t in (flat[:off], flat[off + size:]) if t.numel()]
+
     def backward_dense_grads(self, loss):
         """Backprop; dense grads land in the flat dense grad buffer."""
         names = ["embed"] + [f"{i}.norm{j}" for i in range(self.cfg.layers) for j in (1, 2)] + ["norm_f", "head"]
         grads = torch.autograd.grad(loss, self._leaves, allow_unused=True)
+        early = getattr(self, "_early_dense", set())
         for name, g in zip(names, grads):
-            if g is not None:  # None: written in place by its backward (the fused embedding)
+            # None: written in place by its backward (fused embedding / RMSNorm);
+            # early: added (and all-reduced) by its hook during the backward
+            if g is not None and name not in early:
                 self.dense.view(self.dense.grad, name, g.shape).add_(g)
 
 
@@ -1054,7 +1079,7 @@ class Trainer:
             model.backward_dense_grads(loss)
             torch.cuda.current_stream().wait_stream(model.cnp_stream)
             if self.pg is not None:
-                _finish_all_reduce(model.dp_works + [_all_reduce_async(model.dense.grad, self.pg)])
+                _finish_all_reduce(model.dp_works + [_all_reduce_async(t, self.pg) for t in model.dense_grad_rest()])
                 model.dp_works = []
         else:
             model.stack.forward_factors()      # CNP of every block, one batched call
