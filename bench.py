@@ -107,6 +107,155 @@ def cpu_sample(cfg, T=32):
     return tok_s, procs, sample
 
 
+def host_info():
+    """Host cores and CPU model ("1 core used of N host cores")."""
+    model = None
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.lower().startswith("model name"):
+                model = line.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    if model is None:
+        try:
+            for line in open("/proc/cpuinfo"):
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+        except Exception:
+            pass
+    return {"host_cores": os.cpu_count(), "cpu_model": model}
+
+
+def _min_of(fn, reps):
+    fn()  # warmup
+    best = float("inf")
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        fn()
+        best = min(best, time.perf_counter() - t0)
+    return best
+
+
+def cpu_cfg1_split(reps=3):
+    """BASELINE.md §4 / configs[0]: single layer 512x512, b=64, k=3, fp32,
+    T=1024 on one host core through the oracle port (the reference's
+    algorithm and accumulation order, bitwise pinned to it): forward,
+    backward fast and mem, adamw_step, merge_and_reinit; min of `reps` after
+    one warmup, time.perf_counter."""
+    import numpy as np
+
+    from oracle import poetx_oracle as O
+
+    base, fi, fo, q_r, q_p, x, dz = O.cfg1_inputs()
+    out = {}
+    for variant in ("fast", "mem"):
+        lay = O.OracleLayer(base, 64, fi, fo, variant=variant)
+        lay.q_r[...] = q_r
+        lay.q_p[...] = q_p
+        if variant == "fast":
+            out["forward_ms"] = 1e3 * _min_of(lambda: lay.forward(x), reps)
+        out[f"backward_{variant}_ms"] = 1e3 * _min_of(lambda: lay.backward(lay.forward(x)[1], dz), reps) \
+            - out["forward_ms"]
+    lay = O.OracleLayer(base, 64, fi, fo)
+    lay.q_r[...] = q_r
+    lay.q_p[...] = q_p
+    z, c = lay.forward(x)
+    gr, gp, _ = lay.backward(c, dz)
+    params = {"r": lay.q_r.copy(), "p": lay.q_p.copy()}
+    m = {k: np.zeros_like(v) for k, v in params.items()}
+    v = {k: np.zeros_like(v) for k, v in params.items()}
+    out["adamw_step_ms"] = 1e3 * _min_of(lambda: O.adamw_step(params, {"r": gr, "p": gp}, m, v, 1, 1e-3), reps)
+    rng = np.random.default_rng(5)
+    out["merge_and_reinit_ms"] = 1e3 * _min_of(
+        lambda: lay.merge_and_reinit(rng.permutation(512).astype(np.int32), rng.permutation(512).astype(np.int32)),
+        reps)
+    out["fwd_bwd_fast_tokens_per_s"] = 1024 / ((out["forward_ms"] + out["backward_fast_ms"]) / 1e3)
+    out = {k: round(v, 3) for k, v in out.items()}
+    out["config"] = "cfg1: 512x512, b=64, k=3, fp32, T=1024; min of %d after 1 warmup; 1 core (oracle port)" % reps
+    return out
+
+
+def ffma_peak_tflops(dev):
+    """Measured FP32 CUDA-core peak (8 independent FFMA chains per thread,
+    16 CTAs of 256 per SM, best of 5, CUDA events)."""
+    import ctypes as C
+
+    import torch
+
+    from paper_2603_05500_b200 import _native as N
+
+    sink = torch.zeros(256, dtype=torch.float32, device=dev)
+    fl = C.c_double()
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    best = 0.0
+    for _ in range(6):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record()
+        N.call("poetx_ffma_probe", 1 << 16, sms * 8, sink.data_ptr(), C.byref(fl), N.stream_ptr(dev))
+        b.record()
+        b.synchronize()
+        best = max(best, fl.value / (a.elapsed_time(b) / 1e3) / 1e12)
+    return best
+
+
+def gpu_cfg1(dev, reps=5):
+    """configs[0] on the GPU through the drop-in layer API (fp32 parity path,
+    CUDA-core FFMA kernels): the same split as cpu_cfg1_split, device time
+    (CUDA events), inputs resident; fraction of the measured FFMA peak."""
+    import numpy as np
+    import torch
+
+    import paper_2603_05500_b200 as P
+    from oracle import poetx_oracle as O
+
+    base, fi, fo, q_r, q_p, x, dz = O.cfg1_inputs()
+    lay = P.PoetLinearLayer(torch.from_numpy(base), 64, P.Rng.keyed(0, "cfg1"), device=dev)
+    lay.set_permutations(P.PermutationMap.from_forward(fi), P.PermutationMap.from_forward(fo))
+    lay.q_r.packed.copy_(torch.from_numpy(q_r))
+    lay.q_p.packed.copy_(torch.from_numpy(q_p))
+    xd, dzd = torch.from_numpy(x).to(dev), torch.from_numpy(dz).to(dev)
+
+    def dev_ms(fn):
+        fn()
+        torch.cuda.synchronize()
+        best = float("inf")
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            fn()
+            b.record()
+            b.synchronize()
+            best = min(best, a.elapsed_time(b))
+        return best
+
+    out = {"forward_ms": dev_ms(lambda: lay.forward(xd))}
+    for variant in ("fast", "mem"):
+        lay.variant = variant
+        out[f"backward_{variant}_ms"] = dev_ms(lambda: lay.backward(lay.forward(xd)[1], dzd)) - out["forward_ms"]
+    lay.variant = "fast"
+    z, c = lay.forward(xd)
+    g = lay.backward(c, dzd)
+    params = {"q_r": lay.q_r.packed.clone(), "q_p": lay.q_p.packed.clone()}
+    st = P.adamw_init(params)
+    sched = P.ScheduleConfig(base_lr=1e-3, total_steps=100)
+    out["adamw_step_ms"] = dev_ms(lambda: P.optim._adamw_launch(
+        list(params.values()), [g.q_r, g.q_p], list(st.m.values()), list(st.v.values()), 1e-3, sched, 1))
+    rng = P.Rng.keyed(0, "cfg1-merge")
+    out["merge_and_reinit_ms"] = dev_ms(lambda: lay.merge_and_reinit(rng))
+    flops = 1.552e9  # BASELINE.md §3: cfg1 fast fwd+bwd
+    tf = flops / ((out["forward_ms"] + out["backward_fast_ms"]) / 1e3) / 1e12
+    peak = ffma_peak_tflops(dev)
+    out = {k: round(v, 4) for k, v in out.items()}
+    out.update({"fwd_bwd_fast_tokens_per_s": round(1024 / ((out["forward_ms"] + out["backward_fast_ms"]) / 1e3), 1),
+                "fwd_bwd_fast_tflops": round(tf, 3), "fp32_ffma_peak_tflops": round(peak, 2),
+                "frac_of_fp32_peak": round(tf / peak, 4),
+                "config": "cfg1 on cuda: fp32 CUDA-core parity path, device time (CUDA events), min of %d" % reps})
+    return out
+
+
 # ------------------------------------------------------------------ clocks --
 
 
@@ -283,6 +432,10 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
     peak_alloc = torch.cuda.max_memory_allocated(dev) / 1e9
     peak_res = torch.cuda.max_memory_reserved(dev) / 1e9
+    if pg is not None:  # per-GPU peak = max over ranks
+        pk = torch.tensor([peak_alloc, peak_res, peak_eager], device=dev, dtype=torch.float64)
+        dist.all_reduce(pk, op=dist.ReduceOp.MAX)
+        peak_alloc, peak_res, peak_eager = (float(v) for v in pk.tolist())
     e2e_ms, _ = timed(args.steps, resident=False)
     bad = int(trainer.last_bad.item()) if trainer.last_bad is not None else 0
     import ctypes as C
@@ -330,7 +483,8 @@ def run_ours(args, rank, world, local_rank):
             },
             "peak_hbm_gb": {"eager_step_allocated": round(peak_eager, 2),
                             "timed_allocated": round(peak_alloc, 2), "timed_reserved": round(peak_res, 2),
-                            "note": "timed steps replay a CUDA graph whose private pool is in reserved"},
+                            "note": "max over ranks; timed steps replay a CUDA graph whose private pool is in "
+                                    "reserved"},
             "step_tc_roofline": {"achieved_tflops": round(step_tc, 1), "peak": tf_sus,
                                  "frac": round(step_tc / tf_sus, 4),
                                  "flops_per_step": step_flops, "peak_source": src + " sustained"},
@@ -348,6 +502,7 @@ def run_ours(args, rank, world, local_rank):
             },
             "e2e": {"value": round(e2e, 1), "unit": UNIT,
                     "h2d_bytes_per_step": B * (S + 1) * 8, "d2h_bytes_per_step": 4},
+            "comm_nranks": dist.get_world_size() if pg is not None else 1,
             "gpu_launches": launches,
             "nonfinite_grads": bad,
             "clocks": clk,
@@ -376,9 +531,43 @@ def run_reference(args):
         "config": {"workload": f"{cfg.name} POET-X {cfg.variant} b={cfg.block} pretraining step (POET-X path sample)",
                    "seq_len": cfg.seq, "parallelism": "host cores"},
         "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": procs, "kind": "port",
-                         "sample": sample},
+                         "sample": sample, **host_info(), "cfg1_split": cpu_cfg1_split()},
         "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def _free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def relaunch_under_torchrun(args) -> int:
+    """``--gpus N`` (N > 1) outside torchrun: run N ranks on this node, one
+    per GPU, exactly as the driver would launch them (torch.distributed.run,
+    rendezvous on 127.0.0.1).  Returns the launcher's exit code."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__),
+           *sys.argv[1:]]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1")
+    return subprocess.call(cmd, env=env)
+
+
+def dry_run(args, rank, world):
+    """Launcher check (no GPU work): every rank joins the process group and
+    all-reduces its rank; rank 0 prints what the real run would report."""
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([rank + 1.0])
+    if dist.is_initialized():
+        dist.all_reduce(t)
+    return {"metric": METRIC, "dry_run": True, "n_gpus": world, "gpus_requested": args.gpus,
+            "comm_nranks": dist.get_world_size() if dist.is_initialized() else 1,
+            "backend": dist.get_backend() if dist.is_initialized() else None,
+            "rank_sum": float(t.item())}
 
 
 def main():
@@ -394,10 +583,17 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-tokens", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the side measurements (mem variant, merge, cfg1) after the headline line's steps")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="launch eagerly instead of replaying a captured CUDA graph of the step")
+    ap.add_argument("--dry-run", action="store_true", help="launcher check only: join the group, no GPU work")
+    ap.add_argument("--backend", default=None, help="process-group backend (default nccl; gloo for --dry-run)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl == "ours":
+        sys.exit(relaunch_under_torchrun(args))
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -409,21 +605,31 @@ def main():
         print(json.dumps(run_reference(args)), flush=True)
         return
 
+    if world != args.gpus:
+        print(f"warning: WORLD_SIZE={world} but --gpus {args.gpus}; reporting the {world} ranks that run",
+              file=sys.stderr)
     distributed = world > 1 or "TORCHELASTIC_RUN_ID" in os.environ  # torchrun, even at N=1
     if distributed:
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
-    out = run_ours(args, rank, world, local_rank)
+        backend = args.backend or ("gloo" if args.dry_run else "nccl")
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
+    if args.dry_run:
+        out = dry_run(args, rank, world)
+    else:
+        out = run_ours(args, rank, world, local_rank)
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and not args.dry_run:
             from paper_2603_05500_b200.trainer import llama_config
 
             v, procs, sample = cpu_sample(llama_config(args.model, variant=args.variant), T=args.cpu_tokens)
             out["cpu_baseline"] = {"value": round(v, 4), "unit": UNIT, "cores": procs, "kind": "port",
-                                   "sample": sample}
+                                   "sample": sample, **host_info(), "cfg1_split": cpu_cfg1_split()}
         print(json.dumps(out), flush=True)
     if distributed:
         import torch.distributed as dist

@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define POETX_ABI_VERSION 1
+#define POETX_ABI_VERSION 2
 
 /* element types */
 enum { POETX_F32 = 0, POETX_F64 = 1, POETX_BF16 = 2 };
@@ -72,6 +72,9 @@ void poetx_set_gemm_pair_enabled(int on);
 void poetx_prof_enable(int on);
 void poetx_prof_reset(void);
 int poetx_prof_query(const char* name, double* total_ms, int64_t* count, double* flops);
+/* FP32 CUDA-core peak probe: `ctas` x 256 threads, 8 independent FFMA chains
+ * of `iters` each; *flops = FLOP per launch (time it with events on stream). */
+int poetx_ffma_probe(int64_t iters, int64_t ctas, float* sink, double* flops, void* stream);
 
 /* ---------------------------------------------------------------- H1 RNG --
  * numpy Generator(Philox) state (the reference draws permutations through
@@ -287,7 +290,8 @@ int poetx_quant_gather(int dtype, int64_t rows, int64_t cols, int64_t src_cols, 
 /* ----------------------------------------------------------- loss head --
  * cross_entropy_fwd: per-row loss over bf16 logits [T, V] (V % 8 == 0) with
  * row max / sum-exp kept for the backward; cross_entropy_bwd: bf16
- * dlogits = (softmax - onehot) * (*dloss) * scale. */
+ * dlogits = (softmax - onehot) * (*dloss) * scale.  A target outside
+ * [0, V) (e.g. an ignore_index) is rejected: NaN loss row, zero grad row. */
 int poetx_cross_entropy_fwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, float* loss_rows,
                             float* row_max, float* row_sumexp, void* stream);
 int poetx_cross_entropy_bwd(int64_t T, int64_t V, const void* logits, const int64_t* targets, const float* row_max,
@@ -297,11 +301,13 @@ int poetx_cross_entropy_bwd(int64_t T, int64_t V, const void* logits, const int6
  * The trainer's token embedding (model plumbing): out[t] = bf16(table[tok[t]])
  * (fp32 table [V, d]); backward: dtable[v] += sum_{tok[t] = v} dh[t] over the
  * tokens sorted stably by id (sorted_tokens, order = the sort's permutation),
- * one warp per id in ascending position order -- deterministic, no atomics. */
+ * one warp per id in ascending position order -- deterministic, no atomics.
+ * Ids outside [0, V) never address the table: the forward writes a NaN row
+ * and the backward skips them. */
 int poetx_embedding_fwd(int64_t T, int64_t V, int64_t d, const int64_t* tokens, const float* table, void* out,
                         void* stream);
-int poetx_embedding_bwd(int64_t T, int64_t d, const int64_t* sorted_tokens, const int64_t* order, const void* dh,
-                        float* dtable, void* stream);
+int poetx_embedding_bwd(int64_t T, int64_t V, int64_t d, const int64_t* sorted_tokens, const int64_t* order,
+                        const void* dh, float* dtable, void* stream);
 
 /* ---------------------------------------------------- singular values --
  * svd_singular_values (linalg.py:166-218): one-sided Jacobi in float64,
@@ -374,7 +380,8 @@ size_t poetx_sqnorm_workspace_bytes(int ntensors, const int64_t* numel);
 /* fused clip + AdamW (optim.py:84-94 + 127-148), arithmetic in the param
  * type with the reference's operation order.  If sqnorm != NULL (DEVICE
  * double) and sqrt(*sqnorm) > clip_threshold, grads are first scaled by
- * (type)(clip_threshold / norm) -- written back to g when write_back_grads.
+ * (type)(clip_threshold / norm) -- written back to g when write_back_grads;
+ * a non-finite *sqnorm skips the update (nothing is written).
  * bc1 = 1 - beta1^t, bc2 = 1 - beta2^t computed by the caller in double. */
 int poetx_adamw(int dtype, int ntensors, void* const* p, void* const* g, void* const* m,
                 void* const* v, const int64_t* numel, double lr, double beta1, double beta2,

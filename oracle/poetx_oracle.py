@@ -34,8 +34,29 @@ import numpy as np
 # ---------------------------------------------------------------------------
 
 
+# Large-shape float64 parity checks (Llama-1B layer shapes, tests/
+# test_gpu_bench_config.py) may switch the three dense products to numpy's
+# BLAS: in float64 the accumulation order moves results by ~1e-13, far below
+# the 2e-2 bf16 tolerance they are checked at, and the ordered loops would
+# take minutes per layer.  Every golden/bitwise check keeps the default.
+_BLAS = [False]
+
+
+class blas_products:
+    """Context manager: ``with blas_products(): ...`` (float64 only)."""
+
+    def __enter__(self):
+        self._old = _BLAS[0]
+        _BLAS[0] = True
+
+    def __exit__(self, *exc):
+        _BLAS[0] = self._old
+
+
 def matmul(a, b):
     """a @ b, ascending-k rank-1 accumulation (linalg.py:42-60)."""
+    if _BLAS[0] and a.dtype == np.float64:
+        return np.matmul(a, b)
     m, k = a.shape
     out = np.zeros((m, b.shape[1]), dtype=a.dtype)
     tmp = np.empty_like(out)
@@ -47,6 +68,8 @@ def matmul(a, b):
 
 def matmul_abt(a, b):
     """a @ b.T without the transposed copy (linalg.py:63-83)."""
+    if _BLAS[0] and a.dtype == np.float64:
+        return np.matmul(a, b.T)
     out = np.zeros((a.shape[0], b.shape[0]), dtype=a.dtype)
     tmp = np.empty_like(out)
     for i in range(a.shape[1]):
@@ -57,6 +80,8 @@ def matmul_abt(a, b):
 
 def batched_matmul(a, b):
     """out[s] = a[s] @ b[s], ascending shared index (linalg.py:110-130)."""
+    if _BLAS[0] and a.dtype == np.float64:
+        return np.matmul(a, b)
     nb, m, k = a.shape
     out = np.zeros((nb, m, b.shape[2]), dtype=a.dtype)
     tmp = np.empty_like(out)
@@ -168,6 +193,9 @@ def apply_to_features(g, x, transpose=False):
     """Segment s of each row maps through block s (or its transpose) (blockdiag.py:58-73)."""
     nb, b, _ = g.shape
     x3 = np.ascontiguousarray(x).reshape(x.shape[0], nb, b)
+    if _BLAS[0] and x.dtype == np.float64:
+        gg = g.transpose(0, 2, 1) if transpose else g
+        return np.einsum("tsk,skj->tsj", x3, gg, optimize=True).reshape(x.shape[0], nb * b)
     out = np.zeros_like(x3)
     tmp = np.empty_like(x3)
     for k in range(b):
@@ -181,6 +209,9 @@ def apply_to_weight_rows(g, w, transpose=False):
     """Left multiply by the factor, segmenting rows (blockdiag.py:76-90)."""
     nb, b, _ = g.shape
     w3 = np.ascontiguousarray(w).reshape(nb, b, w.shape[1])
+    if _BLAS[0] and w.dtype == np.float64:
+        gg = g.transpose(0, 2, 1) if transpose else g
+        return np.matmul(gg, w3).reshape(nb * b, w.shape[1])
     out = np.zeros_like(w3)
     tmp = np.empty_like(w3)
     for k in range(b):
@@ -195,6 +226,8 @@ def segmented_outer(x, y, b):
     nb = x.shape[1] // b
     x3 = np.ascontiguousarray(x).reshape(x.shape[0], nb, b)
     y3 = np.ascontiguousarray(y).reshape(y.shape[0], nb, b)
+    if _BLAS[0] and x.dtype == np.float64:
+        return np.einsum("tsi,tsj->sij", x3, y3, optimize=True)
     out = np.zeros((nb, b, b), dtype=x.dtype)
     tmp = np.empty_like(out)
     for a in range(x.shape[0]):

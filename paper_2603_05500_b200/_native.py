@@ -21,6 +21,7 @@ from .errors import ConfigError, NumericsError, PoetxError, ShapeError, StateErr
 LIB_PATH = os.environ.get("POETX_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                            "libpoetx_b200.so")
 
+ABI_VERSION = 2  # must equal POETX_ABI_VERSION (include/poetx_b200.h) of the loaded build
 F32, F64, BF16 = 0, 1, 2
 FAST, MEM = 0, 1
 IN_GATHERED, OUT_UNSCATTERED, DZ_GATHERED, DX_UNSCATTERED = 1, 2, 4, 8
@@ -89,6 +90,7 @@ _SIGS = {
     "poetx_prof_reset": (None, []),
     "poetx_prof_query": (I32, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),
                                C.POINTER(C.c_double)]),
+    "poetx_ffma_probe": (I32, [I64, I64, VP, C.POINTER(C.c_double), VP]),
     "poetx_philox_seed": (I32, [C.POINTER(PhiloxState), C.c_uint64, C.c_uint64]),
     "poetx_philox_permutation": (I32, [C.POINTER(PhiloxState), I64, VP, VP]),
     "poetx_skew_from_packed": (I32, [I32, I64, I64, VP, VP, VP]),
@@ -116,7 +118,7 @@ _SIGS = {
     "poetx_attention_bwd": (I32, [I64, I64, I64, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP]),
     "poetx_singular_values_workspace_bytes": (SZ, [I64, I64, I64]),
     "poetx_embedding_fwd": (I32, [I64, I64, I64, VP, VP, VP, VP]),
-    "poetx_embedding_bwd": (I32, [I64, I64, VP, VP, VP, VP, VP]),
+    "poetx_embedding_bwd": (I32, [I64, I64, I64, VP, VP, VP, VP, VP]),
     "poetx_singular_values": (I32, [I64, I64, I64, VP, VP, C.c_double, I32, VP, VP, VP, SZ, VP]),
     "poetx_orthogonality_error": (I32, [I32, I64, I64, VP, VP, VP, SZ, VP]),
     "poetx_permute_cols": (I32, [I32, I64, I64, VP, VP, VP, VP]),
@@ -171,6 +173,10 @@ def lib():
                 fn = getattr(handle, name)
                 fn.restype = res
                 fn.argtypes = args
+            abi = handle.poetx_abi_version()
+            if abi != ABI_VERSION:
+                raise RuntimeError(f"{LIB_PATH} has ABI version {abi}, the Python binding expects {ABI_VERSION}: "
+                                   "rebuild with `python -m paper_2603_05500_b200.build`")
             _lib = handle
     return _lib
 
@@ -218,10 +224,17 @@ def require_cuda(t: torch.Tensor, what: str) -> None:
 
 class _WorkspacePool:
     """One growable scratch buffer per (device, stream).  Kernels are
-    stream-ordered, so reuse on the same stream is race-free."""
+    stream-ordered, so reuse on the same stream is race-free.
+
+    A buffer handed out while a CUDA graph is being captured is PINNED: the
+    graph bakes its address into its kernels, so when a later call needs a
+    larger buffer the pinned one is retired (kept alive for the process)
+    instead of freed -- a replay never reads freed memory."""
 
     def __init__(self):
         self._bufs = {}
+        self._pinned = set()   # data_ptr of buffers referenced by a captured graph
+        self._retired = []     # replaced pinned buffers, kept alive
 
     def get(self, nbytes: int, device=None) -> torch.Tensor:
         dev = torch.device("cuda", torch.cuda.current_device() if device is None else device.index)
@@ -231,11 +244,18 @@ class _WorkspacePool:
             nbytes = max(nbytes, 1 << 20)
             if buf is not None:
                 nbytes = max(nbytes, int(buf.numel() * 1.5))
+                if buf.data_ptr() in self._pinned:
+                    self._retired.append(buf)
             buf = torch.empty(nbytes, dtype=torch.uint8, device=dev)
             self._bufs[key] = buf
+        if torch.cuda.is_current_stream_capturing():
+            self._pinned.add(buf.data_ptr())
         return buf
 
     def clear(self):
+        """Drop the unpinned buffers (pinned ones stay: a graph may replay them)."""
+        keep = {k: b for k, b in self._bufs.items() if b.data_ptr() in self._pinned}
+        self._retired += list(keep.values())
         self._bufs.clear()
 
 

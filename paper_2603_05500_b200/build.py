@@ -8,6 +8,7 @@ with the repo snapshot; the CUDA runtime is linked statically.
 
 from __future__ import annotations
 
+import hashlib
 import os
 import subprocess
 import sys
@@ -27,19 +28,35 @@ FLAGS = [
 ]
 
 
-def _stale() -> bool:
-    if not os.path.exists(LIB):
-        return True
-    t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)]
+def _deps():
+    deps = sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC))
     deps.append(os.path.join(HERE, "..", "include", "poetx_b200.h"))
     deps.append(__file__)
-    return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
+    return [p for p in deps if os.path.isfile(p)]
+
+
+def source_hash() -> str:
+    """Content hash of every source the library is built from (robust to the
+    mtimes a repo snapshot copy may reset)."""
+    h = hashlib.sha256()
+    for p in _deps():
+        h.update(os.path.basename(p).encode())
+        with open(p, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB) or not os.path.exists(LIB + ".sha"):
+        return True
+    with open(LIB + ".sha") as f:
+        return f.read().strip() != source_hash()
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
+    digest = source_hash()
     srcs = [os.path.join(CSRC, s) for s in SOURCES]
     tmp = LIB + ".tmp"
     cmd = [NVCC, *FLAGS, "-o", tmp, *srcs]
@@ -48,6 +65,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
     os.replace(tmp, LIB)
+    with open(LIB + ".sha", "w") as f:
+        f.write(digest)
     return LIB
 
 

@@ -146,11 +146,8 @@ def trainer_tensors(trainer, tokens: int = 0, sv_drift: float = 0.0) -> dict:
         "progress/steps_since_merge": np.array([since], dtype=np.uint32),
         "progress/sv_drift": np.array([sv_drift], dtype=np.float64),
     }
-    for lay in model.poet_layers():
-        t[f"param/{lay.name}.q_r"] = lay.packed_r
-        t[f"param/{lay.name}.q_p"] = lay.packed_p
-    for name, (off, n) in model.dense.offsets.items():
-        t[f"param/{name}"] = model.dense.param[off:off + n]
+    for tag, grp, name, off, n, shape in _named_slices(model):
+        t[f"param/{name}"] = grp.param[off:off + n].view(shape)
     for lay in model.poet_layers():
         key = f"layer/{lay.name}"
         if getattr(lay, "quantized", False):  # W's codes / scales (runner.py:159-161)
@@ -166,24 +163,39 @@ def trainer_tensors(trainer, tokens: int = 0, sv_drift: float = 0.0) -> dict:
         t[f"{key}/perm_in"] = lay.perm_in.forward.astype(np.uint32)
         t[f"{key}/perm_out"] = lay.perm_out.forward.astype(np.uint32)
         t[f"{key}/merge_count"] = np.array([lay.merge_count], dtype=np.uint32)
-    for tag, grp, names in (("poet", model.poet, None), ("dense", model.dense, None)):
-        t[f"opt/{tag}/t"] = np.array([grp.t], dtype=np.uint32)
-        for name, (off, n) in grp.offsets.items():
-            t[f"opt/{tag}/m/{name}"] = grp.m[off:off + n]
-        for name, (off, n) in grp.offsets.items():
-            t[f"opt/{tag}/v/{name}"] = grp.v[off:off + n]
+    # moments keyed by the parameter name with the parameter's shape, as the
+    # reference's AdamWState dicts are (runner.py:166-172)
+    t["opt/poet/t"] = np.array([model.poet.t], dtype=np.uint32)
+    t["opt/dense/t"] = np.array([model.dense.t], dtype=np.uint32)
+    for tag, grp, name, off, n, shape in _named_slices(model):
+        t[f"opt/{tag}/m/{name}"] = grp.m[off:off + n].view(shape)
+    for tag, grp, name, off, n, shape in _named_slices(model):
+        t[f"opt/{tag}/v/{name}"] = grp.v[off:off + n].view(shape)
     return t
+
+
+def _named_slices(model):
+    """(group tag, FlatGroup, reference parameter name, offset, numel, shape)
+    for every trainable tensor: POET packed stacks as ``<layer>.q_r`` /
+    ``<layer>.q_p`` (nb, pairs); dense tensors with their 2-D shapes."""
+    out = []
+    for lay in model.poet_layers():
+        for side, packed in (("r", lay.packed_r), ("p", lay.packed_p)):
+            off, n = model.poet.offsets[f"{lay.name}.{side}"]
+            out.append(("poet", model.poet, f"{lay.name}.q_{side}", off, n, tuple(packed.shape)))
+    d = model.cfg.d
+    for name, (off, n) in model.dense.offsets.items():
+        shape = (n // d, d) if name in ("embed", "head") else (n,)
+        out.append(("dense", model.dense, name, off, n, shape))
+    return out
 
 
 def restore_trainer(trainer, tensors: dict) -> int:
     """Install a state written by ``trainer_tensors`` (same model shape);
     returns the stored token count."""
     model = trainer.model
-    for lay in model.poet_layers():
-        _restore(lay.packed_r, f"param/{lay.name}.q_r", tensors)
-        _restore(lay.packed_p, f"param/{lay.name}.q_p", tensors)
-    for name, (off, n) in model.dense.offsets.items():
-        _restore(model.dense.param[off:off + n], f"param/{name}", tensors)
+    for tag, grp, name, off, n, shape in _named_slices(model):
+        _restore(grp.param[off:off + n].view(shape), f"param/{name}", tensors)
     for lay in model.poet_layers():
         key = f"layer/{lay.name}"
         pin = PermutationMap.from_forward(_get(tensors, f"{key}/perm_in").astype(np.int32))
@@ -202,9 +214,9 @@ def restore_trainer(trainer, tensors: dict) -> int:
     model.refresh_maps()
     for tag, grp in (("poet", model.poet), ("dense", model.dense)):
         grp.t = int(_get(tensors, f"opt/{tag}/t")[0])
-        for name, (off, n) in grp.offsets.items():
-            _restore(grp.m[off:off + n], f"opt/{tag}/m/{name}", tensors)
-            _restore(grp.v[off:off + n], f"opt/{tag}/v/{name}", tensors)
+    for tag, grp, name, off, n, shape in _named_slices(model):
+        _restore(grp.m[off:off + n].view(shape), f"opt/{tag}/m/{name}", tensors)
+        _restore(grp.v[off:off + n].view(shape), f"opt/{tag}/v/{name}", tensors)
     trainer.step_idx = int(_get(tensors, "progress/step")[0])
     since = int(_get(tensors, "progress/steps_since_merge")[0])
     trainer.since_merge = None if since == NO_MERGE else since

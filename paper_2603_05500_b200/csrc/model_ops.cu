@@ -702,21 +702,33 @@ __global__ void __launch_bounds__(kThreads) scatter_add_kernel(
 // within an id): one warp per run of equal ids sums its rows in fp32 in that
 // fixed order and adds the total into the table gradient -- every row is
 // written by exactly one warp, no atomics, deterministic.
-__global__ void __launch_bounds__(256) embedding_fwd_kernel(int64_t T, int64_t d, const int64_t* __restrict__ tok,
+// Token ids outside [0, V) never address the table: the forward writes a
+// NaN row (so the loss turns non-finite and the trainer raises NumericsError,
+// as the reference does for a non-finite loss) and the backward skips them.
+__global__ void __launch_bounds__(256) embedding_fwd_kernel(int64_t T, int64_t V, int64_t d,
+                                                            const int64_t* __restrict__ tok,
                                                             const float* __restrict__ table,
                                                             __nv_bfloat16* __restrict__ out) {
   const int64_t nv = d / 8;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < T * nv;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
     const int64_t t = i / nv, c = i % nv;
-    const float4* src = reinterpret_cast<const float4*>(table + tok[t] * d) + 2 * c;
-    const float4 a = __ldg(src), b = __ldg(src + 1);
-    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    const int64_t id = tok[t];
+    float v[8];
+    if (id < 0 || id >= V) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) v[q] = __int_as_float(0x7fc00000);
+    } else {
+      const float4* src = reinterpret_cast<const float4*>(table + id * d) + 2 * c;
+      const float4 a = __ldg(src), b = __ldg(src + 1);
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    }
     reinterpret_cast<uint4*>(out + t * d)[c] = pack8(v);
   }
 }
 
-__global__ void __launch_bounds__(256) embedding_bwd_kernel(int64_t T, int64_t d, const int64_t* __restrict__ sorted_tok,
+__global__ void __launch_bounds__(256) embedding_bwd_kernel(int64_t T, int64_t V, int64_t d,
+                                                            const int64_t* __restrict__ sorted_tok,
                                                             const int64_t* __restrict__ order,
                                                             const __nv_bfloat16* __restrict__ dh,
                                                             float* __restrict__ dtable) {
@@ -724,6 +736,7 @@ __global__ void __launch_bounds__(256) embedding_bwd_kernel(int64_t T, int64_t d
   const int64_t j = blockIdx.x * static_cast<int64_t>(blockDim.x / 32) + threadIdx.x / 32;
   if (j >= T) return;
   const int64_t id = sorted_tok[j];
+  if (id < 0 || id >= V) return;                  // invalid id: no table row (forward wrote NaN)
   if (j > 0 && sorted_tok[j - 1] == id) return;  // not the start of a run
   int64_t end = j + 1;
   while (end < T && sorted_tok[end] == id) ++end;
@@ -783,7 +796,10 @@ __global__ void __launch_bounds__(256) ce_fwd_kernel(int64_t T, int V, const __n
     if (threadIdx.x == 0) {
       float M = sm_m[0], S = sm_s[0];
       for (int k = 1; k < 8; ++k) ms_combine(M, S, sm_m[k], sm_s[k]);
-      const float xt = __bfloat162float(x[r * V + tgt[r]]);
+      // targets outside [0, V) (e.g. an ignore_index) are rejected, not
+      // ignored: the row's loss is NaN, so the step's loss is non-finite
+      const int64_t t = tgt[r];
+      const float xt = (t >= 0 && t < V) ? __bfloat162float(x[r * V + t]) : __int_as_float(0x7fc00000);
       loss[r] = (M + logf(S)) - xt;
       mx[r] = M;
       se[r] = S;
@@ -803,6 +819,10 @@ __global__ void __launch_bounds__(256) ce_bwd_kernel(int64_t T, int V, const __n
     uint4* out = reinterpret_cast<uint4*>(grad + r * V);
     const float m = mx[r], inv = 1.f / se[r];
     const int64_t t = tgt[r];
+    if (t < 0 || t >= V) {  // rejected target (its loss row is NaN): zero gradient row
+      for (int i = threadIdx.x; i < nv; i += blockDim.x) __stcs(out + i, make_uint4(0, 0, 0, 0));
+      continue;
+    }
     for (int i = threadIdx.x; i < nv; i += blockDim.x) {
       float v[8];
       unpack8(__ldcs(row + i), v);
@@ -1118,17 +1138,17 @@ int poetx_embedding_fwd(int64_t T, int64_t V, int64_t d, const int64_t* tokens, 
   if (T == 0) return POETX_OK;
   const int64_t work = T * (d / 8);
   const unsigned grid = static_cast<unsigned>(work / 256 + 1 < 148 * 16 ? work / 256 + 1 : 148 * 16);
-  embedding_fwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(T, d, tokens, table, static_cast<__nv_bfloat16*>(out));
+  embedding_fwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(T, V, d, tokens, table, static_cast<__nv_bfloat16*>(out));
   POETX_LAUNCHED("embedding_fwd");
   return POETX_OK;
 }
 
-int poetx_embedding_bwd(int64_t T, int64_t d, const int64_t* sorted_tokens, const int64_t* order, const void* dh,
-                        float* dtable, void* stream) {
-  POETX_REQUIRE(T >= 0 && d > 0 && d % 8 == 0, POETX_ESHAPE, "embedding_bwd: d %% 8 == 0 required");
+int poetx_embedding_bwd(int64_t T, int64_t V, int64_t d, const int64_t* sorted_tokens, const int64_t* order,
+                        const void* dh, float* dtable, void* stream) {
+  POETX_REQUIRE(T >= 0 && V > 0 && d > 0 && d % 8 == 0, POETX_ESHAPE, "embedding_bwd: d %% 8 == 0 required");
   if (T == 0) return POETX_OK;
   const unsigned grid = static_cast<unsigned>((T + 7) / 8);
-  embedding_bwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(T, d, sorted_tokens, order,
+  embedding_bwd_kernel<<<grid, 256, 0, as_stream(stream)>>>(T, V, d, sorted_tokens, order,
                                                             static_cast<const __nv_bfloat16*>(dh), dtable);
   POETX_LAUNCHED("embedding_bwd");
   return POETX_OK;

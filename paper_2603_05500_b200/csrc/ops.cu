@@ -774,6 +774,11 @@ __global__ void adamw_kernel(int64_t n, T* __restrict__ p, T* __restrict__ g, T*
   T factor = one;
   if (sqnorm) {
     double norm = sqrt(*sqnorm);
+    // a non-finite gradient norm aborts the step in the reference
+    // (optim.py:87-89); on the device (no host sync, CUDA-graph replays) the
+    // update is skipped so parameters and moments stay intact, and the
+    // caller raises NumericsError from the norm kernel's flag
+    if (!isfinite(norm)) return;
     if (norm > s.thr && norm > 0.0) {  // optim.py:90-93
       clip = true;
       factor = static_cast<T>(s.thr / norm);

@@ -100,3 +100,31 @@ int poetx_prof_query(const char* name, double* total_ms, int64_t* count, double*
   return POETX_OK;
 }
 }
+
+// FP32 CUDA-core peak probe (the fp32 parity path's roofline
+// denominator).  Every thread runs 8 independent FFMA chains, so the FMA
+// pipes, not latency, bound it; FLOP per launch = 2 * 8 * iters * threads.
+namespace poetx {
+__global__ void __launch_bounds__(256) ffma_probe_kernel(int64_t iters, float* sink) {
+  float a[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) a[k] = threadIdx.x * 1e-3f + k;
+  const float b = 0.999f, c = 1e-4f;
+  for (int64_t i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = fmaf(a[k], b, c);
+  }
+  float s = 0.f;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += a[k];
+  if (s == 12345.678f) sink[threadIdx.x] = s;  // keeps the chains live
+}
+}  // namespace poetx
+
+extern "C" int poetx_ffma_probe(int64_t iters, int64_t ctas, float* sink, double* flops, void* stream) {
+  POETX_REQUIRE(iters > 0 && ctas > 0 && sink, POETX_ESHAPE, "ffma_probe: bad arguments");
+  poetx::ffma_probe_kernel<<<static_cast<unsigned>(ctas), 256, 0, as_stream(stream)>>>(iters, sink);
+  POETX_LAUNCHED("ffma_probe");
+  if (flops) *flops = 2.0 * 8.0 * static_cast<double>(iters) * static_cast<double>(ctas) * 256.0;
+  return POETX_OK;
+}

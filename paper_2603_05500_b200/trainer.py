@@ -30,7 +30,7 @@ import torch.nn.functional as F
 
 from . import _native as N
 from .cnp import num_pairs
-from .errors import ConfigError
+from .errors import ConfigError, NumericsError
 from .optim import ScheduleConfig, adamw_dyn_values, clip_threshold_at, fused_clip_adamw_dyn, lr_at
 from .permute import PermutationMap, sample_permutation
 from .rng import Rng
@@ -562,8 +562,8 @@ class _Embedding(torch.autograd.Function):
         (tok,) = ctx.saved_tensors
         dh = dh.contiguous()
         srt, order = torch.sort(tok, stable=True)
-        N.call("poetx_embedding_bwd", tok.numel(), dh.shape[1], srt.data_ptr(), order.data_ptr(), dh.data_ptr(),
-               ctx.grad_view.data_ptr(), N.stream_ptr(dh.device))
+        N.call("poetx_embedding_bwd", tok.numel(), ctx.grad_view.shape[0], dh.shape[1], srt.data_ptr(),
+               order.data_ptr(), dh.data_ptr(), ctx.grad_view.data_ptr(), N.stream_ptr(dh.device))
         return None, None, None
 
 
@@ -1061,6 +1061,14 @@ class Trainer:
         self.dyn_ring = [torch.zeros((2, 5), dtype=torch.float64).pin_memory() for _ in range(4)]
         self.dyn_events = [None] * len(self.dyn_ring)
         self.dyn = torch.zeros((2, 5), dtype=torch.float64, device=self.device)
+        # numerics flags of each step {non-finite grad flag, loss}, copied to a
+        # pinned ring and inspected lazily (4 steps later, or before a merge):
+        # the device skips a non-finite update, the host raises NumericsError
+        # as the reference does (runner.py:282-283, optim.py:87-89)
+        self.flags = torch.zeros(2, dtype=torch.float64, device=self.device)
+        self.flag_ring = [torch.zeros(2, dtype=torch.float64).pin_memory() for _ in range(4)]
+        self.flag_events = [None] * len(self.flag_ring)
+        self.flag_steps = [None] * len(self.flag_ring)
 
     def tokens_per_step(self) -> int:
         return self.micro_batch * self.cfg.seq
@@ -1092,7 +1100,10 @@ class Trainer:
             [([model.poet.param], [model.poet.grad], [model.poet.m], [model.poet.v], self.dyn[0]),
              ([model.dense.param], [model.dense.grad], [model.dense.m], [model.dense.v], self.dyn[1])],
             self.sched)
-        return loss.detach()
+        loss = loss.detach()
+        self.flags[0].copy_(self.last_bad[0])
+        self.flags[1].copy_(loss)
+        return loss
 
     def _prepare_scalars(self):
         """Host side of runner.py:288-296: lr schedule, POET lr scale, clip ramp,
@@ -1114,11 +1125,41 @@ class Trainer:
         ev.record(torch.cuda.current_stream(self.device))
         self.dyn_events[slot] = ev
 
+    def _inspect_flags(self, slot: int) -> None:
+        ev = self.flag_events[slot]
+        if ev is None:
+            return
+        ev.synchronize()
+        self.flag_events[slot] = None
+        bad, loss = (float(v) for v in self.flag_ring[slot])
+        if bad:
+            raise NumericsError(f"non-finite gradient at step {self.flag_steps[slot]} (update skipped on the device)")
+        if not math.isfinite(loss):
+            raise NumericsError(f"non-finite training loss at step {self.flag_steps[slot]}")
+
+    def _record_flags(self) -> None:
+        slot = self.step_idx % len(self.flag_ring)
+        self._inspect_flags(slot)  # the step that used this slot 4 steps ago
+        self.flag_ring[slot].copy_(self.flags, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record(torch.cuda.current_stream(self.device))
+        self.flag_events[slot], self.flag_steps[slot] = ev, self.step_idx
+
+    def check_numerics(self) -> None:
+        """Raise NumericsError if any step since the last check saw a
+        non-finite gradient norm or loss (synchronises with the device)."""
+        order = sorted((s for s in range(len(self.flag_ring)) if self.flag_events[s] is not None),
+                       key=lambda s: self.flag_steps[s])
+        for slot in order:
+            self._inspect_flags(slot)
+
     def _advance(self):
+        self._record_flags()
         self.step_idx += 1
         if self.since_merge is not None:
             self.since_merge += 1
-        if self.merge_gap and self.step_idx % self.merge_gap == 0:
+        # every merge_gap steps, never after the final step (runner.py:303)
+        if self.merge_gap and self.step_idx % self.merge_gap == 0 and self.step_idx < self.sched.total_steps:
             self.merge()
 
     def step(self, tokens: torch.Tensor, targets: torch.Tensor) -> torch.Tensor:
@@ -1194,6 +1235,7 @@ class Trainer:
         """Merge-then-reinitialize every layer (runner.py:302-326): keyed merge
         RNGs, fresh AdamW moments for the POET group, and a merge audit per
         layer (orthogonality errors of the folded factors, read back once)."""
+        self.check_numerics()  # never fold a non-finite step into the frozen weights
         layers = self.model.poet_layers()
         audit = torch.zeros((len(layers), 2), dtype=torch.float64, device=self.device)
         for i, (lay, rng) in enumerate(zip(layers, merge_rngs(self.seed, self.step_idx, len(layers)))):

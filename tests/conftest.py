@@ -11,10 +11,10 @@ def pytest_configure(config):
 
 
 def pytest_sessionstart(session):
-    """Build libpoetx_b200.so once if it is missing (nvcc cross-compiles for
-    sm_100a without a GPU); an existing build is used as is."""
-    so = os.path.join(ROOT, "paper_2603_05500_b200", "libpoetx_b200.so")
-    if not os.path.exists(so):
-        from paper_2603_05500_b200.build import build
+    """Build libpoetx_b200.so if it is missing or older than its sources (a
+    content hash of csrc/ + the header, so a stale build whose struct layout
+    no longer matches is never tested; nvcc cross-compiles for sm_100a
+    without a GPU).  _native.lib() also checks the ABI version on load."""
+    from paper_2603_05500_b200.build import build
 
-        build(force=True)
+    build()
