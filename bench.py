@@ -507,6 +507,12 @@ def run_ours(args, rank, world, local_rank):
             "nonfinite_grads": bad,
             "clocks": clk,
         }
+    if rank == 0 and world == 1 and not args.no_extras:
+        # side measurements after the headline steps (never inside them)
+        try:
+            out["cfg1_gpu"] = gpu_cfg1(dev)
+        except Exception as e:  # reported, never fatal to the headline line
+            out["cfg1_gpu"] = {"error": f"{type(e).__name__}: {e}"[:300]}
     return out
 
 
