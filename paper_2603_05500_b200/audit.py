@@ -97,8 +97,10 @@ def spectrum_audit(cfg, device=None, verbose: bool = True) -> dict:
         raise ConfigError("audit_dim must be divisible by block_size")
     dtype = np.float32 if cfg.precision == 32 else np.float64
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    # device-resident layer state (torch dtype): the whole audit stays on the GPU
     layer = init_layer(dim, dim, cfg.block_size, Rng.keyed(cfg.seed, "audit", "init"), name="audit",
-                       variant=cfg.variant, neumann_k=cfg.neumann_k, dtype=dtype, device=dev)
+                       variant=cfg.variant, neumann_k=cfg.neumann_k,
+                       dtype=torch.float32 if dtype == np.float32 else torch.float64, device=dev)
     # gaussian_matrix (linalg.py:147-158): float64 draws cast to the layer type
     teacher = (Rng.keyed(cfg.seed, "audit", "teacher").normal((dim, dim)) * (1.0 / np.sqrt(dim))).astype(dtype)
     x = (Rng.keyed(cfg.seed, "audit", "input").normal((cfg.batch_size, dim)) * 1.0).astype(dtype)

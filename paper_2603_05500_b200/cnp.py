@@ -37,15 +37,15 @@ def _out(t, was_np):
 @dataclass
 class SkewParams:
     """Packed skew-symmetric parameters for a stack of blocks (cnp.py:42-59).
-    ``packed`` is a device tensor (num_blocks, b(b-1)/2)."""
+    ``packed`` (num_blocks, b(b-1)/2) is a device tensor, or a host numpy
+    array kept as is (numpy-constructed layers: the optimizer and the caller
+    mutate it in place, as with the reference)."""
 
     num_blocks: int
     block_dim: int
     packed: torch.Tensor
 
     def __post_init__(self):
-        if isinstance(self.packed, np.ndarray):
-            self.packed = torch.from_numpy(np.ascontiguousarray(self.packed)).cuda()
         want = (self.num_blocks, num_pairs(self.block_dim))
         if tuple(self.packed.shape) != want:
             raise ShapeError(f"packed shape {tuple(self.packed.shape)}, expected {want}")
@@ -66,12 +66,13 @@ def _pdtype(t: torch.Tensor) -> int:
 
 def skew_from_packed(params: SkewParams):
     """Unpack to a (num_blocks, b, b) skew-symmetric stack (cnp.py:71-78)."""
-    p = params.packed
+    p, was_np = _to_dev(params.packed)
+    p = p.contiguous()
     b = params.block_dim
     q = torch.empty((params.num_blocks, b, b), dtype=p.dtype, device=p.device)
     N.call("poetx_skew_from_packed", _pdtype(p), params.num_blocks, b, p.data_ptr(), q.data_ptr(),
            N.stream_ptr(p.device))
-    return q
+    return _out(q, was_np)
 
 
 def packed_grad_from_skew_grad(dq):

@@ -92,7 +92,7 @@ class Factors:
         self.packed_r, self.packed_p = packed_r, packed_p
         self.g_r = torch.empty((nbr, b, b), dtype=pdt, device=dev)
         self.g_p = torch.empty((nbp, b, b), dtype=pdt, device=dev)
-        low = layer.dtype == torch.bfloat16
+        low = layer.tdtype == torch.bfloat16
         self.g_r_lowp = torch.empty((nbr, b, b), dtype=torch.bfloat16, device=dev) if low else None
         self.g_p_lowp = torch.empty((nbp, b, b), dtype=torch.bfloat16, device=dev) if low else None
         self.q2_r = torch.empty((nbr, b, b), dtype=pdt, device=dev) if k == 3 else None
@@ -105,7 +105,14 @@ class Factors:
 class PoetLinearLayer:
     def __init__(self, base_weight, block_size: int, rng: Rng, *, name: str = "poet",
                  variant: str = "fast", neumann_k: int = 3, device=None):
-        if isinstance(base_weight, np.ndarray):
+        # numpy in => numpy state (the reference's own types, drop-in for
+        # poetx.layer): q_r/q_p.packed are host numpy arrays the caller and
+        # the optimizer mutate in place, base/premerged/materialize_weight come
+        # back as numpy, dtype is a numpy dtype; the weight itself lives on the
+        # device and every forward/backward/merge runs there.  Torch in =>
+        # device-resident state (torch CUDA tensors, no copies).
+        self._host = isinstance(base_weight, np.ndarray)
+        if self._host:
             if base_weight.dtype not in (np.float32, np.float64):
                 raise ShapeError(f"unsupported dtype {base_weight.dtype}")
             base_weight = torch.from_numpy(np.ascontiguousarray(base_weight))
@@ -131,73 +138,128 @@ class PoetLinearLayer:
         self.block_size = int(block_size)
         self.variant = variant
         self.neumann_k = int(neumann_k)
-        self.dtype = base_weight.dtype
-        self.param_dtype = param_dtype(self.dtype)
-        self.q_r = SkewParams.zeros(self.m // block_size, block_size, dtype=self.param_dtype, device=self.device)
-        self.q_p = SkewParams.zeros(self.n // block_size, block_size, dtype=self.param_dtype, device=self.device)
+        self.tdtype = base_weight.dtype  # torch dtype of the device computation
+        self.param_dtype = param_dtype(self.tdtype)
+        nbr, nbp = self.m // block_size, self.n // block_size
+        if self._host:
+            np_dt = np.float64 if self.param_dtype == torch.float64 else np.float32
+            self.q_r = SkewParams(nbr, block_size, np.zeros((nbr, num_pairs(block_size)), dtype=np_dt))
+            self.q_p = SkewParams(nbp, block_size, np.zeros((nbp, num_pairs(block_size)), dtype=np_dt))
+        else:
+            self.q_r = SkewParams.zeros(nbr, block_size, dtype=self.param_dtype, device=self.device)
+            self.q_p = SkewParams.zeros(nbp, block_size, dtype=self.param_dtype, device=self.device)
         self.merge_count = 0
         self.perm_in = sample_permutation(self.m, rng)
         self.perm_out = sample_permutation(self.n, rng)
         w = base_weight.to(self.device).contiguous()
-        self.premerged = self._premerge(w, self.perm_in, self.perm_out)
+        self._pm = self._premerge(w, self.perm_in, self.perm_out)
 
     # -- construction helpers ----------------------------------------------------
 
     @property
+    def dtype(self):
+        """numpy dtype for a numpy-constructed layer (as the reference), else
+        the torch dtype."""
+        if self._host:
+            return np.dtype(np.float64 if self.tdtype == torch.float64 else np.float32)
+        return self.tdtype
+
+    @property
+    def premerged(self):
+        """PM = Psi_m W Psi_n^T (layer.py:161-167): the device tensor, or a
+        numpy copy for a numpy-constructed layer."""
+        if self._host and isinstance(self._pm, torch.Tensor):
+            return self._pm.cpu().numpy()
+        return self._pm
+
+    @premerged.setter
+    def premerged(self, pm) -> None:
+        if isinstance(pm, np.ndarray):
+            pm = torch.from_numpy(np.ascontiguousarray(pm)).to(self.device, self.tdtype)
+        self._pm = pm
+
+    def _packed_dev(self, side: str) -> torch.Tensor:
+        """The packed parameters of one side as a device tensor (a copy of the
+        host array for a numpy-constructed layer)."""
+        p = (self.q_r if side == "r" else self.q_p).packed
+        if isinstance(p, np.ndarray):
+            return torch.from_numpy(np.ascontiguousarray(p)).to(self.device)
+        return p
+
+    def _zero_packed(self) -> None:
+        """Zero both packed stacks IN PLACE (layer.py:306-309: optimizer state
+        keyed to these arrays stays attached)."""
+        for sp in (self.q_r, self.q_p):
+            if isinstance(sp.packed, np.ndarray):
+                sp.packed[...] = 0.0
+            else:
+                sp.packed.zero_()
+
+    @property
     def quantized(self) -> bool:
-        return isinstance(self.premerged, QuantizedMatrix)
+        return isinstance(self._pm, QuantizedMatrix)
 
     def trainable_param_count(self) -> int:
-        return int(self.q_r.packed.numel() + self.q_p.packed.numel())
+        return int(np.prod(self.q_r.packed.shape) + np.prod(self.q_p.packed.shape))
 
     def _stream(self) -> int:
         return N.stream_ptr(self.device)
 
     def _premerge(self, w: torch.Tensor, pin: PermutationMap, pout: PermutationMap) -> torch.Tensor:
-        out = torch.empty((self.m, self.n), dtype=self.dtype, device=self.device)
+        out = torch.empty((self.m, self.n), dtype=self.tdtype, device=self.device)
         rf, _ = pin.device(self.device)
         cf, _ = pout.device(self.device)
-        N.call("poetx_gather2d", N.dtype_code(self.dtype), self.m, self.n, rf.data_ptr(),
+        N.call("poetx_gather2d", N.dtype_code(self.tdtype), self.m, self.n, rf.data_ptr(),
                cf.data_ptr(), w.data_ptr(), out.data_ptr(), self._stream())
+        return out
+
+    def _base_dev(self):
+        """W[r, c] = PM[pi_in^-1(r), pi_out^-1(c)] on the device (exact gather;
+        a QuantizedMatrix when the base is quantized)."""
+        if self.quantized:
+            return self._pm.gather(self.perm_in.inverse, self.perm_out.inverse)
+        _, ri = self.perm_in.device(self.device)
+        _, ci = self.perm_out.device(self.device)
+        out = torch.empty((self.m, self.n), dtype=self.tdtype, device=self.device)
+        N.call("poetx_gather2d", N.dtype_code(self.tdtype), self.m, self.n, ri.data_ptr(),
+               ci.data_ptr(), self._pm.data_ptr(), out.data_ptr(), self._stream())
         return out
 
     @property
     def base(self):
-        """Frozen weight W recovered from the premerged copy:
-        W[r, c] = PM[pi_in^-1(r), pi_out^-1(c)] (exact; a QuantizedMatrix
-        when the base is quantized, as in the reference)."""
-        if self.quantized:
-            return self.premerged.gather(self.perm_in.inverse, self.perm_out.inverse)
-        _, ri = self.perm_in.device(self.device)
-        _, ci = self.perm_out.device(self.device)
-        out = torch.empty((self.m, self.n), dtype=self.dtype, device=self.device)
-        N.call("poetx_gather2d", N.dtype_code(self.dtype), self.m, self.n, ri.data_ptr(),
-               ci.data_ptr(), self.premerged.data_ptr(), out.data_ptr(), self._stream())
-        return out
+        """Frozen weight W recovered from the premerged copy (exact; a
+        QuantizedMatrix when the base is quantized, as in the reference;
+        numpy for a numpy-constructed layer)."""
+        w = self._base_dev()
+        if self._host and isinstance(w, torch.Tensor):
+            return w.cpu().numpy()
+        return w
 
     @base.setter
     def base(self, w) -> None:
         if isinstance(w, np.ndarray):
             w = torch.from_numpy(np.ascontiguousarray(w))
+        if not isinstance(w, (torch.Tensor, QuantizedMatrix)) and hasattr(w, "codes") and hasattr(w, "scales"):
+            w = QuantizedMatrix(w.codes, w.scales, float_dtype=self.tdtype)  # the reference's QuantizedMatrix
         if isinstance(w, QuantizedMatrix):
             if w.shape != (self.m, self.n):
                 raise ShapeError(f"base weight shape {w.shape}, expected ({self.m}, {self.n})")
-            self.premerged = w.gather(self.perm_in.forward, self.perm_out.forward)
+            self._pm = w.gather(self.perm_in.forward, self.perm_out.forward)
             return
         if tuple(w.shape) != (self.m, self.n):
             raise ShapeError(f"base weight shape {tuple(w.shape)}, expected ({self.m}, {self.n})")
-        self.premerged = self._premerge(w.to(self.device, self.dtype).contiguous(), self.perm_in, self.perm_out)
+        self._pm = self._premerge(w.to(self.device, self.tdtype).contiguous(), self.perm_in, self.perm_out)
 
     def set_permutations(self, perm_in: PermutationMap, perm_out: PermutationMap) -> None:
         """Install explicit permutations keeping W fixed (layer.py:153-159)."""
         if perm_in.n != self.m or perm_out.n != self.n:
             raise ShapeError("permutation sizes do not match layer dims")
-        w = self.base
+        w = self._base_dev()
         self.perm_in, self.perm_out = perm_in, perm_out
         if isinstance(w, QuantizedMatrix):
-            self.premerged = w.gather(perm_in.forward, perm_out.forward)
+            self._pm = w.gather(perm_in.forward, perm_out.forward)
         else:
-            self.premerged = self._premerge(w, perm_in, perm_out)
+            self._pm = self._premerge(w, perm_in, perm_out)
 
     def quantize_base(self) -> None:
         """Switch the frozen weight to per-row int8 (POET-XQ, layer.py:169-177).
@@ -207,8 +269,8 @@ class PoetLinearLayer:
         if self.variant != "mem":
             raise ConfigError("quantized base requires the mem variant")
         if not self.quantized:
-            self.premerged = QuantizedMatrix.quantize(self.base).gather(self.perm_in.forward,
-                                                                        self.perm_out.forward)
+            self._pm = QuantizedMatrix.quantize(self._base_dev()).gather(self.perm_in.forward,
+                                                                         self.perm_out.forward)
 
     # -- descriptor ----------------------------------------------------------------
 
@@ -216,7 +278,7 @@ class PoetLinearLayer:
         fi, ii = self.perm_in.device(self.device)
         fo, io = self.perm_out.device(self.device)
         d = N.LayerDesc()
-        d.dtype = N.dtype_code(self.dtype)
+        d.dtype = N.dtype_code(self.tdtype)
         d.variant = N.FAST if self.variant == "fast" else N.MEM
         d.neumann_k = self.neumann_k
         d.m, d.n, d.b = self.m, self.n, self.block_size
@@ -225,15 +287,15 @@ class PoetLinearLayer:
         d.fold_weight = int(getattr(self, "fold_weight", True))
         if self.quantized:
             d.premerged = None
-            d.pm_codes = self.premerged.codes.data_ptr()
-            d.pm_scales = self.premerged.scales.data_ptr()
+            d.pm_codes = self._pm.codes.data_ptr()
+            d.pm_scales = self._pm.scales.data_ptr()
         else:
-            d.premerged = self.premerged.data_ptr()
+            d.premerged = self._pm.data_ptr()
         return d
 
     def compute_factors(self, packed_r=None, packed_p=None) -> Factors:
-        f = Factors(self, self.q_r.packed if packed_r is None else packed_r,
-                    self.q_p.packed if packed_p is None else packed_p)
+        f = Factors(self, self._packed_dev("r") if packed_r is None else packed_r,
+                    self._packed_dev("p") if packed_p is None else packed_p)
         d = self._desc()
         ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(
             N.dtype_code(self.param_dtype), max(self.m, self.n) // self.block_size,
@@ -246,10 +308,10 @@ class PoetLinearLayer:
     def _input(self, x, what):
         was_np = isinstance(x, np.ndarray)
         if was_np:
-            if _NP_TO_TORCH.get(x.dtype) != self.dtype:
+            if _NP_TO_TORCH.get(x.dtype) != self.tdtype:
                 raise ShapeError(f"{what} dtype {x.dtype} does not match layer dtype {self.dtype}")
             x = torch.from_numpy(np.ascontiguousarray(x)).to(self.device)
-        elif x.dtype != self.dtype:
+        elif x.dtype != self.tdtype:
             raise ShapeError(f"{what} dtype {x.dtype} does not match layer dtype {self.dtype}")
         if not x.is_cuda:
             x = x.to(self.device)
@@ -261,9 +323,10 @@ class PoetLinearLayer:
         x, was_np = self._input(x, "input")
         T = x.shape[0]
         # snapshot the parameters so backward differentiates this forward's factors
-        f = self.compute_factors(self.q_r.packed.clone(), self.q_p.packed.clone())
-        z = torch.empty((T, self.n), dtype=self.dtype, device=self.device)
-        saved = torch.empty((T, self.n), dtype=self.dtype, device=self.device) if self.variant == "fast" else None
+        pr, pp = self._packed_dev("r"), self._packed_dev("p")
+        f = self.compute_factors(pr if self._host else pr.clone(), pp if self._host else pp.clone())
+        z = torch.empty((T, self.n), dtype=self.tdtype, device=self.device)
+        saved = torch.empty((T, self.n), dtype=self.tdtype, device=self.device) if self.variant == "fast" else None
         d = self._desc()
         ws, wsb = N.workspace(N.lib().poetx_layer_workspace_bytes(d, T), self.device)
         N.call("poetx_layer_forward", d, f.struct, T, x.data_ptr(), z.data_ptr(), N.ptr(saved), ws, wsb,
@@ -281,9 +344,9 @@ class PoetLinearLayer:
         dz, _ = self._input(dz, "cotangent")
         cache.consumed = True
         T = cache.x.shape[0]
-        dx = torch.empty((T, self.m), dtype=self.dtype, device=self.device)
-        gr = torch.empty_like(self.q_r.packed)
-        gp = torch.empty_like(self.q_p.packed)
+        dx = torch.empty((T, self.m), dtype=self.tdtype, device=self.device)
+        gr = torch.empty_like(cache.factors.packed_r)
+        gp = torch.empty_like(cache.factors.packed_p)
         d = self._desc()
         ws, wsb = N.workspace(N.lib().poetx_layer_workspace_bytes(d, T), self.device)
         N.call("poetx_layer_backward", d, cache.factors.struct, T, cache.x.data_ptr(), dz.data_ptr(),
@@ -300,32 +363,35 @@ class PoetLinearLayer:
         if not use_exact_cayley:
             return f.g_r, f.g_p
         from .cnp import skew_from_packed
-        return cayley_exact(skew_from_packed(self.q_r)), cayley_exact(skew_from_packed(self.q_p))
+        b = self.block_size
+        q_r = SkewParams(self.m // b, b, self._packed_dev("r"))
+        q_p = SkewParams(self.n // b, b, self._packed_dev("p"))
+        return cayley_exact(skew_from_packed(q_r)), cayley_exact(skew_from_packed(q_p))
 
     def _merge_call(self, g_r, g_p, new_in=None, new_out=None, want_w=False):
         d = self._desc()
         ws, wsb = N.workspace(N.lib().poetx_merge_workspace_bytes(d), self.device)
         if self.quantized:
-            w = torch.empty((self.m, self.n), dtype=self.dtype, device=self.device) if want_w else None
+            w = torch.empty((self.m, self.n), dtype=self.tdtype, device=self.device) if want_w else None
             if new_in is None:  # materialize only: the float transform of the dequantized base
                 N.call("poetx_layer_merge", d, g_r.contiguous().data_ptr(), g_p.contiguous().data_ptr(),
                        None, None, None, N.ptr(w), ws, wsb, self._stream())
                 return None, w
-            q = self.premerged
+            q = self._pm
             codes = torch.empty_like(q.codes)
             scales = torch.empty_like(q.scales)
             N.call("poetx_layer_merge_quant", d, g_r.contiguous().data_ptr(), g_p.contiguous().data_ptr(),
                    new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
                    codes.data_ptr(), scales.data_ptr(), N.ptr(w), ws, wsb, self._stream())
-            return QuantizedMatrix(codes, scales, float_dtype=self.dtype), w
+            return QuantizedMatrix(codes, scales, float_dtype=self.tdtype), w
         pm_new = w = None
         ni = no = None
         if new_in is not None:
-            pm_new = torch.empty_like(self.premerged)
+            pm_new = torch.empty_like(self._pm)
             ni = new_in.device(self.device)[0]
             no = new_out.device(self.device)[0]
         if want_w:
-            w = torch.empty_like(self.premerged)
+            w = torch.empty_like(self._pm)
         N.call("poetx_layer_merge", d, g_r.contiguous().data_ptr(), g_p.contiguous().data_ptr(),
                N.ptr(ni), N.ptr(no), N.ptr(pm_new), N.ptr(w), ws, wsb, self._stream())
         return pm_new, w
@@ -337,7 +403,8 @@ class PoetLinearLayer:
 
     def materialize_weight(self):
         """Dense effective weight R W P (layer.py:275-277)."""
-        return self._transformed_base(use_exact_cayley=False)
+        w = self._transformed_base(use_exact_cayley=False)
+        return w.cpu().numpy() if self._host else w
 
     def merge_and_reinit(self, rng: Rng, *, use_exact_cayley: bool = False,
                          compute_sv_drift: bool = False) -> MergeAudit:
@@ -349,7 +416,7 @@ class PoetLinearLayer:
         new_in = sample_permutation(self.m, rng)
         new_out = sample_permutation(self.n, rng)
         drift = float("nan")
-        old_base = self.base if compute_sv_drift else None
+        old_base = self._base_dev() if compute_sv_drift else None
         if isinstance(old_base, QuantizedMatrix):
             old_base = old_base.dequantize()
         pm_new, w_new = self._merge_call(g_r, g_p, new_in, new_out, want_w=compute_sv_drift)
@@ -364,9 +431,8 @@ class PoetLinearLayer:
                 sv_new = torch.linalg.svdvals(w_new.double())
             denom = torch.clamp(sv_old, min=np.finfo(np.float64).tiny)
             drift = float(torch.max(torch.abs(sv_new - sv_old) / denom))
-        self.premerged = pm_new
-        self.q_r.packed.zero_()
-        self.q_p.packed.zero_()
+        self._pm = pm_new
+        self._zero_packed()
         self.perm_in, self.perm_out = new_in, new_out
         self.merge_count += 1
         return MergeAudit(self.merge_count, float(err_r), float(err_p), drift)
@@ -377,19 +443,26 @@ def init_layer(m: int, n: int, block_size: int, rng: Rng, *, name: str = "poet",
                weight_std: float | None = None, base_weight=None, device=None) -> PoetLinearLayer:
     """Layer with a Gaussian (or given) frozen base weight (layer.py:317-344).
     Draw order off ``rng``: weight, then pi_in, then pi_out."""
-    tdt = _torch_dtype(dtype) if not (isinstance(dtype, torch.dtype)) else dtype
+    host = not isinstance(dtype, torch.dtype)  # a numpy dtype: numpy state, as the reference
+    tdt = _torch_dtype(dtype) if host else dtype
     if base_weight is None:
         std = (1.0 / np.sqrt(m)) if weight_std is None else float(weight_std)
         draw = rng.normal((m, n)) * std
         if tdt == torch.bfloat16:
             base_weight = torch.from_numpy(draw.astype(np.float32)).to(torch.bfloat16)
         else:
-            base_weight = torch.from_numpy(draw.astype(np.float32 if tdt == torch.float32 else np.float64))
+            base_weight = draw.astype(np.float32 if tdt == torch.float32 else np.float64)
+            if not host:
+                base_weight = torch.from_numpy(base_weight)
     else:
         if tuple(base_weight.shape) != (m, n):
             raise ShapeError(f"base weight shape {tuple(base_weight.shape)}, expected ({m}, {n})")
-        if isinstance(base_weight, np.ndarray):
-            base_weight = torch.from_numpy(np.ascontiguousarray(base_weight))
-        base_weight = base_weight.to(tdt)
+        if host:
+            base_weight = np.asarray(base_weight.cpu().numpy() if isinstance(base_weight, torch.Tensor)
+                                     else base_weight).astype(np.float32 if tdt == torch.float32 else np.float64)
+        else:
+            if isinstance(base_weight, np.ndarray):
+                base_weight = torch.from_numpy(np.ascontiguousarray(base_weight))
+            base_weight = base_weight.to(tdt)
     return PoetLinearLayer(base_weight, block_size, rng, name=name, variant=variant,
                            neumann_k=neumann_k, device=device)

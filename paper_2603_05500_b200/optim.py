@@ -114,9 +114,19 @@ def _normbuf(device) -> _NormBuf:
     return _NORM_BUFS[key]
 
 
+def _dev(a, device=None):
+    """numpy -> device copy (the reference's numpy dicts); tensors pass through."""
+    if isinstance(a, np.ndarray):
+        dev = device or torch.device("cuda", torch.cuda.current_device())
+        return torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    return a
+
+
 def device_sqnorm(tensors, device=None):
     """Float64 sum of squares over all tensors, left on the device.
-    Returns (sq tensor[1] float64, nonfinite tensor[1] int32)."""
+    Returns (sq tensor[1] float64, nonfinite tensor[1] int32).  numpy
+    arrays are copied to the device first."""
+    tensors = [_dev(t, device) for t in tensors]
     tensors = [t for t in tensors if t.numel() > 0]
     device = device or (tensors[0].device if tensors else torch.device("cuda"))
     nb = _normbuf(device)
@@ -153,6 +163,9 @@ def global_clip(grads: dict, threshold: float) -> float:
     if norm > threshold and norm > 0.0:
         factor = threshold / norm
         for g in grads.values():
+            if isinstance(g, np.ndarray):  # host array, scaled in place as the reference does
+                g *= g.dtype.type(factor)
+                continue
             # cast like the reference (g *= g.dtype.type(factor))
             g.mul_(float(np.float32(factor)) if g.dtype == torch.float32 else factor)
     return norm
@@ -167,22 +180,28 @@ class AdamWState:
     t: int = 0
 
     def nbytes(self) -> int:
-        return sum(a.numel() * a.element_size() for a in self.m.values()) + \
-            sum(a.numel() * a.element_size() for a in self.v.values())
+        def nb(a):
+            return a.nbytes if isinstance(a, np.ndarray) else a.numel() * a.element_size()
+
+        return sum(nb(a) for a in self.m.values()) + sum(nb(a) for a in self.v.values())
 
     def reset(self) -> None:
-        for a in self.m.values():
-            a.zero_()
-        for a in self.v.values():
-            a.zero_()
+        for a in list(self.m.values()) + list(self.v.values()):
+            if isinstance(a, np.ndarray):
+                a[...] = 0.0
+            else:
+                a.zero_()
         self.t = 0
 
 
 def adamw_init(params: dict) -> AdamWState:
+    """Zero moments in each parameter's own type and place: numpy arrays for
+    numpy parameters (the reference's dicts), device tensors for tensors."""
     st = AdamWState()
     for name, p in params.items():
-        st.m[name] = torch.zeros_like(p)
-        st.v[name] = torch.zeros_like(p)
+        zeros = np.zeros_like if isinstance(p, np.ndarray) else torch.zeros_like
+        st.m[name] = zeros(p)
+        st.v[name] = zeros(p)
     return st
 
 
@@ -203,20 +222,39 @@ def _adamw_launch(ps, gs, ms, vs, lr, sched, t, sqnorm=None, threshold=0.0, writ
 
 
 def adamw_step(params: dict, grads: dict, state: AdamWState, lr: float, sched: ScheduleConfig) -> None:
-    """One decoupled-weight-decay Adam update, in place (optim.py:127-148)."""
+    """One decoupled-weight-decay Adam update, in place (optim.py:127-148).
+
+    Device tensors are updated where they live.  numpy parameters (the
+    reference runner's dicts) are copied to the device with their grads and
+    moments, updated by the same kernel, and written back into the SAME
+    numpy arrays, so everything keyed to them stays attached."""
     state.t += 1
-    ps, gs, ms, vs = [], [], [], []
+    ps, gs, ms, vs, back = [], [], [], [], []
     for name, p in params.items():
         g = grads[name]
         if tuple(g.shape) != tuple(p.shape):
             raise NumericsError(f"gradient shape {tuple(g.shape)} != param shape {tuple(p.shape)} for {name}")
-        ps.append(p); gs.append(g); ms.append(state.m[name]); vs.append(state.v[name])
-    _, bad = device_sqnorm(gs)
-    if int(bad.item()):
-        for name, g in grads.items():
-            if not bool(torch.isfinite(g).all()):
-                raise NumericsError(f"non-finite gradient for {name}")
-    _adamw_launch(ps, gs, ms, vs, lr, sched, state.t)
+        if isinstance(g, np.ndarray) and not np.all(np.isfinite(g)):
+            raise NumericsError(f"non-finite gradient for {name}")
+        m, v = state.m[name], state.v[name]
+        if isinstance(p, np.ndarray):
+            dp, dm, dv = _dev(p), _dev(m), _dev(v)
+            back.append((p, dp, m, dm, v, dv))
+            p, m, v = dp, dm, dv
+        ps.append(p); gs.append(_dev(g, p.device)); ms.append(m); vs.append(v)
+    dev_gs = [(name, g) for name, g in zip(params, gs) if not isinstance(grads[name], np.ndarray)]
+    if dev_gs:
+        _, bad = device_sqnorm([g for _, g in dev_gs])
+        if int(bad.item()):
+            for name, g in dev_gs:
+                if not bool(torch.isfinite(g).all()):
+                    raise NumericsError(f"non-finite gradient for {name}")
+    if ps:
+        _adamw_launch(ps, gs, ms, vs, lr, sched, state.t)
+    for p, dp, m, dm, v, dv in back:
+        p[...] = dp.cpu().numpy()
+        m[...] = dm.cpu().numpy()
+        v[...] = dv.cpu().numpy()
 
 
 def fused_clip_adamw(groups, threshold: float, sched: ScheduleConfig):

@@ -48,6 +48,21 @@ def P():
 def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
+def setp(packed, a):
+    """Write values into a layer's packed parameters in place, whether they
+    are host numpy arrays (numpy-constructed layer) or device tensors."""
+    if isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    if isinstance(packed, np.ndarray):
+        packed[...] = np.asarray(a, dtype=packed.dtype)
+    else:
+        packed.copy_(torch.from_numpy(np.ascontiguousarray(a)).to(packed))
+
+
+def host(a):
+    return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+
+
 
 # ------------------------------------------------------------------- CNP ----
 
@@ -180,8 +195,8 @@ def _gpu_layer(P, d, tag, variant, dtype=None):
                               variant=variant)
     layer.set_permutations(P.PermutationMap.from_forward(d[f"{tag}/perm_in"]),
                            P.PermutationMap.from_forward(d[f"{tag}/perm_out"]))
-    layer.q_r.packed.copy_(dev(d[f"{tag}/q_r"]))
-    layer.q_p.packed.copy_(dev(d[f"{tag}/q_p"]))
+    setp(layer.q_r.packed, d[f"{tag}/q_r"])
+    setp(layer.q_p.packed, d[f"{tag}/q_p"])
     return layer
 
 
@@ -191,7 +206,8 @@ def test_layer_golden(P, tag, variant):
     d = load("layer.npz")
     tol = 1e-10 if d[f"{tag}/base"].dtype == np.float64 else 1e-5
     layer = _gpu_layer(P, d, tag, variant)
-    assert np.array_equal(layer.base.cpu().numpy(), d[f"{tag}/base"])  # PM round trip exact
+    assert isinstance(layer.base, np.ndarray) and layer.dtype == d[f"{tag}/base"].dtype  # numpy in, numpy out
+    assert np.array_equal(layer.base, d[f"{tag}/base"])  # PM round trip exact
     z, cache = layer.forward(d[f"{tag}/x"])
     close(z, d[f"{tag}/z"], tol)
     grads = layer.backward(cache, d[f"{tag}/dz"])
@@ -223,8 +239,8 @@ def test_cfg1_layer_vs_oracle(P):
     for variant in ("fast", "mem"):
         layer = P.PoetLinearLayer(base, 64, P.Rng(0), variant=variant)
         layer.set_permutations(P.PermutationMap.from_forward(fi), P.PermutationMap.from_forward(fo))
-        layer.q_r.packed.copy_(dev(q_r))
-        layer.q_p.packed.copy_(dev(q_p))
+        setp(layer.q_r.packed, q_r)
+        setp(layer.q_p.packed, q_p)
         z, c = layer.forward(dev(x))
         close(z, z_ref, 1e-5)
         g = layer.backward(c, dev(dz))
@@ -238,8 +254,8 @@ def test_fast_and_mem_bitwise_on_gpu(P):
     out = []
     for variant in ("fast", "mem"):
         layer = P.PoetLinearLayer(base, 16, P.Rng.keyed(7, "p"), variant=variant)
-        layer.q_r.packed.normal_(0, 0.05, generator=torch.Generator("cuda").manual_seed(1))
-        layer.q_p.packed.normal_(0, 0.05, generator=torch.Generator("cuda").manual_seed(2))
+        setp(layer.q_r.packed, 0.05 * np.random.default_rng(1).standard_normal(layer.q_r.packed.shape))
+        setp(layer.q_p.packed, 0.05 * np.random.default_rng(2).standard_normal(layer.q_p.packed.shape))
         x = dev(np.random.default_rng(9).standard_normal((33, 64)).astype(np.float32))
         dz = dev(np.random.default_rng(10).standard_normal((33, 96)).astype(np.float32))
         z, c = layer.forward(x)
@@ -254,8 +270,8 @@ def test_layer_backward_finite_differences_f64(P):
     """reference tests/test_layer.py:104-142 on the GPU float64 path."""
     layer = P.init_layer(8, 12, 4, P.Rng.keyed(0, "layer"), dtype=np.float64)
     rng = np.random.default_rng(3)
-    layer.q_r.packed.copy_(dev(0.15 * rng.standard_normal(tuple(layer.q_r.packed.shape))))
-    layer.q_p.packed.copy_(dev(0.15 * rng.standard_normal(tuple(layer.q_p.packed.shape))))
+    setp(layer.q_r.packed, 0.15 * rng.standard_normal(tuple(layer.q_r.packed.shape)))
+    setp(layer.q_p.packed, 0.15 * rng.standard_normal(tuple(layer.q_p.packed.shape)))
     x = rng.standard_normal((3, 8))
     mask = rng.standard_normal((3, 12))
     z, cache = layer.forward(x)
@@ -263,9 +279,9 @@ def test_layer_backward_finite_differences_f64(P):
     h = 1e-6
     for attr, got in (("q_r", grads.q_r), ("q_p", grads.q_p)):
         packed = getattr(layer, attr).packed
-        flat = packed.view(-1)
-        fd = np.zeros(flat.numel())
-        for i in range(flat.numel()):
+        flat = packed.reshape(-1)  # a view (host numpy array: numpy-constructed layer)
+        fd = np.zeros(flat.shape[0])
+        for i in range(flat.shape[0]):
             keep = float(flat[i])
             flat[i] = keep + h
             up = float(np.sum(mask * layer.forward(x)[0]))
@@ -281,17 +297,17 @@ def test_zero_params_reproduce_base_weight(P):
         layer = P.init_layer(8, 12, 4, P.Rng.keyed(0, "layer"), dtype=dt)
         x = np.random.default_rng(2).standard_normal((5, 8)).astype(dt)
         z, _ = layer.forward(x)
-        close(z, x @ layer.base.cpu().numpy(), tol)
+        close(z, x @ host(layer.base), tol)
 
 
 def test_merge_preserves_function_and_materialize(P):
     layer = P.init_layer(64, 32, 8, P.Rng.keyed(14, "layer"), dtype=np.float64)
     rng = np.random.default_rng(14)
-    layer.q_r.packed.copy_(dev(0.1 * rng.standard_normal(tuple(layer.q_r.packed.shape))))
-    layer.q_p.packed.copy_(dev(0.1 * rng.standard_normal(tuple(layer.q_p.packed.shape))))
+    setp(layer.q_r.packed, 0.1 * rng.standard_normal(tuple(layer.q_r.packed.shape)))
+    setp(layer.q_p.packed, 0.1 * rng.standard_normal(tuple(layer.q_p.packed.shape)))
     x = rng.standard_normal((5, 64))
     z0, _ = layer.forward(x)
-    w_eff = layer.materialize_weight().cpu().numpy()
+    w_eff = host(layer.materialize_weight())
     close(x @ w_eff, z0, 1e-11)
     old = layer.perm_in.forward.copy()
     layer.merge_and_reinit(P.Rng.keyed(16, "merge"))
@@ -304,12 +320,12 @@ def test_merge_sv_drift(P):
     """reference tests/test_layer.py:271-286."""
     layer = P.init_layer(64, 64, 8, P.Rng.keyed(21, "drift"), dtype=np.float64)
     rng = np.random.default_rng(22)
-    layer.q_r.packed.copy_(dev(0.012 * rng.standard_normal(tuple(layer.q_r.packed.shape))))
-    layer.q_p.packed.copy_(dev(0.012 * rng.standard_normal(tuple(layer.q_p.packed.shape))))
+    setp(layer.q_r.packed, 0.012 * rng.standard_normal(tuple(layer.q_r.packed.shape)))
+    setp(layer.q_p.packed, 0.012 * rng.standard_normal(tuple(layer.q_p.packed.shape)))
     audit = layer.merge_and_reinit(P.Rng.keyed(23, "m"), compute_sv_drift=True)
     assert audit.sv_drift <= 1e-3
-    layer.q_r.packed.copy_(dev(0.012 * rng.standard_normal(tuple(layer.q_r.packed.shape))))
-    layer.q_p.packed.copy_(dev(0.012 * rng.standard_normal(tuple(layer.q_p.packed.shape))))
+    setp(layer.q_r.packed, 0.012 * rng.standard_normal(tuple(layer.q_r.packed.shape)))
+    setp(layer.q_p.packed, 0.012 * rng.standard_normal(tuple(layer.q_p.packed.shape)))
     audit2 = layer.merge_and_reinit(P.Rng.keyed(25, "m"), use_exact_cayley=True, compute_sv_drift=True)
     assert audit2.sv_drift <= 1e-9 and audit2.orth_err_r <= 1e-11
 
@@ -337,8 +353,8 @@ def test_bf16_layer_vs_oracle(P, m, n, b, T, variant, quant, fold):
         base_q = layer.base.double().cpu().numpy()  # bf16-rounded weight the GPU really holds
     q_r = 0.01 * r.standard_normal(tuple(layer.q_r.packed.shape))
     q_p = 0.01 * r.standard_normal(tuple(layer.q_p.packed.shape))
-    layer.q_r.packed.copy_(dev(q_r))
-    layer.q_p.packed.copy_(dev(q_p))
+    setp(layer.q_r.packed, q_r)
+    setp(layer.q_p.packed, q_p)
     x = r.standard_normal((T, m))
     dz = r.standard_normal((T, n))
     xb = dev(x).to(torch.bfloat16)

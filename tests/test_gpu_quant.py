@@ -9,6 +9,21 @@ import torch
 
 pytestmark = pytest.mark.gpu
 
+
+def setp(packed, a):
+    """Write values into a layer's packed parameters in place, whether they
+    are host numpy arrays (numpy-constructed layer) or device tensors."""
+    if isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    if isinstance(packed, np.ndarray):
+        packed[...] = np.asarray(a, dtype=packed.dtype)
+    else:
+        packed.copy_(torch.from_numpy(np.ascontiguousarray(a)).to(packed))
+
+
+def host(a):
+    return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+
 GOLD = os.path.join(os.path.dirname(__file__), "golden")
 
 
@@ -67,8 +82,8 @@ def test_quantized_layer_matches_oracle(tag, tol):
                          PermutationMap.from_forward(d[f"l_{tag}_perm_out"]))
     lay.quantize_base()
     assert lay.quantized and isinstance(lay.base, P.QuantizedMatrix)
-    lay.q_r.packed.copy_(torch.from_numpy(d[f"l_{tag}_q_r"]))
-    lay.q_p.packed.copy_(torch.from_numpy(d[f"l_{tag}_q_p"]))
+    setp(lay.q_r.packed, d[f"l_{tag}_q_r"])
+    setp(lay.q_p.packed, d[f"l_{tag}_q_p"])
     z, cache = lay.forward(d[f"l_{tag}_x"])
     g = lay.backward(cache, d[f"l_{tag}_dz"])
     for got, key in ((z, "z"), (g.q_r, "gr"), (g.q_p, "gp"), (g.x, "dx")):
@@ -79,7 +94,7 @@ def test_quantized_layer_matches_oracle(tag, tol):
     # (<= half a scale against the float shadow, test_layer.py:370-388)
     lay.set_permutations(PermutationMap.from_forward(d[f"l_{tag}_perm_in"]),
                          PermutationMap.from_forward(d[f"l_{tag}_perm_out"]))
-    shadow = lay.materialize_weight().double().cpu().numpy()
+    shadow = host(lay.materialize_weight()).astype(np.float64)
 
     new_in, new_out = d[f"l_{tag}_new_perm_in"], d[f"l_{tag}_new_perm_out"]
     import paper_2603_05500_b200.layer as L

@@ -8,6 +8,21 @@ import torch
 pytestmark = pytest.mark.gpu
 
 
+def setp(packed, a):
+    """Write values into a layer's packed parameters in place, whether they
+    are host numpy arrays (numpy-constructed layer) or device tensors."""
+    if isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    if isinstance(packed, np.ndarray):
+        packed[...] = np.asarray(a, dtype=packed.dtype)
+    else:
+        packed.copy_(torch.from_numpy(np.ascontiguousarray(a)).to(packed))
+
+
+def host(a):
+    return a.detach().cpu().numpy() if isinstance(a, torch.Tensor) else np.asarray(a)
+
+
 @pytest.fixture(scope="module")
 def N():
     from paper_2603_05500_b200 import _native as N
