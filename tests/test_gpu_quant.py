@@ -114,7 +114,7 @@ def test_quantized_layer_matches_oracle(tag, tol):
     same = np.mean(codes == d[f"l_{tag}_merged_codes"])
     assert same >= 0.995, same
     assert np.allclose(scales, d[f"l_{tag}_merged_scales"], rtol=1e-5)
-    assert np.all(lay.q_r.packed.cpu().numpy() == 0)
+    assert np.all(host(lay.q_r.packed) == 0)
 
 
 def test_quantized_llama_trains_and_checkpoints(tmp_path):
