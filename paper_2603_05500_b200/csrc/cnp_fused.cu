@@ -344,7 +344,9 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
       float* out = dpacked + s * PAIRS;
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
-        if (c + 31 <= i) continue;  // no upper-triangle entry in this chunk
+        // no upper-triangle entry for any row of this warp: skip (warp-uniform,
+        // tcgen05.ld is .sync.aligned)
+        if (c + 31 <= i - lane) continue;
         float v[32], a[32], t[32];
         tmem_ld(A1 + tl + c, v);
         dg_rowcol32<B>(n1, i, c, a, t);
