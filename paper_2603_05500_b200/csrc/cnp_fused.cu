@@ -53,15 +53,17 @@ using namespace tc;
 
 constexpr int THREADS = 256;
 constexpr uint32_t NEG_A = 1u << 13, NEG_B = 1u << 14;
-
 template <int B>
 struct Cfg {
   static constexpr bool PAIR = B == 256;
-  static constexpr int SLAB = 128 * B * 2;  // 128 rows x b bf16
-  static constexpr int SMEM = 3 * SLAB + 1024 + 64;
+  static constexpr int SLAB = 128 * B * 2;       // 128 rows x b bf16 (K-major, SW128)
+  static constexpr int TILE = 32 * 33 * 4;       // per-warp 32 x 32 fp32 transpose tile
+  static constexpr int SMEM = 3 * SLAB + 8 * TILE + 1024 + 64;
   static constexpr int TMEM_COLS = 2 * B;
   static constexpr uint32_t IDESC = idesc_bf16(PAIR ? 256 : 128, B, false, false);
-  static constexpr int HALF = B / 2;  // columns per thread (two threads per row)
+  static constexpr int HALF = B / 2;             // columns per thread in thread-per-row phases
+  static constexpr int PITCH = B + 4;            // fp32 staging row pitch (floats), bank-spread
+  static_assert(128 * PITCH * 4 <= 3 * SLAB, "fp32 staging must fit in the operand slabs");
 };
 
 __device__ __forceinline__ int64_t pidx(int64_t i, int64_t j, int64_t b) {
@@ -71,6 +73,9 @@ __device__ __forceinline__ int64_t pidx(int64_t i, int64_t j, int64_t b) {
 // byte offset of element (r, j) (j % 8 == 0) in a K-major SW128 slab of 128 rows
 __device__ __forceinline__ uint32_t soff(int r, int j) {
   return static_cast<uint32_t>((j >> 6) * 16384 + r * 128 + ((((j & 63) >> 3) ^ (r & 7)) << 4));
+}
+__device__ __forceinline__ void put1(uint8_t* slab, int r, int j, float v) {
+  *reinterpret_cast<__nv_bfloat16*>(slab + soff(r, j & ~7) + (j & 7) * 2) = __float2bfloat16_rn(v);
 }
 __device__ __forceinline__ void store32(uint8_t* slab, int r, int j0, const float (&v)[32]) {
 #pragma unroll
@@ -99,27 +104,40 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[32]) {
   tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
 }
 
-// Q[i, j0 .. j0+31] in fp32 from the packed strict upper triangle
+// Q rows [lo, lo + 128) of one block, bf16, into a slab -- warp-cooperative so
+// every global read is a coalesced run of one packed row (the packed strict
+// upper triangle is row-contiguous, cnp.py:66-68).  Packed row j supplies
+// Q[j, i] = p (when j is one of this CTA's rows) and Q[i, j] = -p (when i is).
 template <int B>
-__device__ __forceinline__ void q_row32(const float* __restrict__ pk, int i, int j0, float (&v)[32]) {
-#pragma unroll
-  for (int q = 0; q < 32; ++q) {
-    const int j = j0 + q;
-    v[q] = j > i ? __ldg(pk + pidx(i, j, B)) : (j < i ? -__ldg(pk + pidx(j, i, B)) : 0.f);
+__device__ __forceinline__ void unpack_q(uint8_t* slab, const float* __restrict__ pk, int lo, int warp, int lane) {
+  const int hi = lo + 128;
+  for (int j = warp; j < hi; j += 8) {
+    const int i0 = j < lo ? lo : j + 1;
+    const float* row = pk + pidx(j, j + 1, B) - (j + 1);  // row[i] = p(j, i)
+    for (int i = i0 + lane; i < B; i += 32) {
+      const float p = __ldg(row + i);
+      if (j >= lo) put1(slab, j - lo, i, p);
+      if (i < hi) put1(slab, i - lo, j, -p);
+    }
   }
+  if (warp == 0)
+    for (int r = lane; r < 128; r += 32) put1(slab, r, lo + r, 0.f);
 }
-// N1[i, j0..] (row, float4) and N1[j0.., i] (column: coalesced across the warp's rows)
+
+// 32 x 32 tile of N1 = dG at rows i0.., columns j0..: lane x gets, for every
+// y, a[y] = N1[i0 + y, j0 + x] and t[y] = N1[j0 + x, i0 + y]; both read as
+// coalesced 128-byte rows, the transposed one through the warp's smem tile.
 template <int B>
-__device__ __forceinline__ void dg_rowcol32(const float* __restrict__ dg, int i, int j0, float (&a)[32],
-                                            float (&t)[32]) {
-  const float4* row = reinterpret_cast<const float4*>(dg + static_cast<int64_t>(i) * B + j0);
+__device__ __forceinline__ void dg_tile(const float* __restrict__ n1, int i0, int j0, int lane, float* tile,
+                                        float (&a)[32], float (&t)[32]) {
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    const float4 x = __ldg(row + q);
-    a[4 * q] = x.x; a[4 * q + 1] = x.y; a[4 * q + 2] = x.z; a[4 * q + 3] = x.w;
-  }
+  for (int y = 0; y < 32; ++y) a[y] = __ldg(n1 + static_cast<int64_t>(i0 + y) * B + j0 + lane);
 #pragma unroll
-  for (int q = 0; q < 32; ++q) t[q] = __ldg(dg + static_cast<int64_t>(j0 + q) * B + i);
+  for (int y = 0; y < 32; ++y) tile[y * 33 + lane] = __ldg(n1 + static_cast<int64_t>(j0 + y) * B + i0 + lane);
+  __syncwarp();
+#pragma unroll
+  for (int y = 0; y < 32; ++y) t[y] = tile[lane * 33 + y];
+  __syncwarp();
 }
 
 // one b x b x b product into TMEM column offset d (leader thread)
@@ -144,20 +162,24 @@ __device__ __forceinline__ void commit(uint64_t* bar) {
     umma_commit(bar);
 }
 
+template <int B>
+__device__ __forceinline__ void cta_sync() {
+  if constexpr (Cfg<B>::PAIR)
+    pair::cluster_sync();
+  else
+    __syncthreads();
+}
+
 // every thread's smem / TMEM writes are visible to the tensor core, and both
 // CTAs of a pair have arrived, before the leader issues the next products
 template <int B>
 __device__ __forceinline__ void publish() {
   fence_async_smem();
   fence_before();
-  if constexpr (Cfg<B>::PAIR)
-    pair::cluster_sync();
-  else
-    __syncthreads();
+  cta_sync<B>();
   fence_after();
 }
 
-template <int B>
 __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
   mbar_wait(bar, phase);
   phase ^= 1;
@@ -176,16 +198,18 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
   uint8_t* S0 = smem;
   uint8_t* S1 = smem + CF::SLAB;
   uint8_t* S2 = smem + 2 * CF::SLAB;
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * CF::SLAB);
+  float* stage = reinterpret_cast<float*>(smem);  // fp32 staging over the slabs (final phase)
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  float* tile = reinterpret_cast<float*>(smem + 3 * CF::SLAB) + warp * (32 * 33);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * CF::SLAB + 8 * CF::TILE);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = CF::PAIR ? pair::cta_rank() : 0;
   const bool issuer = rank == 0 && threadIdx.x == 0;
   const int64_t unit = CF::PAIR ? blockIdx.x / 2 : blockIdx.x;
   const int64_t units = CF::PAIR ? gridDim.x / 2 : gridDim.x;
+  const int lo = static_cast<int>(rank) * 128;     // this CTA's rows of the b x b block
   const int r = (warp & 3) * 32 + lane;           // TMEM lane = row within this CTA's 128
-  const int i = static_cast<int>(rank) * 128 + r;  // row within the b x b block
   const int c_lo = (warp >> 2) * CF::HALF;         // this thread's column half
 
   if (threadIdx.x == 0) {
@@ -206,10 +230,10 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
     }
   }
   fence_before();
-  if constexpr (CF::PAIR) pair::cluster_sync(); else __syncthreads();
+  cta_sync<B>();
   fence_after();
   const uint32_t tmem = *tmem_slot;
-  const uint32_t A0 = tmem, A1 = tmem + B;                 // accumulators (columns)
+  const uint32_t A0 = tmem, A1 = tmem + B;                           // accumulators (columns)
   const uint32_t tl = static_cast<uint32_t>((warp & 3) * 32) << 16;  // this warp's TMEM lanes
   const uint32_t s0 = smem_u32(S0), s1 = smem_u32(S1), s2 = smem_u32(S2);
   uint32_t phase = 0;
@@ -219,19 +243,14 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
     const float* pk = packed + s * PAIRS;
     if constexpr (FWD) {
       // ---- S0 <- Q
-#pragma unroll 1
-      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
-        float v[32];
-        q_row32<B>(pk, i, c, v);
-        store32(S0, r, c, v);
-      }
+      unpack_q<B>(S0, pk, lo, warp, lane);
       publish<B>();
       if (issuer) {
-        mma<B>(A0, s0, s0, NEG_B, false);  // Q Q = Q (-Q)^T
+        mma<B>(A0, s0, s0, NEG_B, false);  // Q Q = S0 (-S0)^T
         commit<B>(bar);
       }
-      wait_mma<B>(bar, phase);
-      // ---- S1 <- Q^2 ; S2 <- Q^2 - 2Q (rows of H^T)
+      wait_mma(bar, phase);
+      // ---- S1 <- Q^2 ; S2 <- Q^2 - 2Q (rows of H^T, H = 2Q + Q^2)
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
         float q2[32], q[32];
@@ -247,31 +266,21 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
         mma<B>(A1, s1, s2, 0, false);  // Q^2 H = 2 Q^3 + Q^4
         commit<B>(bar);
       }
-      wait_mma<B>(bar, phase);
-      // ---- G = I + 2Q + 2Q^2 + (2Q^3 + Q^4)
-      const int64_t grow = (s * B + i) * B;
+      wait_mma(bar, phase);
+      // ---- G = I + 2 (Q + Q^2) + (2 Q^3 + Q^4), staged bf16 in S1 (free now)
+      const int64_t grow = (s * B + lo + r) * B;
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
         float q[32], q2[32], p[32];
-        q_row32<B>(pk, i, c, q);
+        load32(S0, r, c, q);  // Q as the bf16 operand (2Q: exact in bf16)
         tmem_ld(A0 + tl + c, q2);
         tmem_ld(A1 + tl + c, p);
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
           p[k] = 2.f * (q[k] + q2[k]) + p[k];
-          if (c + k == i) p[k] += 1.f;
+          if (c + k == lo + r) p[k] += 1.f;
         }
-        if (g16) {
-#pragma unroll
-          for (int q8 = 0; q8 < 4; ++q8) {
-            uint4 u;
-            u.x = pack_bf16(__float_as_uint(p[8 * q8 + 0]), __float_as_uint(p[8 * q8 + 1]));
-            u.y = pack_bf16(__float_as_uint(p[8 * q8 + 2]), __float_as_uint(p[8 * q8 + 3]));
-            u.z = pack_bf16(__float_as_uint(p[8 * q8 + 4]), __float_as_uint(p[8 * q8 + 5]));
-            u.w = pack_bf16(__float_as_uint(p[8 * q8 + 6]), __float_as_uint(p[8 * q8 + 7]));
-            *reinterpret_cast<uint4*>(g16 + grow + c + 8 * q8) = u;
-          }
-        }
+        if (g16) store32(S1, r, c, p);
         if (g32) {
 #pragma unroll
           for (int q4 = 0; q4 < 8; ++q4)
@@ -279,34 +288,41 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
                 make_float4(p[4 * q4], p[4 * q4 + 1], p[4 * q4 + 2], p[4 * q4 + 3]);
         }
       }
-      // the next block's unpack overwrites S0 only after its publish: the reads
-      // of A0/A1 above completed (tcgen05.wait::ld) before that barrier
+      if (g16) {
+        __syncthreads();
+        // one 16-byte unit per lane: each warp instruction writes a coalesced row
+        __nv_bfloat16* gb = g16 + (s * B + lo) * B;
+        for (int e = threadIdx.x; e < 128 * (B / 8); e += THREADS) {
+          const int row = e / (B / 8), u = e % (B / 8);
+          *reinterpret_cast<uint4*>(gb + static_cast<int64_t>(row) * B + 8 * u) =
+              *reinterpret_cast<const uint4*>(S1 + soff(row, 8 * u));
+        }
+      }
+      // the next block's unpack overwrites S0 / S1 only after this CTA's
+      // threads passed the publish barrier, i.e. after these reads
+      __syncthreads();
     } else {
       const float* n1 = dg + s * static_cast<int64_t>(B) * B;
       // ---- S0 <- Q ; S1 <- E = N1 - N1^T ; S2 <- F = N1 + N1^T
-#pragma unroll 1
-      for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
+      unpack_q<B>(S0, pk, lo, warp, lane);
+      for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
+        const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
         float a[32], t[32];
-        q_row32<B>(pk, i, c, a);
-        store32(S0, r, c, a);
-        dg_rowcol32<B>(n1, i, c, a, t);
-        float e[32];
+        dg_tile<B>(n1, i0, j0, lane, tile, a, t);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          e[k] = a[k] - t[k];
-          a[k] = a[k] + t[k];
+        for (int y = 0; y < 32; ++y) {
+          put1(S1, i0 - lo + y, j0 + lane, a[y] - t[y]);
+          put1(S2, i0 - lo + y, j0 + lane, a[y] + t[y]);
         }
-        store32(S1, r, c, e);
-        store32(S2, r, c, a);
       }
       publish<B>();
       if (issuer) {
-        mma<B>(A0, s0, s1, NEG_B, false);           // Q E = Q (-E)^T
-        mma<B>(A1, s2, s0, 0, false);               // -(F Q) = F S0^T   (Q = -S0^T)
-        mma<B>(A1, s0, s2, NEG_A, true);            // -(Q F) = (-S0) S2^T (F = F^T)
+        mma<B>(A0, s0, s1, NEG_B, false);  // Q E = S0 (-S1)^T          (E = -E^T)
+        mma<B>(A1, s2, s0, 0, false);      // -(F Q) = S2 S0^T          (Q = -S0^T)
+        mma<B>(A1, s0, s2, NEG_A, true);   // -(Q F) = (-S0) S2^T       (F = F^T)
         commit<B>(bar);
       }
-      wait_mma<B>(bar, phase);
+      wait_mma(bar, phase);
       // ---- S2 <- Q E ; S1 <- Z = E + A1 / 2
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
@@ -325,7 +341,7 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
         mma<B>(A1, s2, s0, NEG_B, true);   // += (Q E) Q
         commit<B>(bar);
       }
-      wait_mma<B>(bar, phase);
+      wait_mma(bar, phase);
       // ---- S0 <- Q^2
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
@@ -335,36 +351,49 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
       }
       publish<B>();
       if (issuer) {
-        mma<B>(A1, s1, s0, 0, true);      // += Z Q^2
-        mma<B>(A1, s0, s1, NEG_B, true);  // += Q^2 Z = Q^2 (-Z)^T
+        mma<B>(A1, s1, s0, 0, true);      // += Z Q^2        (Q^2 = (Q^2)^T)
+        mma<B>(A1, s0, s1, NEG_B, true);  // += Q^2 Z = Q^2 (-S1)^T
         commit<B>(bar);
       }
-      wait_mma<B>(bar, phase);
-      // ---- g_ij = 2 E_ij + 2 A1_ij, i < j (E in fp32 from dG)
-      float* out = dpacked + s * PAIRS;
+      wait_mma(bar, phase);
+      // ---- stage A1 (fp32, thread per row) over the slabs, then per 32 x 32
+      // tile of the upper triangle g_ij = 2 (E_ij + A1_ij) written as coalesced
+      // runs of the packed rows (E in fp32 from dG)
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
-        // no upper-triangle entry for any row of this warp: skip (warp-uniform,
-        // tcgen05.ld is .sync.aligned)
-        if (c + 31 <= i - lane) continue;
-        float v[32], a[32], t[32];
+        float v[32];
         tmem_ld(A1 + tl + c, v);
-        dg_rowcol32<B>(n1, i, c, a, t);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) {
-          const int j = c + k;
+        for (int q4 = 0; q4 < 8; ++q4)
+          *reinterpret_cast<float4*>(stage + r * CF::PITCH + c + 4 * q4) =
+              make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+      }
+      __syncthreads();
+      float* out = dpacked + s * PAIRS;
+      for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
+        const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
+        if (j0 + 31 <= i0) continue;  // tile entirely on/below the diagonal (warp-uniform)
+        float a[32], t[32];
+        dg_tile<B>(n1, i0, j0, lane, tile, a, t);
+        const int j = j0 + lane;
+#pragma unroll
+        for (int y = 0; y < 32; ++y) {
+          const int i = i0 + y;
           if (j > i) {
-            const float gv = 2.f * ((a[k] - t[k]) + v[k]);
+            const float gv = 2.f * ((a[y] - t[y]) + stage[(i - lo) * CF::PITCH + j]);
             float* dst = out + pidx(i, j, B);
             *dst = accumulate ? *dst + gv : gv;
           }
         }
       }
+      // the next block's unpack overwrites the staging only after every warp
+      // of this CTA is done reading it
+      __syncthreads();
     }
   }
 
   fence_before();
-  if constexpr (CF::PAIR) pair::cluster_sync(); else __syncthreads();
+  cta_sync<B>();
   fence_after();
   if (warp == 2) {
     if constexpr (CF::PAIR)
@@ -404,7 +433,12 @@ int launch(int64_t nb, const float* packed, const float* dg, __nv_bfloat16* g16,
     cudaLaunchKernelEx(&cfg, kern, nb, packed, dg, g16, g32, dpacked, accumulate);
     prof_end(pf, FWD ? "cnp_fused_fwd" : "cnp_fused_bwd", (FWD ? 2.0 : 7.0) * 2.0 * B * B * B * nb, st);
   } else {
-    const int64_t ctas = nb < 2 * sms ? nb : 2 * sms;
+    static int per_sm = [&] {
+      int n = 1;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, THREADS, CF::SMEM);
+      return n < 1 ? 1 : n;
+    }();
+    const int64_t ctas = nb < per_sm * sms ? nb : per_sm * sms;
     grid = static_cast<unsigned>(ctas);
     void* pf = prof_begin(st);
     kern<<<grid, THREADS, CF::SMEM, st>>>(nb, packed, dg, g16, g32, dpacked, accumulate);
