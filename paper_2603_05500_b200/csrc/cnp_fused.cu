@@ -111,13 +111,33 @@ __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[32]) {
 template <int B>
 __device__ __forceinline__ void unpack_q(uint8_t* slab, const float* __restrict__ pk, int lo, int warp, int lane) {
   const int hi = lo + 128;
-  for (int j = warp; j < hi; j += 8) {
-    const int i0 = j < lo ? lo : j + 1;
-    const float* row = pk + pidx(j, j + 1, B) - (j + 1);  // row[i] = p(j, i)
-    for (int i = i0 + lane; i < B; i += 32) {
-      const float p = __ldg(row + i);
-      if (j >= lo) put1(slab, j - lo, i, p);
-      if (i < hi) put1(slab, i - lo, j, -p);
+  constexpr int NI = B / 32;  // 32-wide runs per packed row (at most)
+  constexpr int NR = 4;       // packed rows per pass: NR * NI independent loads in flight
+  for (int j0 = warp; j0 < hi; j0 += 8 * NR) {
+    float v[NR][NI];
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int j = j0 + 8 * q;
+      const int i0 = j < lo ? lo : j + 1;
+      const float* row = pk + pidx(j, j + 1, B) - (j + 1);  // row[i] = p(j, i)
+#pragma unroll
+      for (int k = 0; k < NI; ++k) {
+        const int i = i0 + lane + 32 * k;
+        v[q][k] = (j < hi && i < B) ? __ldg(row + i) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < NR; ++q) {
+      const int j = j0 + 8 * q;
+      const int i0 = j < lo ? lo : j + 1;
+#pragma unroll
+      for (int k = 0; k < NI; ++k) {
+        const int i = i0 + lane + 32 * k;
+        if (j < hi && i < B) {
+          if (j >= lo) put1(slab, j - lo, i, v[q][k]);
+          if (i < hi) put1(slab, i - lo, j, -v[q][k]);
+        }
+      }
     }
   }
   if (warp == 0)
