@@ -74,9 +74,6 @@ __device__ __forceinline__ int64_t pidx(int64_t i, int64_t j, int64_t b) {
 __device__ __forceinline__ uint32_t soff(int r, int j) {
   return static_cast<uint32_t>((j >> 6) * 16384 + r * 128 + ((((j & 63) >> 3) ^ (r & 7)) << 4));
 }
-__device__ __forceinline__ void put1(uint8_t* slab, int r, int j, float v) {
-  *reinterpret_cast<__nv_bfloat16*>(slab + soff(r, j & ~7) + (j & 7) * 2) = __float2bfloat16_rn(v);
-}
 __device__ __forceinline__ void store32(uint8_t* slab, int r, int j0, const float (&v)[32]) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -103,45 +100,72 @@ __device__ __forceinline__ void load32(const uint8_t* slab, int r, int j0, float
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[32]) {
   tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
 }
+// distributed shared memory: the peer CTA's copy of a shared address
+__device__ __forceinline__ uint32_t peer_addr(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float ld_cluster(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
+  return v;
+}
 
-// Q rows [lo, lo + 128) of one block, bf16, into a slab -- warp-cooperative so
-// every global read is a coalesced run of one packed row (the packed strict
-// upper triangle is row-contiguous, cnp.py:66-68).  Packed row j supplies
-// Q[j, i] = p (when j is one of this CTA's rows) and Q[i, j] = -p (when i is).
+// Column j0 + lane of rows rr0 .. rr0 + 31 of a slab <- v[0 .. 31] (bf16):
+// rr0 % 8 == 0, j0 % 32 == 0, so the swizzle term is a per-y constant XOR.
+__device__ __forceinline__ void tile_put(uint8_t* slab, int rr0, int j0, int lane, const float (&v)[32]) {
+  const int col = j0 + lane;
+  uint8_t* base = slab + (col >> 6) * 16384 + rr0 * 128 + (col & 7) * 2;
+  const int unit = (col & 63) >> 3;
+#pragma unroll
+  for (int y = 0; y < 32; ++y)
+    *reinterpret_cast<__nv_bfloat16*>(base + y * 128 + ((unit ^ (y & 7)) << 4)) = __float2bfloat16_rn(v[y]);
+}
+
+// 32 x 32 tile (rows i0.., columns j0..) of Q from the packed strict upper
+// triangle (row-contiguous, cnp.py:66-68): lane x gets v[y] = Q[i0 + y, j0 + x].
+// Upper entries p(i, j) are read along packed row i (coalesced across lanes);
+// lower entries -p(j, i) are read along packed row j (coalesced) into the
+// warp's smem tile and transposed.
 template <int B>
-__device__ __forceinline__ void unpack_q(uint8_t* slab, const float* __restrict__ pk, int lo, int warp, int lane) {
-  const int hi = lo + 128;
-  constexpr int NI = B / 32;  // 32-wide runs per packed row (at most)
-  constexpr int NR = 4;       // packed rows per pass: NR * NI independent loads in flight
-  for (int j0 = warp; j0 < hi; j0 += 8 * NR) {
-    float v[NR][NI];
+__device__ __forceinline__ void q_tile(const float* __restrict__ pk, int i0, int j0, int lane, float* tile,
+                                       float (&v)[32]) {
+  const int x = lane;
+  if (j0 + 31 > i0) {  // some entry above the diagonal
 #pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const int j = j0 + 8 * q;
-      const int i0 = j < lo ? lo : j + 1;
-      const float* row = pk + pidx(j, j + 1, B) - (j + 1);  // row[i] = p(j, i)
-#pragma unroll
-      for (int k = 0; k < NI; ++k) {
-        const int i = i0 + lane + 32 * k;
-        v[q][k] = (j < hi && i < B) ? __ldg(row + i) : 0.f;
-      }
+    for (int y = 0; y < 32; ++y) {
+      const int i = i0 + y, j = j0 + x;
+      v[y] = j > i ? __ldg(pk + pidx(i, j, B)) : 0.f;
     }
+  } else {
 #pragma unroll
-    for (int q = 0; q < NR; ++q) {
-      const int j = j0 + 8 * q;
-      const int i0 = j < lo ? lo : j + 1;
-#pragma unroll
-      for (int k = 0; k < NI; ++k) {
-        const int i = i0 + lane + 32 * k;
-        if (j < hi && i < B) {
-          if (j >= lo) put1(slab, j - lo, i, v[q][k]);
-          if (i < hi) put1(slab, i - lo, j, -v[q][k]);
-        }
-      }
-    }
+    for (int y = 0; y < 32; ++y) v[y] = 0.f;
   }
-  if (warp == 0)
-    for (int r = lane; r < 128; r += 32) put1(slab, r, lo + r, 0.f);
+  if (j0 < i0 + 31) {  // some entry below the diagonal
+#pragma unroll
+    for (int y = 0; y < 32; ++y) {
+      const int j = j0 + y, i = i0 + x;  // packed row j, column i
+      tile[y * 33 + x] = i > j ? __ldg(pk + pidx(j, i, B)) : 0.f;
+    }
+    __syncwarp();
+#pragma unroll
+    for (int y = 0; y < 32; ++y) v[y] -= tile[x * 33 + y];  // -p(j0 + x, i0 + y)
+    __syncwarp();
+  }
+}
+
+// Q rows [lo, lo + 128) of one block, bf16, into a slab, one 32 x 32 tile per
+// warp pass (all global reads coalesced)
+template <int B>
+__device__ __forceinline__ void unpack_q(uint8_t* slab, const float* __restrict__ pk, int lo, int warp, int lane,
+                                         float* tile) {
+  for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
+    const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
+    float v[32];
+    q_tile<B>(pk, i0, j0, lane, tile, v);
+    tile_put(slab, i0 - lo, j0, lane, v);
+  }
 }
 
 // 32 x 32 tile of N1 = dG at rows i0.., columns j0..: lane x gets, for every
@@ -263,7 +287,7 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
     const float* pk = packed + s * PAIRS;
     if constexpr (FWD) {
       // ---- S0 <- Q
-      unpack_q<B>(S0, pk, lo, warp, lane);
+      unpack_q<B>(S0, pk, lo, warp, lane, tile);
       publish<B>();
       if (issuer) {
         mma<B>(A0, s0, s0, NEG_B, false);  // Q Q = S0 (-S0)^T
@@ -324,16 +348,19 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
     } else {
       const float* n1 = dg + s * static_cast<int64_t>(B) * B;
       // ---- S0 <- Q ; S1 <- E = N1 - N1^T ; S2 <- F = N1 + N1^T
-      unpack_q<B>(S0, pk, lo, warp, lane);
+      unpack_q<B>(S0, pk, lo, warp, lane, tile);
       for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
         const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
         float a[32], t[32];
         dg_tile<B>(n1, i0, j0, lane, tile, a, t);
 #pragma unroll
         for (int y = 0; y < 32; ++y) {
-          put1(S1, i0 - lo + y, j0 + lane, a[y] - t[y]);
-          put1(S2, i0 - lo + y, j0 + lane, a[y] + t[y]);
+          const float e = a[y] - t[y];
+          a[y] += t[y];
+          t[y] = e;
         }
+        tile_put(S1, i0 - lo, j0, lane, t);
+        tile_put(S2, i0 - lo, j0, lane, a);
       }
       publish<B>();
       if (issuer) {
@@ -388,27 +415,45 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
           *reinterpret_cast<float4*>(stage + r * CF::PITCH + c + 4 * q4) =
               make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
       }
-      __syncthreads();
+      cta_sync<B>();  // both CTAs' staging complete (a pair reads its peer's rows)
       float* out = dpacked + s * PAIRS;
-      for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
-        const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
-        if (j0 + 31 <= i0) continue;  // tile entirely on/below the diagonal (warp-uniform)
-        float a[32], t[32];
-        dg_tile<B>(n1, i0, j0, lane, tile, a, t);
-        const int j = j0 + lane;
+      {
+        // the upper-triangle tiles of the whole b x b block, dealt round-robin
+        // to the CTAs of the pair and then to warps (a pair splits the
+        // top-right 128 x 128 quadrant; rows owned by the peer are read from
+        // its staging through distributed shared memory)
+        constexpr int NT = B / 32, NCTA = CF::PAIR ? 2 : 1;
+        int k = 0;
+        for (int ta = 0; ta < NT; ++ta) {
+          for (int tb = ta; tb < NT; ++tb, ++k) {
+            if (k % NCTA != static_cast<int>(rank) || (k / NCTA) % 8 != warp) continue;
+            const int i0 = 32 * ta, j0 = 32 * tb;
+            const uint32_t owner = static_cast<uint32_t>(i0 / 128);
+            float a[32], t[32];
+            dg_tile<B>(n1, i0, j0, lane, tile, a, t);
+            const int j = j0 + lane;
+            const uint32_t row0 = smem_u32(stage + (i0 - 128 * static_cast<int>(owner)) * CF::PITCH + j);
+            const uint32_t src = owner == rank ? row0 : peer_addr(row0, owner);
 #pragma unroll
-        for (int y = 0; y < 32; ++y) {
-          const int i = i0 + y;
-          if (j > i) {
-            const float gv = 2.f * ((a[y] - t[y]) + stage[(i - lo) * CF::PITCH + j]);
-            float* dst = out + pidx(i, j, B);
-            *dst = accumulate ? *dst + gv : gv;
+            for (int y = 0; y < 32; ++y) {
+              const int i = i0 + y;
+              if (j > i) {
+                float acc;
+                if (owner == rank)
+                  acc = stage[(i0 - 128 * static_cast<int>(owner) + y) * CF::PITCH + j];
+                else
+                  acc = ld_cluster(src + y * CF::PITCH * 4);
+                const float gv = 2.f * ((a[y] - t[y]) + acc);
+                float* dst = out + pidx(i, j, B);
+                *dst = accumulate ? *dst + gv : gv;
+              }
+            }
           }
         }
       }
       // the next block's unpack overwrites the staging only after every warp
-      // of this CTA is done reading it
-      __syncthreads();
+      // of the pair is done reading it
+      cta_sync<B>();
     }
   }
 
