@@ -66,10 +66,6 @@ struct Cfg {
   static_assert(128 * PITCH * 4 <= 3 * SLAB, "fp32 staging must fit in the operand slabs");
 };
 
-__device__ __forceinline__ int64_t pidx(int64_t i, int64_t j, int64_t b) {
-  return i * b - i * (i + 1) / 2 + (j - i - 1);
-}
-
 // byte offset of element (r, j) (j % 8 == 0) in a K-major SW128 slab of 128 rows
 __device__ __forceinline__ uint32_t soff(int r, int j) {
   return static_cast<uint32_t>((j >> 6) * 16384 + r * 128 + ((((j & 63) >> 3) ^ (r & 7)) << 4));
@@ -112,72 +108,83 @@ __device__ __forceinline__ float ld_cluster(uint32_t addr) {
   return v;
 }
 
-// Column j0 + lane of rows rr0 .. rr0 + 31 of a slab <- v[0 .. 31] (bf16):
-// rr0 % 8 == 0, j0 % 32 == 0, so the swizzle term is a per-y constant XOR.
-__device__ __forceinline__ void tile_put(uint8_t* slab, int rr0, int j0, int lane, const float (&v)[32]) {
-  const int col = j0 + lane;
-  uint8_t* base = slab + (col >> 6) * 16384 + rr0 * 128 + (col & 7) * 2;
-  const int unit = (col & 63) >> 3;
-#pragma unroll
-  for (int y = 0; y < 32; ++y)
-    *reinterpret_cast<__nv_bfloat16*>(base + y * 128 + ((unit ^ (y & 7)) << 4)) = __float2bfloat16_rn(v[y]);
+// Packed strict upper triangle (row-contiguous, cnp.py:66-68): element (i, j),
+// i < j, lives at rowp(i) + j with rowp(i) = i*b - i(i+1)/2 - i - 1 (b <= 256,
+// so 32-bit offsets).
+template <int B>
+__device__ __forceinline__ int rowp(int i) {
+  return i * B - (i * (i + 1)) / 2 - i - 1;
 }
 
-// 32 x 32 tile (rows i0.., columns j0..) of Q from the packed strict upper
-// triangle (row-contiguous, cnp.py:66-68): lane x gets v[y] = Q[i0 + y, j0 + x].
-// Upper entries p(i, j) are read along packed row i (coalesced across lanes);
-// lower entries -p(j, i) are read along packed row j (coalesced) into the
-// warp's smem tile and transposed.
+// 32 x 32 tile (rows i0.., columns j0..) of Q, one row per lane:
+// w[x] = Q[i0 + lane, j0 + x].  Lower entries -p(j, i) are read along packed
+// row j (lanes over i: coalesced); upper entries p(i, j) along packed row i
+// with lanes over j (coalesced) into the warp's smem tile, then transposed.
 template <int B>
 __device__ __forceinline__ void q_tile(const float* __restrict__ pk, int i0, int j0, int lane, float* tile,
-                                       float (&v)[32]) {
-  const int x = lane;
-  if (j0 + 31 > i0) {  // some entry above the diagonal
+                                       float (&w)[32]) {
+  const int i = i0 + lane;
 #pragma unroll
-    for (int y = 0; y < 32; ++y) {
-      const int i = i0 + y, j = j0 + x;
-      v[y] = j > i ? __ldg(pk + pidx(i, j, B)) : 0.f;
+  for (int x = 0; x < 32; ++x) w[x] = 0.f;
+  if (j0 < i0 + 31) {  // entries below the diagonal: Q[i, j] = -p(j, i)
+#pragma unroll
+    for (int x = 0; x < 32; ++x) {
+      const int j = j0 + x;
+      if (j < i) w[x] = -__ldg(pk + rowp<B>(j) + i);
     }
-  } else {
-#pragma unroll
-    for (int y = 0; y < 32; ++y) v[y] = 0.f;
   }
-  if (j0 < i0 + 31) {  // some entry below the diagonal
+  if (j0 + 31 > i0) {  // entries above the diagonal: Q[i, j] = p(i, j)
 #pragma unroll
     for (int y = 0; y < 32; ++y) {
-      const int j = j0 + y, i = i0 + x;  // packed row j, column i
-      tile[y * 33 + x] = i > j ? __ldg(pk + pidx(j, i, B)) : 0.f;
+      const int ii = i0 + y, jj = j0 + lane;
+      tile[y * 33 + lane] = jj > ii ? __ldg(pk + rowp<B>(ii) + jj) : 0.f;
     }
     __syncwarp();
 #pragma unroll
-    for (int y = 0; y < 32; ++y) v[y] -= tile[x * 33 + y];  // -p(j0 + x, i0 + y)
+    for (int x = 0; x < 32; ++x) w[x] += tile[lane * 33 + x];
     __syncwarp();
   }
 }
 
 // Q rows [lo, lo + 128) of one block, bf16, into a slab, one 32 x 32 tile per
-// warp pass (all global reads coalesced)
+// warp pass (all global reads coalesced, 16-byte swizzled smem stores)
 template <int B>
 __device__ __forceinline__ void unpack_q(uint8_t* slab, const float* __restrict__ pk, int lo, int warp, int lane,
                                          float* tile) {
   for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
     const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
-    float v[32];
-    q_tile<B>(pk, i0, j0, lane, tile, v);
-    tile_put(slab, i0 - lo, j0, lane, v);
+    float w[32];
+    q_tile<B>(pk, i0, j0, lane, tile, w);
+    store32(slab, i0 - lo + lane, j0, w);
   }
 }
 
-// 32 x 32 tile of N1 = dG at rows i0.., columns j0..: lane x gets, for every
-// y, a[y] = N1[i0 + y, j0 + x] and t[y] = N1[j0 + x, i0 + y]; both read as
-// coalesced 128-byte rows, the transposed one through the warp's smem tile.
+// 32 x 32 tile of N1 = dG, one row per lane: a[x] = N1[i0 + lane, j0 + x]
+// (read along rows i0.. with lanes over columns, transposed through the
+// warp's smem tile) and t[x] = N1[j0 + x, i0 + lane] (lanes over columns of
+// row j0 + x: coalesced).
 template <int B>
-__device__ __forceinline__ void dg_tile(const float* __restrict__ n1, int i0, int j0, int lane, float* tile,
-                                        float (&a)[32], float (&t)[32]) {
+__device__ __forceinline__ void dg_tile_rows(const float* __restrict__ n1, int i0, int j0, int lane, float* tile,
+                                             float (&a)[32], float (&t)[32]) {
 #pragma unroll
-  for (int y = 0; y < 32; ++y) a[y] = __ldg(n1 + static_cast<int64_t>(i0 + y) * B + j0 + lane);
+  for (int y = 0; y < 32; ++y) tile[y * 33 + lane] = __ldg(n1 + (i0 + y) * B + j0 + lane);
 #pragma unroll
-  for (int y = 0; y < 32; ++y) tile[y * 33 + lane] = __ldg(n1 + static_cast<int64_t>(j0 + y) * B + i0 + lane);
+  for (int x = 0; x < 32; ++x) t[x] = __ldg(n1 + (j0 + x) * B + i0 + lane);
+  __syncwarp();
+#pragma unroll
+  for (int x = 0; x < 32; ++x) a[x] = tile[lane * 33 + x];
+  __syncwarp();
+}
+
+// the same tile one column per lane: a[y] = N1[i0 + y, j0 + lane] (coalesced)
+// and t[y] = N1[j0 + lane, i0 + y] (through the smem tile)
+template <int B>
+__device__ __forceinline__ void dg_tile_cols(const float* __restrict__ n1, int i0, int j0, int lane, float* tile,
+                                             float (&a)[32], float (&t)[32]) {
+#pragma unroll
+  for (int y = 0; y < 32; ++y) a[y] = __ldg(n1 + (i0 + y) * B + j0 + lane);
+#pragma unroll
+  for (int y = 0; y < 32; ++y) tile[y * 33 + lane] = __ldg(n1 + (j0 + y) * B + i0 + lane);
   __syncwarp();
 #pragma unroll
   for (int y = 0; y < 32; ++y) t[y] = tile[lane * 33 + y];
@@ -231,14 +238,15 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
 }
 
 template <int B, bool FWD>
-__global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
+__global__ void __launch_bounds__(THREADS, 1)
     cnp_fused_kernel(int64_t nb, const float* __restrict__ packed, const float* __restrict__ dg,
                      __nv_bfloat16* __restrict__ g16, float* __restrict__ g32, float* __restrict__ dpacked,
                      int accumulate) {
   using CF = Cfg<B>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  // 1024-byte alignment by offsetting the shared array itself (keeps the
+  // pointers in the shared address space: STS/LDS, not generic accesses)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* S0 = smem;
   uint8_t* S1 = smem + CF::SLAB;
   uint8_t* S2 = smem + 2 * CF::SLAB;
@@ -352,15 +360,15 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
       for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
         const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
         float a[32], t[32];
-        dg_tile<B>(n1, i0, j0, lane, tile, a, t);
+        dg_tile_rows<B>(n1, i0, j0, lane, tile, a, t);
 #pragma unroll
-        for (int y = 0; y < 32; ++y) {
-          const float e = a[y] - t[y];
-          a[y] += t[y];
-          t[y] = e;
+        for (int x = 0; x < 32; ++x) {
+          const float e = a[x] - t[x];
+          a[x] += t[x];
+          t[x] = e;
         }
-        tile_put(S1, i0 - lo, j0, lane, t);
-        tile_put(S2, i0 - lo, j0, lane, a);
+        store32(S1, i0 - lo + lane, j0, t);  // E
+        store32(S2, i0 - lo + lane, j0, a);  // F
       }
       publish<B>();
       if (issuer) {
@@ -430,7 +438,7 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
             const int i0 = 32 * ta, j0 = 32 * tb;
             const uint32_t owner = static_cast<uint32_t>(i0 / 128);
             float a[32], t[32];
-            dg_tile<B>(n1, i0, j0, lane, tile, a, t);
+            dg_tile_cols<B>(n1, i0, j0, lane, tile, a, t);
             const int j = j0 + lane;
             const uint32_t row0 = smem_u32(stage + (i0 - 128 * static_cast<int>(owner)) * CF::PITCH + j);
             const uint32_t src = owner == rank ? row0 : peer_addr(row0, owner);
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(THREADS, Cfg<B>::PAIR ? 1 : 2)
                 else
                   acc = ld_cluster(src + y * CF::PITCH * 4);
                 const float gv = 2.f * ((a[y] - t[y]) + acc);
-                float* dst = out + pidx(i, j, B);
+                float* dst = out + rowp<B>(i) + j;
                 *dst = accumulate ? *dst + gv : gv;
               }
             }
