@@ -225,7 +225,12 @@ typedef struct {
   void* g_p;
   void* g_r_lowp;        /* BF16 copies (BF16 layers only, else NULL) */
   void* g_p_lowp;
-  void* q2_r;            /* Q^2 caches (k == 3), may be NULL */
+  void* q2_r;            /* Q^2 caches (k == 3), may be NULL.  A BF16 layer with
+                          * k == 3, b in {128, 256} and BOTH caches NULL runs
+                          * its CNP as the fused tensor-core kernels
+                          * (poetx_cnp_forward_fused / _backward_fused);
+                          * supplying the caches selects the fp32 CUDA-core
+                          * CNP (the merge uses it for accuracy). */
   void* q2_p;
   /* optional precomputed weight folds of a BF16 layer (else built per call):
    * w_in_fold = bd(G_R) PM, w_out_fold = PM bd(G_P), both [m, n] bf16 */

@@ -80,6 +80,13 @@ const void* layer_pm(const poetx_layer_desc* d, Workspace& w, cudaStream_t st, i
   return s;
 }
 
+// BF16 layers with k = 3, b in {128, 256} and NO Q^2 cache in the factor
+// struct run the CNP as the fused tensor-core kernels (csrc/cnp_fused.cu);
+// a supplied Q^2 cache selects the CUDA-core fp32 path (merge accuracy)
+bool cnp_fused_ok(const poetx_layer_desc* d, const poetx_layer_factors_t* f) {
+  return d->dtype == POETX_BF16 && d->neumann_k == 3 && !f->q2_r && !f->q2_p && poetx_cnp_fused_supported(d->b);
+}
+
 // G used by the activation path: the bf16 copy for BF16 layers
 const void* act_g(const poetx_layer_desc* d, const void* g, const void* g16) {
   return d->dtype == POETX_BF16 ? g16 : g;
@@ -202,6 +209,12 @@ int poetx_layer_factors(const poetx_layer_desc* d, poetx_layer_factors_t* f, voi
     POETX_REQUIRE(f->g_r_lowp && f->g_p_lowp, POETX_ESHAPE, "layer_factors: bf16 layer needs lowp G");
   const int pdt = param_dtype(d->dtype);
   const int k = d->neumann_k;
+  if (cnp_fused_ok(d, f)) {
+    POETX_TRY(poetx_cnp_forward_fused(d->m / d->b, d->b, static_cast<const float*>(f->packed_r), f->g_r_lowp,
+                                      static_cast<float*>(f->g_r), stream));
+    return poetx_cnp_forward_fused(d->n / d->b, d->b, static_cast<const float*>(f->packed_p), f->g_p_lowp,
+                                   static_cast<float*>(f->g_p), stream);
+  }
   void* q2r = k == 3 ? f->q2_r : nullptr;
   void* q2p = k == 3 ? f->q2_p : nullptr;
   POETX_TRY(poetx_cnp_forward(pdt, d->m / d->b, d->b, k, nullptr, f->packed_r, f->g_r,
@@ -378,6 +391,15 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   void* cws = static_cast<char*>(ws) + wsp.used;
   size_t cwsb = ws_bytes - wsp.used;
   const int k = d->neumann_k;
+  if (cnp_fused_ok(d, f)) {
+    // BF16 layer without a Q^2 cache: the fused tensor-core CNP backward
+    // recomputes Q^2 on chip and writes the packed gradients (cnp_fused.cu)
+    POETX_TRY(poetx_cnp_backward_fused(nbr, b, static_cast<const float*>(f->packed_r),
+                                       static_cast<const float*>(dgr), static_cast<float*>(dpacked_r), accumulate,
+                                       stream));
+    return poetx_cnp_backward_fused(nbp, b, static_cast<const float*>(f->packed_p), static_cast<const float*>(dgp),
+                                    static_cast<float*>(dpacked_p), accumulate, stream);
+  }
   POETX_TRY(poetx_cnp_backward(pdt, nbr, b, k, nullptr, f->packed_r, k == 3 ? f->q2_r : nullptr,
                                dgr, nullptr, dpacked_r, accumulate, cws, cwsb, stream));
   POETX_TRY(poetx_cnp_backward(pdt, nbp, b, k, nullptr, f->packed_p, k == 3 ? f->q2_p : nullptr,

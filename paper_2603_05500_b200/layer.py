@@ -85,7 +85,8 @@ class Factors:
     """Device factor state for one forward: G (param dtype), bf16 copies,
     Q^2 caches and the packed parameters they were computed from."""
 
-    def __init__(self, layer: "PoetLinearLayer", packed_r: torch.Tensor, packed_p: torch.Tensor):
+    def __init__(self, layer: "PoetLinearLayer", packed_r: torch.Tensor, packed_p: torch.Tensor,
+                 accurate: bool = False):
         dev, pdt = layer.device, layer.param_dtype
         b, k = layer.block_size, layer.neumann_k
         nbr, nbp = layer.m // b, layer.n // b
@@ -95,8 +96,12 @@ class Factors:
         low = layer.tdtype == torch.bfloat16
         self.g_r_lowp = torch.empty((nbr, b, b), dtype=torch.bfloat16, device=dev) if low else None
         self.g_p_lowp = torch.empty((nbp, b, b), dtype=torch.bfloat16, device=dev) if low else None
-        self.q2_r = torch.empty((nbr, b, b), dtype=pdt, device=dev) if k == 3 else None
-        self.q2_p = torch.empty((nbp, b, b), dtype=pdt, device=dev) if k == 3 else None
+        # BF16 layers with b in {128, 256} leave the Q^2 caches out: the C ABI
+        # then runs the fused tensor-core CNP both ways (csrc/cnp_fused.cu);
+        # ``accurate`` (the merge) keeps the fp32 CUDA-core CNP
+        tc = low and k == 3 and not accurate and bool(N.lib().poetx_cnp_fused_supported(b))
+        self.q2_r = torch.empty((nbr, b, b), dtype=pdt, device=dev) if k == 3 and not tc else None
+        self.q2_p = torch.empty((nbp, b, b), dtype=pdt, device=dev) if k == 3 and not tc else None
         self.struct = N.LayerFactors(
             packed_r.data_ptr(), packed_p.data_ptr(), self.g_r.data_ptr(), self.g_p.data_ptr(),
             N.ptr(self.g_r_lowp), N.ptr(self.g_p_lowp), N.ptr(self.q2_r), N.ptr(self.q2_p))
@@ -293,9 +298,9 @@ class PoetLinearLayer:
             d.premerged = self._pm.data_ptr()
         return d
 
-    def compute_factors(self, packed_r=None, packed_p=None) -> Factors:
+    def compute_factors(self, packed_r=None, packed_p=None, accurate: bool = False) -> Factors:
         f = Factors(self, self._packed_dev("r") if packed_r is None else packed_r,
-                    self._packed_dev("p") if packed_p is None else packed_p)
+                    self._packed_dev("p") if packed_p is None else packed_p, accurate)
         d = self._desc()
         ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(
             N.dtype_code(self.param_dtype), max(self.m, self.n) // self.block_size,
@@ -359,7 +364,7 @@ class PoetLinearLayer:
     # -- merge -------------------------------------------------------------------------
 
     def _merge_factors(self, use_exact_cayley: bool):
-        f = self.compute_factors()
+        f = self.compute_factors(accurate=True)
         if not use_exact_cayley:
             return f.g_r, f.g_p
         from .cnp import skew_from_packed

@@ -116,7 +116,13 @@ class PoetStack:
         self.nb = self.group.numel // self.pairs
         self.block_off = {name: off // self.pairs for name, (off, _) in self.group.offsets.items()}
         self.g16 = torch.empty((self.nb, b, b), dtype=torch.bfloat16, device=device)
-        self.qq2 = torch.empty((self.nb, b, 2 * b), dtype=torch.bfloat16, device=device)
+        # b in {128, 256}: one fused tensor-core kernel per direction
+        # (csrc/cnp_fused.cu) that unpacks, multiplies and packs on chip and
+        # keeps no [Q | Q^2] cache; other block sizes use the staged kernels
+        # of csrc/cnp_tc.cu and their cache
+        self.fused = (os.environ.get("POETX_CNP_FUSED", "1") != "0" and torch.device(device).type == "cuda"
+                      and bool(N.lib().poetx_cnp_fused_supported(b)))
+        self.qq2 = None if self.fused else torch.empty((self.nb, b, 2 * b), dtype=torch.bfloat16, device=device)
         self.dg = torch.zeros((self.nb, b, b), dtype=torch.float32, device=device)
         self.device = device
 
@@ -125,27 +131,33 @@ class PoetStack:
         return buf[o:o + nb]
 
     def forward_factors(self):
-        ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(self.nb, self.b), self.device)
-        N.call("poetx_cnp_forward_tc", self.nb, self.b, self.group.param.data_ptr(), self.qq2.data_ptr(),
-               self.g16.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
+        self.forward_factors_range(0, self.nb)
 
     def backward_factors(self):
-        ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(self.nb, self.b), self.device)
-        N.call("poetx_cnp_backward_tc", self.nb, self.b, self.qq2.data_ptr(), self.dg.data_ptr(),
-               self.group.grad.data_ptr(), 0, ws, wsb, N.stream_ptr(self.device))
+        self.backward_factors_range(0, self.nb)
 
     # block ranges (one decoder block's seven layers are contiguous in the stack)
     def forward_factors_range(self, off: int, nb: int):
         b, pairs = self.b, self.pairs
+        packed = self.group.param[off * pairs:].data_ptr()
+        if self.fused:
+            N.call("poetx_cnp_forward_fused", nb, b, packed, self.g16[off].data_ptr(), None,
+                   N.stream_ptr(self.device))
+            return
         ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(nb, b), self.device)
-        N.call("poetx_cnp_forward_tc", nb, b, self.group.param[off * pairs:].data_ptr(), self.qq2[off].data_ptr(),
+        N.call("poetx_cnp_forward_tc", nb, b, packed, self.qq2[off].data_ptr(),
                self.g16[off].data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
 
     def backward_factors_range(self, off: int, nb: int):
         b, pairs = self.b, self.pairs
+        grad = self.group.grad[off * pairs:].data_ptr()
+        if self.fused:
+            N.call("poetx_cnp_backward_fused", nb, b, self.group.param[off * pairs:].data_ptr(),
+                   self.dg[off].data_ptr(), grad, 0, N.stream_ptr(self.device))
+            return
         ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(nb, b), self.device)
         N.call("poetx_cnp_backward_tc", nb, b, self.qq2[off].data_ptr(), self.dg[off].data_ptr(),
-               self.group.grad[off * pairs:].data_ptr(), 0, ws, wsb, N.stream_ptr(self.device))
+               grad, 0, ws, wsb, N.stream_ptr(self.device))
 
 
 # --------------------------------------------------------------------------
@@ -303,8 +315,10 @@ class PoetLinear(torch.nn.Module):
         b = self.b
         g_r = torch.empty((self.m // b, b, b), dtype=torch.float32, device=self.device)
         g_p = torch.empty((self.n // b, b, b), dtype=torch.float32, device=self.device)
+        # Q^2 caches supplied: the fp32 CUDA-core CNP (not the fused bf16 one)
+        q2_r, q2_p = torch.empty_like(g_r), torch.empty_like(g_p)
         f = N.LayerFactors(self.packed_r.data_ptr(), self.packed_p.data_ptr(), g_r.data_ptr(), g_p.data_ptr(),
-                           self.g_r16.data_ptr(), self.g_p16.data_ptr(), None, None)
+                           self.g_r16.data_ptr(), self.g_p16.data_ptr(), q2_r.data_ptr(), q2_p.data_ptr())
         ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(N.F32, max(self.m, self.n) // b, b, self.k),
                               self.device)
         N.call("poetx_layer_factors", self.desc, f, ws, wsb, N.stream_ptr(self.device))

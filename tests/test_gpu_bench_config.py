@@ -128,6 +128,20 @@ def test_benchmarked_trainer_path_matches_sequential_path(monkeypatch):
         close(a.premerged, b.premerged, 2e-2)
         assert rel_norm(a.premerged, b.premerged) < 3e-2
     assert rel_norm(bench.model.dense.param, seq.model.dense.param) < 3e-2
+    # after four Adam steps the two runs' parameters have drifted apart (Adam's
+    # sign-like early updates amplify rounding), so gradients are compared on
+    # a common state: the sequential run's parameters and frozen weights are
+    # copied into the benchmarked trainer's fixed buffers (the captured graph
+    # reads them in place) and one more step runs on each
+    bench.model.poet.param.copy_(seq.model.poet.param)
+    bench.model.dense.param.copy_(seq.model.dense.param)
+    for a, b in zip(bench.model.poet_layers(), seq.model.poet_layers()):
+        a.premerged.copy_(b.premerged)
+    a = float(bench.step(toks[0][:, :-1], toks[0][:, 1:]))  # graph replay, no merge after step 5
+    b = float(seq.step(toks[0][:, :-1], toks[0][:, 1:]))
+    assert abs(a - b) <= 2e-2 * abs(b), (a, b)
+    close(bench.model.poet.grad, seq.model.poet.grad, 2e-2)
+    close(bench.model.dense.grad, seq.model.dense.grad, 2e-2)
     assert rel_norm(bench.model.poet.grad, seq.model.poet.grad) < 5e-2
     assert rel_norm(bench.model.dense.grad, seq.model.dense.grad) < 5e-2
 
