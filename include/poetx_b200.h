@@ -274,6 +274,18 @@ int poetx_layer_backward_dg(const poetx_layer_desc* d, const poetx_layer_factors
  * M = blockdiag(G_R) PM blockdiag(G_P) computed in fp32/fp64 from the
  * given factors; optional W_out = Psi^T M Psi (materialize_weight). */
 size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d);
+/* Tensor-core merge product (kernel K9; layer.py:260-271, blockdiag.py:76-97):
+ * out = blockdiag(G_R) PM blockdiag(G_P) for fp32 factors G_R [m/b, b, b],
+ * G_P [n/b, b, b] and a bf16 premerged PM [m, ldp] -- or int8 codes [m, ldp]
+ * with per-row fp32 scales (POET-XQ, PM = codes * scales[row]) when pm_bf16
+ * is NULL.  Factors are split on chip into bf16 hi + lo (fp32 accumulation
+ * in TMEM; only the lo*lo term is dropped).  out is bf16 or fp32 [m, ldo].
+ * b in {128, 256} (poetx_merge_tc_supported); no workspace.  Used by
+ * poetx_layer_merge / _merge_quant for BF16 layers. */
+int poetx_merge_tc_supported(int64_t b);
+int poetx_merge_tc(int64_t m, int64_t n, int64_t b, const float* g_r, const float* g_p, const void* pm_bf16,
+                   const int8_t* pm_codes, const float* pm_scales, int64_t ldp, void* out, int out_dtype,
+                   int64_t ldo, void* stream);
 int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_p,
                       const int32_t* new_in_fwd, const int32_t* new_out_fwd,
                       void* premerged_out, void* w_out, void* ws, size_t ws_bytes,

@@ -18,7 +18,7 @@ CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libpoetx_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
-SOURCES = ["ops.cu", "layer.cu", "tc_gemm.cu", "tc_blockdiag.cu", "cnp_tc.cu", "cnp_fused.cu", "model_ops.cu", "quant.cu", "attention.cu", "svd.cu", "prof.cu", "philox.cpp"]
+SOURCES = ["ops.cu", "layer.cu", "tc_gemm.cu", "tc_blockdiag.cu", "cnp_tc.cu", "cnp_fused.cu", "merge_tc.cu", "model_ops.cu", "quant.cu", "attention.cu", "svd.cu", "prof.cu", "philox.cpp"]
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",

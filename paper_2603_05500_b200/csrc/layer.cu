@@ -87,6 +87,16 @@ bool cnp_fused_ok(const poetx_layer_desc* d, const poetx_layer_factors_t* f) {
   return d->dtype == POETX_BF16 && d->neumann_k == 3 && !f->q2_r && !f->q2_p && poetx_cnp_fused_supported(d->b);
 }
 
+// BF16 layers with b in {128, 256} merge on tensor cores (csrc/merge_tc.cu);
+// POETX_MERGE_TC=0 keeps the CUDA-core fp32 passes (A/B timing)
+bool merge_tc_ok(const poetx_layer_desc* d) {
+  static int on = [] {
+    const char* e = getenv("POETX_MERGE_TC");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return on && d->dtype == POETX_BF16 && poetx_merge_tc_supported(d->b) && d->n % 8 == 0;
+}
+
 // G used by the activation path: the bf16 copy for BF16 layers
 const void* act_g(const poetx_layer_desc* d, const void* g, const void* g16) {
   return d->dtype == POETX_BF16 ? g16 : g;
@@ -468,6 +478,23 @@ int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_
   int32_t* ridx = wsp.take<int32_t>(m);
   int32_t* cidx = wsp.take<int32_t>(n);
   POETX_REQUIRE(pm && mid1 && mid2 && ridx && cidx, POETX_ESHAPE, "layer_merge: workspace too small");
+  // BF16 layers, b in {128, 256}: mid = blockdiag(G_R) PM blockdiag(G_P) as
+  // ONE tensor-core pass (csrc/merge_tc.cu: fp32 factors split hi/lo, fp32
+  // accumulation), bf16 out, then the composite re-permutation gather
+  if (merge_tc_ok(d)) {
+    POETX_TRY(poetx_merge_tc(m, n, b, static_cast<const float*>(g_r), static_cast<const float*>(g_p), d->premerged,
+                             nullptr, nullptr, n, mid2, POETX_BF16, n, stream));
+    if (w_out) POETX_TRY(gather2d(dt, m, n, d->perm_in_inv, d->perm_out_inv, mid2, w_out, st));
+    if (premerged_out) {
+      POETX_REQUIRE(new_in_fwd && new_out_fwd, POETX_ESHAPE, "layer_merge: missing new permutations");
+      compose_kernel<<<grid_for(m, 256), 256, 0, st>>>(m, d->perm_in_inv, new_in_fwd, ridx);
+      POETX_LAUNCHED("compose");
+      compose_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, d->perm_out_inv, new_out_fwd, cidx);
+      POETX_LAUNCHED("compose");
+      POETX_TRY(gather2d(dt, m, n, ridx, cidx, mid2, premerged_out, st));
+    }
+    return POETX_OK;
+  }
   // mid = blockdiag(G_R) PM blockdiag(G_P) in the parameter type (layer.py:269-271)
   const void* pm_src = d->premerged;
   if (quantized(d)) {
@@ -515,10 +542,17 @@ int poetx_layer_merge_quant(const poetx_layer_desc* d, const void* g_r, const vo
   int8_t* qc = wsp.take<int8_t>(static_cast<size_t>(m * n));
   void* qs = wsp.take_bytes(m * acc);
   POETX_REQUIRE(pm && mid1 && mid2 && ridx && cidx && qc && qs, POETX_ESHAPE, "layer_merge_quant: workspace too small");
-  // mid = blockdiag(G_R) deq(PM) blockdiag(G_P)  (layer.py:260-271, dequantized premerged)
-  POETX_TRY(quant_dequant(pdt, m, n, d->pm_codes, d->pm_scales, nullptr, nullptr, pm, st));
-  POETX_TRY(apply_weight_rows(pdt, m / b, b, n, g_r, 0, pm, mid1, st));
-  POETX_TRY(apply_features(pdt, m, n / b, b, g_p, 0, mid1, mid2, st));
+  // mid = blockdiag(G_R) deq(PM) blockdiag(G_P)  (layer.py:260-271, dequantized premerged);
+  // on tensor cores the row scales fold into G_R's columns and the codes are
+  // exact bf16 operands (csrc/merge_tc.cu), fp32 out for the requantization
+  if (merge_tc_ok(d)) {
+    POETX_TRY(poetx_merge_tc(m, n, b, static_cast<const float*>(g_r), static_cast<const float*>(g_p), nullptr,
+                             d->pm_codes, static_cast<const float*>(d->pm_scales), n, mid2, POETX_F32, n, stream));
+  } else {
+    POETX_TRY(quant_dequant(pdt, m, n, d->pm_codes, d->pm_scales, nullptr, nullptr, pm, st));
+    POETX_TRY(apply_weight_rows(pdt, m / b, b, n, g_r, 0, pm, mid1, st));
+    POETX_TRY(apply_features(pdt, m, n / b, b, g_p, 0, mid1, mid2, st));
+  }
   if (w_out) POETX_TRY(gather_to(pdt, dt, m, n, d->perm_in_inv, d->perm_out_inv, mid2, w_out, st));
   // requantize per row (rows of the new base W are rows of mid, columns only
   // permuted: absmax and every code are invariant), then gather the codes
