@@ -28,7 +28,8 @@ class LoRALinear(torch.nn.Module):
         self.b = torch.nn.Parameter(torch.zeros(n, r, device=device))
 
     def forward(self, x):
-        return F.linear(x, self.w) + F.linear(F.linear(x, self.a.to(x.dtype)), self.b.to(x.dtype))
+        # autocast runs the adapter products in bf16 (fp32 master adapters)
+        return F.linear(x, self.w) + F.linear(F.linear(x, self.a), self.b)
 
 
 class Llama(torch.nn.Module):
@@ -82,7 +83,9 @@ class Llama(torch.nn.Module):
                 h = h + blk["down"](F.silu(blk["gate"](x)) * blk["up"](x))
             h = F.rms_norm(h, (cfg.d,), self.nf, 1e-6)
             logits = self.head(h)
-        return F.cross_entropy(logits.float().view(-1, cfg.vocab), targets.reshape(-1))
+        # bf16 logits straight into the loss (fp32 accumulation inside the
+        # kernel): no fp32 copy of the T x V logits and their gradient
+        return F.cross_entropy(logits.view(-1, cfg.vocab), targets.reshape(-1)).float()
 
 
 class BaselineTrainer:
