@@ -32,13 +32,16 @@
 //   P = odd-power part in E - even-power part in F
 //     = 2E + 2(E Q^2 + Q E Q + Q^2 E) - 2 V - (V Q^2 + Q^2 V),  V = F Q + Q F
 // computed as (7 b^3 products, no transposed operand ever needed):
-//   S0 <- Q, S1 <- E, S2 <- F
-//   A0  = Q E ;  A1 = -(F Q + Q F)                 (= -V)
-//   S2 <- Q E ;  S1 <- Z = E + A1/2                 (= E - V/2, skew)
+//   S0 <- Q, S1 <- E, S2 <- F, A1 <- E (fp32, tcgen05.st)
+//   A0  = Q E ;  A1 += -(F Q + Q F)                (A1 = E - V)
+//   S2 <- Q E ;  S1 <- Z = (A1 + E)/2               (= E - V/2, skew)
 //   A0  = Q Q ;  A1 += (Q E) Q
 //   S0 <- Q^2
 //   A1 += Z Q^2 + Q^2 Z
-//   g_ij = 2 E_ij + 2 A1_ij   (i < j; E in fp32 from dG)
+//   g_ij = 2 A1_ij   (i < j; the fp32 E term rides in the accumulator, so
+//                      dG is read from HBM once)
+// The next block's packed parameters (and dG) are prefetched into L2 while
+// the current block computes.
 #include "tc_common.cuh"
 #include "tc_gemm.cuh"
 
@@ -96,6 +99,29 @@ __device__ __forceinline__ void load32(const uint8_t* slab, int r, int j0, float
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, float (&v)[32]) {
   tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(v));
 }
+// 32 lanes x 32 columns of fp32 into TMEM (this warp's lane quarter)
+__device__ __forceinline__ void tmem_st(uint32_t taddr, const float (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], "
+      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "f"(v[0]), "f"(v[1]), "f"(v[2]), "f"(v[3]), "f"(v[4]), "f"(v[5]), "f"(v[6]), "f"(v[7]), "f"(v[8]),
+      "f"(v[9]), "f"(v[10]), "f"(v[11]), "f"(v[12]), "f"(v[13]), "f"(v[14]), "f"(v[15]), "f"(v[16]),
+      "f"(v[17]), "f"(v[18]), "f"(v[19]), "f"(v[20]), "f"(v[21]), "f"(v[22]), "f"(v[23]), "f"(v[24]),
+      "f"(v[25]), "f"(v[26]), "f"(v[27]), "f"(v[28]), "f"(v[29]), "f"(v[30]), "f"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+// bulk L2 prefetch of a contiguous range (16-byte aligned, multiple of 16 B)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  const char* c = static_cast<const char*>(p);
+  for (uint32_t o = 0; o < bytes; o += 32768) {
+    const uint32_t n = bytes - o < 32768 ? bytes - o : 32768;
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(c + o)), "r"(n)
+                 : "memory");
+  }
+}
+
 // distributed shared memory: the peer CTA's copy of a shared address
 __device__ __forceinline__ uint32_t peer_addr(uint32_t saddr, uint32_t rank) {
   uint32_t r;
@@ -173,21 +199,6 @@ __device__ __forceinline__ void dg_tile_rows(const float* __restrict__ n1, int i
   __syncwarp();
 #pragma unroll
   for (int x = 0; x < 32; ++x) a[x] = tile[lane * 33 + x];
-  __syncwarp();
-}
-
-// the same tile one column per lane: a[y] = N1[i0 + y, j0 + lane] (coalesced)
-// and t[y] = N1[j0 + lane, i0 + y] (through the smem tile)
-template <int B>
-__device__ __forceinline__ void dg_tile_cols(const float* __restrict__ n1, int i0, int j0, int lane, float* tile,
-                                             float (&a)[32], float (&t)[32]) {
-#pragma unroll
-  for (int y = 0; y < 32; ++y) a[y] = __ldg(n1 + (i0 + y) * B + j0 + lane);
-#pragma unroll
-  for (int y = 0; y < 32; ++y) tile[y * 33 + lane] = __ldg(n1 + (j0 + y) * B + i0 + lane);
-  __syncwarp();
-#pragma unroll
-  for (int y = 0; y < 32; ++y) t[y] = tile[lane * 33 + y];
   __syncwarp();
 }
 
@@ -293,6 +304,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   for (int64_t s = unit; s < nb; s += units) {
     const float* pk = packed + s * PAIRS;
+    if (threadIdx.x == 0 && s + units < nb) {
+      // the next block's inputs into L2 while this one computes (each CTA of a
+      // pair fetches half): its unpack then waits on L2, not DRAM, latency
+      constexpr uint32_t PB = static_cast<uint32_t>(PAIRS) * 4, HB = PB / 32 * 16;
+      const char* nx = reinterpret_cast<const char*>(packed + (s + units) * PAIRS);
+      if (CF::PAIR)
+        prefetch_l2(nx + rank * HB, rank ? PB - HB : HB);
+      else
+        prefetch_l2(nx, PB);
+      if (!FWD) {
+        constexpr uint32_t DB = static_cast<uint32_t>(B) * B * 4 / (CF::PAIR ? 2 : 1);
+        prefetch_l2(reinterpret_cast<const char*>(dg + (s + units) * B * B) + rank * DB, DB);
+      }
+    }
     if constexpr (FWD) {
       // ---- S0 <- Q
       unpack_q<B>(S0, pk, lo, warp, lane, tile);
@@ -355,10 +380,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncthreads();
     } else {
       const float* n1 = dg + s * static_cast<int64_t>(B) * B;
-      // ---- S0 <- Q ; S1 <- E = N1 - N1^T ; S2 <- F = N1 + N1^T
+      // ---- S0 <- Q ; S1 <- E = N1 - N1^T ; S2 <- F = N1 + N1^T ; A1 <- E (fp32)
+      // (warp w owns TMEM lanes [32 (w & 3), +32): its tiles are that row group)
       unpack_q<B>(S0, pk, lo, warp, lane, tile);
-      for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
-        const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
+      for (int k = 0; k < B / 64; ++k) {
+        const int i0 = lo + (warp & 3) * 32, j0 = ((warp >> 2) * (B / 64) + k) * 32;
         float a[32], t[32];
         dg_tile_rows<B>(n1, i0, j0, lane, tile, a, t);
 #pragma unroll
@@ -367,18 +393,20 @@ __global__ void __launch_bounds__(THREADS, 1)
           a[x] += t[x];
           t[x] = e;
         }
+        tmem_st(A1 + tl + j0, t);            // E, the fp32 start of the accumulator
         store32(S1, i0 - lo + lane, j0, t);  // E
         store32(S2, i0 - lo + lane, j0, a);  // F
       }
+      tmem_st_wait();
       publish<B>();
       if (issuer) {
         mma<B>(A0, s0, s1, NEG_B, false);  // Q E = S0 (-S1)^T          (E = -E^T)
-        mma<B>(A1, s2, s0, 0, false);      // -(F Q) = S2 S0^T          (Q = -S0^T)
+        mma<B>(A1, s2, s0, 0, true);       // E - (F Q) = S2 S0^T       (Q = -S0^T)
         mma<B>(A1, s0, s2, NEG_A, true);   // -(Q F) = (-S0) S2^T       (F = F^T)
         commit<B>(bar);
       }
       wait_mma(bar, phase);
-      // ---- S2 <- Q E ; S1 <- Z = E + A1 / 2
+      // ---- S2 <- Q E ; S1 <- Z = E - V/2 = (A1 + E) / 2   (A1 = E - V)
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
         float v[32], e[32];
@@ -387,7 +415,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld(A1 + tl + c, v);
         load32(S1, r, c, e);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) e[k] += 0.5f * v[k];
+        for (int k = 0; k < 32; ++k) e[k] = 0.5f * (e[k] + v[k]);
         store32(S1, r, c, e);
       }
       publish<B>();
@@ -411,9 +439,9 @@ __global__ void __launch_bounds__(THREADS, 1)
         commit<B>(bar);
       }
       wait_mma(bar, phase);
-      // ---- stage A1 (fp32, thread per row) over the slabs, then per 32 x 32
-      // tile of the upper triangle g_ij = 2 (E_ij + A1_ij) written as coalesced
-      // runs of the packed rows (E in fp32 from dG)
+      // ---- stage A1 = E + R (fp32, thread per row) over the slabs, then per
+      // 32 x 32 tile of the upper triangle g_ij = 2 A1_ij written as coalesced
+      // runs of the packed rows
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
         float v[32];
@@ -437,8 +465,6 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (k % NCTA != static_cast<int>(rank) || (k / NCTA) % 8 != warp) continue;
             const int i0 = 32 * ta, j0 = 32 * tb;
             const uint32_t owner = static_cast<uint32_t>(i0 / 128);
-            float a[32], t[32];
-            dg_tile_cols<B>(n1, i0, j0, lane, tile, a, t);
             const int j = j0 + lane;
             const uint32_t row0 = smem_u32(stage + (i0 - 128 * static_cast<int>(owner)) * CF::PITCH + j);
             const uint32_t src = owner == rank ? row0 : peer_addr(row0, owner);
@@ -451,7 +477,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                   acc = stage[(i0 - 128 * static_cast<int>(owner) + y) * CF::PITCH + j];
                 else
                   acc = ld_cluster(src + y * CF::PITCH * 4);
-                const float gv = 2.f * ((a[y] - t[y]) + acc);
+                const float gv = 2.f * acc;
                 float* dst = out + rowp<B>(i) + j;
                 *dst = accumulate ? *dst + gv : gv;
               }
