@@ -482,8 +482,9 @@ int poetx_layer_merge(const poetx_layer_desc* d, const void* g_r, const void* g_
   // ONE tensor-core pass (csrc/merge_tc.cu: fp32 factors split hi/lo, fp32
   // accumulation), bf16 out, then the composite re-permutation gather
   if (merge_tc_ok(d)) {
-    POETX_TRY(poetx_merge_tc(m, n, b, static_cast<const float*>(g_r), static_cast<const float*>(g_p), d->premerged,
-                             nullptr, nullptr, n, mid2, POETX_BF16, n, stream));
+    POETX_TRY(poetx_merge_tc(m, n, b, static_cast<const float*>(g_r), static_cast<const float*>(g_p),
+                             quantized(d) ? nullptr : d->premerged, d->pm_codes,
+                             static_cast<const float*>(d->pm_scales), n, mid2, POETX_BF16, n, stream));
     if (w_out) POETX_TRY(gather2d(dt, m, n, d->perm_in_inv, d->perm_out_inv, mid2, w_out, st));
     if (premerged_out) {
       POETX_REQUIRE(new_in_fwd && new_out_fwd, POETX_ESHAPE, "layer_merge: missing new permutations");

@@ -34,7 +34,7 @@ FAMILIES = [
     ("swiglu", "swiglu+gather"), ("rope", "rope+scatter"), ("scatter_add", "residual scatter"),
     ("permute", "permute"),
     ("unpack_q", "CNP glue"), ("combine_fwd", "CNP glue"), ("bwd_prep", "CNP glue"), ("pack_dq", "CNP glue"),
-    ("to_bf16", "CNP glue"),
+    ("to_bf16", "CNP glue"), ("cnp_fused", "CNP fused (tcgen05)"), ("merge_tc", "merge (tcgen05)"),
     ("adamw", "AdamW+norm"), ("sqdev", "AdamW+norm"),
     ("sdpa", "attention"), ("cudnn", "attention"), ("attn_bwd", "attention"),
     ("nvjet", "lm_head GEMMs (cuBLAS)"), ("SoftMax", "cross-entropy"), ("ce_fwd", "cross-entropy"),
