@@ -65,7 +65,7 @@ struct Cfg {
   static constexpr int TMEM_COLS = 2 * B;
   static constexpr uint32_t IDESC = idesc_bf16(PAIR ? 256 : 128, B, false, false);
   static constexpr int HALF = B / 2;             // columns per thread in thread-per-row phases
-  static constexpr int PITCH = B + 4;            // fp32 staging row pitch (floats), bank-spread
+  static constexpr int PITCH = B + 1;            // fp32 staging row pitch (floats): odd, conflict-free
   static_assert(128 * PITCH * 4 <= 3 * SLAB, "fp32 staging must fit in the operand slabs");
 };
 
@@ -120,18 +120,6 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<uint64_t>(c + o)), "r"(n)
                  : "memory");
   }
-}
-
-// distributed shared memory: the peer CTA's copy of a shared address
-__device__ __forceinline__ uint32_t peer_addr(uint32_t saddr, uint32_t rank) {
-  uint32_t r;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
-  return r;
-}
-__device__ __forceinline__ float ld_cluster(uint32_t addr) {
-  float v;
-  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-  return v;
 }
 
 // Packed strict upper triangle (row-contiguous, cnp.py:66-68): element (i, j),
@@ -439,44 +427,40 @@ __global__ void __launch_bounds__(THREADS, 1)
         commit<B>(bar);
       }
       wait_mma(bar, phase);
-      // ---- stage A1 = E + R (fp32, thread per row) over the slabs, then per
-      // 32 x 32 tile of the upper triangle g_ij = 2 A1_ij written as coalesced
-      // runs of the packed rows
+      // ---- stage A1 = E + R (fp32, thread per row, odd pitch: conflict-free
+      // for row and column reads) over the slabs, then per 32 x 32 tile of the
+      // upper triangle g_ij = 2 A1_ij written as coalesced runs of packed rows.
+      // P = A1 is skew-symmetric (every term is: E, V, E Q^2 + Q E Q + Q^2 E,
+      // V Q^2 + Q^2 V), so g_ij = -2 A1_ji too: each CTA of a pair writes the
+      // upper tiles of its own diagonal quadrant and half of the off-diagonal
+      // quadrant -- CTA 0 from its rows i < 128, CTA 1 from its rows j >= 128
+      // transposed -- all from its own staging (no peer reads, balanced).
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
         float v[32];
         tmem_ld(A1 + tl + c, v);
 #pragma unroll
-        for (int q4 = 0; q4 < 8; ++q4)
-          *reinterpret_cast<float4*>(stage + r * CF::PITCH + c + 4 * q4) =
-              make_float4(v[4 * q4], v[4 * q4 + 1], v[4 * q4 + 2], v[4 * q4 + 3]);
+        for (int k = 0; k < 32; ++k) stage[r * CF::PITCH + c + k] = v[k];
       }
-      cta_sync<B>();  // both CTAs' staging complete (a pair reads its peer's rows)
+      __syncthreads();
       float* out = dpacked + s * PAIRS;
       {
-        // the upper-triangle tiles of the whole b x b block, dealt round-robin
-        // to the CTAs of the pair and then to warps (a pair splits the
-        // top-right 128 x 128 quadrant; rows owned by the peer are read from
-        // its staging through distributed shared memory)
-        constexpr int NT = B / 32, NCTA = CF::PAIR ? 2 : 1;
+        constexpr int NT = B / 32, QT = 4;  // tiles per side; per 128-row quadrant
+        const int q0 = lo / 32;             // this CTA's diagonal quadrant
         int k = 0;
         for (int ta = 0; ta < NT; ++ta) {
-          for (int tb = ta; tb < NT; ++tb, ++k) {
-            if (k % NCTA != static_cast<int>(rank) || (k / NCTA) % 8 != warp) continue;
-            const int i0 = 32 * ta, j0 = 32 * tb;
-            const uint32_t owner = static_cast<uint32_t>(i0 / 128);
-            const int j = j0 + lane;
-            const uint32_t row0 = smem_u32(stage + (i0 - 128 * static_cast<int>(owner)) * CF::PITCH + j);
-            const uint32_t src = owner == rank ? row0 : peer_addr(row0, owner);
-#pragma unroll
+          for (int tb = ta; tb < NT; ++tb) {
+            const bool diag = ta >= q0 && tb < q0 + QT;                       // own quadrant
+            const bool off = CF::PAIR && ta < QT && tb >= QT && ((ta + tb) & 1) == static_cast<int>(rank);
+            if (!diag && !off) continue;
+            if (k++ % 8 != warp) continue;
+            const int i0 = 32 * ta, j0 = 32 * tb, j = j0 + lane;
+            const bool trans = off && rank == 1;  // g_ij = -2 P_ji from own row j
+#pragma unroll 4
             for (int y = 0; y < 32; ++y) {
               const int i = i0 + y;
               if (j > i) {
-                float acc;
-                if (owner == rank)
-                  acc = stage[(i0 - 128 * static_cast<int>(owner) + y) * CF::PITCH + j];
-                else
-                  acc = ld_cluster(src + y * CF::PITCH * 4);
+                const float acc = trans ? -stage[(j - lo) * CF::PITCH + i] : stage[(i - lo) * CF::PITCH + j];
                 const float gv = 2.f * acc;
                 float* dst = out + rowp<B>(i) + j;
                 *dst = accumulate ? *dst + gv : gv;
@@ -485,9 +469,9 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
-      // the next block's unpack overwrites the staging only after every warp
-      // of the pair is done reading it
-      cta_sync<B>();
+      // the next block's unpack overwrites this CTA's staging only after every
+      // warp is done reading it (the peer never reads it)
+      __syncthreads();
     }
   }
 

@@ -98,6 +98,8 @@ if args.timeline:
         # split the pair-GEMM family by grid: full-width launches (mm2 / adjoint /
         # folds / CNP) vs the SM-share-sized segmented outer products
         f = family(ev["name"])
+        if "cnp_fused" in ev["name"]:
+            f += " fwd" if "true>" in ev["name"] or "1>" in ev["name"] else " bwd"
         if "tc2_kernel" in ev["name"]:
             grid = ev.get("args", {}).get("grid", [0])
             f += " [outer, partial grid]" if grid and grid[0] < 140 else " [full grid]"
@@ -116,6 +118,7 @@ if args.timeline:
     by_stream = collections.defaultdict(float)
     last = t0
     gaps = []
+    cnp_alone = []
     prev_end = None
     for ts, kind, ev in edges:
         dt = ts - last
@@ -124,7 +127,10 @@ if args.timeline:
                 idle += dt
                 gaps.append((dt, prev_end["name"][:60] if prev_end else "-", ev["name"][:60]))
             elif len(active) == 1:
-                alone[tfam(next(iter(active.values())))] += dt
+                only = next(iter(active.values()))
+                alone[tfam(only)] += dt
+                if "cnp_fused" in only["name"]:
+                    cnp_alone.append((last - t0, dt, tfam(only), prev_end["name"][:50] if prev_end else "-"))
             else:
                 for e2 in active.values():
                     overl[tfam(e2)] += dt / len(active)
@@ -145,6 +151,9 @@ if args.timeline:
     for f, us in sorted(alone.items(), key=lambda x: -x[1]):
         print(f"  {us / 1e3 / args.steps:8.3f}  {f}")
     print(f"  {sum(alone.values()) / 1e3 / args.steps:8.3f}  total")
+    print("CNP kernels running alone (offset in the trace us, duration us, which, last kernel to end before):")
+    for off, dt, f, before in sorted(cnp_alone, key=lambda x: -x[1])[:16]:
+        print(f"  {off:10.1f} {dt:8.1f}  {f:28s} {before}")
     print("overlapped time, shared equally among running kernels (ms/step):")
     for f, us in sorted(overl.items(), key=lambda x: -x[1]):
         print(f"  {us / 1e3 / args.steps:8.3f}  {f}")
