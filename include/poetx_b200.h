@@ -66,6 +66,9 @@ void poetx_set_tc_enabled(int on);
  * (cta_group::2, 256 x 256 tile) kernel; 0 selects the single-CTA kernel */
 int poetx_gemm_pair_enabled(void);
 void poetx_set_gemm_pair_enabled(int on);
+/* A sub-tiles per CTA of the pair GEMM: 0 = by shape (512 x 256 pair tiles
+ * for single products with M >= 512), 1 = 256 x 256, 2 = 512 x 256 (A/B) */
+void poetx_set_gemm_pair_ms(int ms);
 /* device timing hooks: while enabled, tensor-core kernel launches are
  * bracketed by CUDA events on their stream; query sums durations (ms),
  * launch count and algorithmic FLOPs per kernel name ("tc_gemm", ...). */

@@ -86,6 +86,7 @@ _SIGS = {
     "poetx_set_tc_enabled": (None, [I32]),
     "poetx_gemm_pair_enabled": (I32, []),
     "poetx_set_gemm_pair_enabled": (None, [I32]),
+    "poetx_set_gemm_pair_ms": (None, [I32]),
     "poetx_prof_enable": (None, [I32]),
     "poetx_prof_reset": (None, []),
     "poetx_prof_query": (I32, [C.c_char_p, C.POINTER(C.c_double), C.POINTER(C.c_int64),

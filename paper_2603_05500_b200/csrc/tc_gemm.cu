@@ -352,21 +352,36 @@ __global__ void __launch_bounds__(THREADS, 1)
 //           release the accumulator on the leader's tempty barrier.
 namespace pair {
 
-constexpr int HALF = 128;                       // rows of A / columns of B per CTA
-constexpr int A_B = HALF * BK * 2;              // 16 KB
+constexpr int HALF = 128;                       // rows of A / columns of B per CTA and sub-tile
+constexpr int A_B = HALF * BK * 2;              // 16 KB per 128-row A sub-tile
 constexpr int B_B = HALF * BK * 2;              // 16 KB
-constexpr int STAGE = A_B + B_B;
 constexpr int EPI = 4 * 2 * 32 * 128;
 #ifndef POETX_PAIR_STAGES
 #define POETX_PAIR_STAGES 8
 #endif
-constexpr int STAGES_FIT = (227 * 1024 - EPI - 2048) / STAGE;
-constexpr int STAGES = STAGES_FIT > POETX_PAIR_STAGES ? POETX_PAIR_STAGES : STAGES_FIT;  // 6 by default
-constexpr int SMEM = STAGES * STAGE + EPI + 1024 + 256;
-template <bool A_MN, bool B_MN>
+// MS = 128-row A sub-tiles per CTA.  MS = 1: 256 x 256 per pair, TMEM
+// accumulators double-buffered (2 x 256 columns), 6-stage ring.  MS = 2:
+// 512 x 256 per pair (each CTA 256 x 256): the B stage serves two M = 256
+// products, so each pair moves 48 KB per 64-deep K block for twice the
+// FLOPs (0.75x the L2 -> SM bytes per FLOP; the MS = 1 kernel runs at the
+// chip's L2 -> SM throughput cap on the mm2 shapes, ncu
+// profiles/r02/ncu_gemm_vs_cublas.txt); the two accumulators fill TMEM, so
+// the next tile starts its first stages on sub-tile 0 while the epilogue
+// still drains sub-tile 1.
+template <int MS>
+struct PCfg {
+  static constexpr int STAGE = MS * A_B + B_B;
+  static constexpr int FIT = (227 * 1024 - EPI - 2048) / STAGE;
+  static constexpr int STAGES = FIT > POETX_PAIR_STAGES ? POETX_PAIR_STAGES : FIT;  // 6 (MS 1), 4 (MS 2)
+  static constexpr int SMEM = STAGES * STAGE + EPI + 1024 + 256;
+  static constexpr int TILE_M = 256 * MS;
+};
+template <int MS, bool A_MN, bool B_MN>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const __grid_constant__ CUtensorMap map_c, Args args) {
+  using PC = PCfg<MS>;
+  constexpr int STAGES = PC::STAGES, STAGE = PC::STAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -381,16 +396,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   const uint32_t rank = cta_rank();
   const bool leader = rank == 0;
   const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
-  const int tiles_per_split = args.m_tiles * args.n_tiles;  // 256 x 256 tiles
+  const int tiles_per_split = args.m_tiles * args.n_tiles;  // TILE_M x 256 tiles
   const int num_tiles = tiles_per_split * args.splits * args.groups;
 
-  // tile -> group, K split, 256-row / 256-column origin, K-block range
+  // tile -> group, K split, row / 256-column origin, K-block range
   auto decode = [&](int tile, int& g, int& s, int& m0, int& n0, int& kb0, int& kbn) {
     g = tile / (tiles_per_split * args.splits);
     int r = tile % (tiles_per_split * args.splits);
     s = r / tiles_per_split;
     r %= tiles_per_split;
-    m0 = (r / args.n_tiles) * 256;
+    m0 = (r / args.n_tiles) * PC::TILE_M;
     n0 = (r % args.n_tiles) * 256;
     const int k0 = s * args.kps;
     const int k1 = k0 + args.kps < args.K ? k0 + args.kps : args.K;
@@ -430,20 +445,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       for (int tile = cluster; tile < num_tiles; tile += nclusters) {
         int g, sp, m0, n0, kb0, kbn;
         decode(tile, g, sp, m0, n0, kb0, kbn);
-        const int am = m0 + rank * HALF, bn = n0 + rank * HALF;  // this CTA's halves
+        const int bn = n0 + rank * HALF;  // this CTA's half of B
         const int ag0 = args.a_g0 * g, ag1 = args.a_g1 * g, bg0 = args.b_g0 * g, bg1 = args.b_g1 * g;
         for (int kb = kb0; kb < kb0 + kbn; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = smem + stage * STAGE;
-          uint8_t* sb = sa + A_B;
+          uint8_t* sb = sa + MS * A_B;
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
           if (leader) mbar_expect_tx(&full[stage], 2 * STAGE);
           const int k = kb * BK;
-          if constexpr (A_MN) {
 #pragma unroll
-            for (int j = 0; j < HALF / 64; ++j) tma_load_2sm(sa + j * (BK * 128), &map_a, fb, ag0 + am + j * 64, ag1 + k);
-          } else {
-            tma_load_2sm(sa, &map_a, fb, ag0 + k, ag1 + am);
+          for (int h = 0; h < MS; ++h) {
+            const int am = m0 + h * 256 + rank * HALF;  // this CTA's rows of sub-tile h
+            if constexpr (A_MN) {
+#pragma unroll
+              for (int j = 0; j < HALF / 64; ++j)
+                tma_load_2sm(sa + h * A_B + j * (BK * 128), &map_a, fb, ag0 + am + j * 64, ag1 + k);
+            } else {
+              tma_load_2sm(sa + h * A_B, &map_a, fb, ag0 + k, ag1 + am);
+            }
           }
           if constexpr (B_MN) {
 #pragma unroll
@@ -460,33 +480,87 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
       constexpr uint32_t idesc = idesc_bf16(256, 256, A_MN, B_MN);
       int stage = 0;
       uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
-        int g, sp, m0, n0, kb0, kbn;
-        decode(tile, g, sp, m0, n0, kb0, kbn);
-        wait_cluster(&tempty[acc], acc_phase ^ 1);
-        fence_after();
-        const uint32_t tmem_d = tmem_base + acc * 256;
-        for (int kb = 0; kb < kbn; ++kb) {
-          mbar_wait(&full[stage], phase);
-          fence_after();
-          if (lane == 0) {
-            const uint32_t a_addr = smem_u32(smem + stage * STAGE);
-            const uint32_t b_addr = a_addr + A_B;
+      // one 256 x 256 x 64 product set from a stage's A sub-tile h into TMEM column d
+      auto mma_stage = [&](int st, int h, uint32_t d, bool acc) {
+        const uint32_t a_addr = smem_u32(smem + st * STAGE) + h * A_B;
+        const uint32_t b_addr = smem_u32(smem + st * STAGE) + MS * A_B;
 #pragma unroll
-            for (int k = 0; k < BK / 16; ++k)
-              umma2_bf16(tmem_d, operand_desc<A_MN>(a_addr, k), operand_desc<B_MN>(b_addr, k), idesc,
-                         (kb | k) != 0);
-            commit2(&empty[stage]);
-            if (kb == kbn - 1) commit2(&tfull[acc]);
+        for (int k = 0; k < BK / 16; ++k)
+          umma2_bf16(d, operand_desc<A_MN>(a_addr, k), operand_desc<B_MN>(b_addr, k), idesc, (acc || k) ? 1u : 0u);
+      };
+      if constexpr (MS == 1) {
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+          int g, sp, m0, n0, kb0, kbn;
+          decode(tile, g, sp, m0, n0, kb0, kbn);
+          wait_cluster(&tempty[acc], acc_phase ^ 1);
+          fence_after();
+          const uint32_t tmem_d = tmem_base + acc * 256;
+          for (int kb = 0; kb < kbn; ++kb) {
+            mbar_wait(&full[stage], phase);
+            fence_after();
+            if (lane == 0) {
+              mma_stage(stage, 0, tmem_d, kb != 0);
+              commit2(&empty[stage]);
+              if (kb == kbn - 1) commit2(&tfull[acc]);
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
+          if (kbn == 0 && lane == 0) commit2(&tfull[acc]);  // empty K range
           __syncwarp();
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          if (++acc == 2) { acc = 0; acc_phase ^= 1; }
         }
-        if (kbn == 0 && lane == 0) commit2(&tfull[acc]);  // empty K range
-        __syncwarp();
-        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      } else {
+        uint32_t tph = 0;
+        for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+          int g, sp, m0, n0, kb0, kbn;
+          decode(tile, g, sp, m0, n0, kb0, kbn);
+          const int lead = kbn < STAGES ? kbn : STAGES;
+          // sub-tile 0 starts on the first `lead` stages as soon as its
+          // accumulator is drained; sub-tile 1 follows on the same (held)
+          // stages once the epilogue has drained its accumulator too
+          wait_cluster(&tempty[0], tph ^ 1);
+          fence_after();
+          const int st0 = stage;
+          const uint32_t ph0 = phase;
+          for (int kb = 0; kb < lead; ++kb) {
+            mbar_wait(&full[stage], phase);
+            fence_after();
+            if (lane == 0) mma_stage(stage, 0, tmem_base, kb != 0);
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          wait_cluster(&tempty[1], tph ^ 1);
+          fence_after();
+          stage = st0;
+          phase = ph0;
+          for (int kb = 0; kb < lead; ++kb) {
+            if (lane == 0) {
+              mma_stage(stage, 1, tmem_base + 256, kb != 0);
+              commit2(&empty[stage]);
+              if (kb == kbn - 1) commit2(&tfull[0]);
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          for (int kb = lead; kb < kbn; ++kb) {
+            mbar_wait(&full[stage], phase);
+            fence_after();
+            if (lane == 0) {
+              mma_stage(stage, 0, tmem_base, true);
+              mma_stage(stage, 1, tmem_base + 256, true);
+              commit2(&empty[stage]);
+              if (kb == kbn - 1) commit2(&tfull[0]);
+            }
+            __syncwarp();
+            if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          }
+          if (kbn == 0 && lane == 0) commit2(&tfull[0]);  // empty K range
+          __syncwarp();
+          tph ^= 1;
+        }
       }
     }
   } else if (warp >= 4) {
@@ -498,55 +572,63 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
     for (int tile = cluster; tile < num_tiles; tile += nclusters) {
       int g, sp, m0, n0, kb0, kbn;
       decode(tile, g, sp, m0, n0, kb0, kbn);
-      const int row0 = m0 + rank * HALF + ew * 32;  // this warp's 32 rows (within the group)
-      const int64_t crow = args.c_row0 + g * args.c_grow + sp * args.c_srow + row0;
-      mbar_wait(&tfull[acc], acc_phase);
+      const int tf = MS == 1 ? acc : 0;
+      mbar_wait(&tfull[tf], acc_phase);
       fence_after();
-      const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + acc * 256;
 #pragma unroll 1
-      for (int c = 0; c < 256; c += step) {
-        uint32_t r[64];
-        tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
-        if (!args.out_f32) tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
-        if (kbn == 0) {
+      for (int h = 0; h < MS; ++h) {
+        const int row0 = m0 + h * 256 + rank * HALF + ew * 32;  // this warp's 32 rows (within the group)
+        const int64_t crow = args.c_row0 + g * args.c_grow + sp * args.c_srow + row0;
+        const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + (MS == 1 ? acc : h) * 256;
+#pragma unroll 1
+        for (int c = 0; c < 256; c += step) {
+          uint32_t r[64];
+          tmem_ld32(tbase + c, *reinterpret_cast<uint32_t(*)[32]>(r));
+          if (!args.out_f32) tmem_ld32(tbase + c + 32, *reinterpret_cast<uint32_t(*)[32]>(r + 32));
+          if (kbn == 0) {
 #pragma unroll
-          for (int q = 0; q < 64; ++q) r[q] = 0u;
-        }
-        if (args.alpha != 1.0f) {
-#pragma unroll
-          for (int q = 0; q < 64; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * args.alpha);
-        }
-        if (lane == 0) bulk_wait_read<1>();
-        __syncwarp();
-        uint8_t* rowp = stg + buf * (32 * 128) + lane * 128;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          uint4 v;
-          if (args.out_f32) {
-            v = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
-          } else {
-            v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
-            v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
-            v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
-            v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
+            for (int q = 0; q < 64; ++q) r[q] = 0u;
           }
-          *reinterpret_cast<uint4*>(rowp + ((q ^ (lane & 7)) * 16)) = v;
+          if (args.alpha != 1.0f) {
+#pragma unroll
+            for (int q = 0; q < 64; ++q) r[q] = __float_as_uint(__uint_as_float(r[q]) * args.alpha);
+          }
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          uint8_t* rowp = stg + buf * (32 * 128) + lane * 128;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            uint4 v;
+            if (args.out_f32) {
+              v = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+            } else {
+              v.x = pack_bf16(r[8 * q + 0], r[8 * q + 1]);
+              v.y = pack_bf16(r[8 * q + 2], r[8 * q + 3]);
+              v.z = pack_bf16(r[8 * q + 4], r[8 * q + 5]);
+              v.w = pack_bf16(r[8 * q + 6], r[8 * q + 7]);
+            }
+            *reinterpret_cast<uint4*>(rowp + ((q ^ (lane & 7)) * 16)) = v;
+          }
+          fence_async_smem();
+          __syncwarp();
+          if (lane == 0 && row0 < args.M && n0 + c < args.N) {
+            if (args.accumulate)
+              tma_reduce_add_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
+            else
+              tma_store_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
+          }
+          if (lane == 0) bulk_commit();
+          buf ^= 1;
         }
-        fence_async_smem();
+        fence_before();
         __syncwarp();
-        if (lane == 0 && row0 < args.M && n0 + c < args.N) {
-          if (args.accumulate)
-            tma_reduce_add_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
-          else
-            tma_store_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
-        }
-        if (lane == 0) bulk_commit();
-        buf ^= 1;
+        if (lane == 0) arrive_leader(&tempty[MS == 1 ? acc : h]);
       }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) arrive_leader(&tempty[acc]);
-      if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      if (MS == 1) {
+        if (++acc == 2) { acc = 0; acc_phase ^= 1; }
+      } else {
+        acc_phase ^= 1;
+      }
     }
     if (lane == 0) bulk_wait<0>();
   }
@@ -672,14 +754,27 @@ static int g_pair_on = [] {
   const char* e = getenv("POETX_GEMM_PAIR");
   return e && e[0] == '0' ? 0 : 1;
 }();
+// A sub-tiles per pair CTA: 0 = by shape, 1 / 2 forced (POETX_PAIR_MS, A/B)
+static int g_pair_ms = [] {
+  const char* e = getenv("POETX_PAIR_MS");
+  return e ? atoi(e) : 0;
+}();
+// 512 x 256 pair tiles for one single-split product with M >= 512 (mm2 /
+// adjoint); grouped and split-K products keep 256 x 256
+static int pair_ms(const TcProblem& p, int nblk) {
+  if (nblk != 1 || p.M < 512) return 1;
+  if (g_pair_ms == 1 || g_pair_ms == 2) return g_pair_ms;
+  return 2;
+}
 
 namespace tc {
-template <bool A_MN, bool B_MN>
+template <int MS, bool A_MN, bool B_MN>
 int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& a,
                 const char* name, cudaStream_t st) {
+  using PC = pair::PCfg<MS>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(pair::tc2_kernel<A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, pair::SMEM);
+    cudaFuncSetAttribute(pair::tc2_kernel<MS, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, PC::SMEM);
     attr_set = true;
   }
   const int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles * a.splits * a.groups;
@@ -687,10 +782,16 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int grid = static_cast<int>(2 * (tiles < pairs ? tiles : pairs));
   if (grid <= 0) return POETX_OK;
   void* tok = prof_begin(st);
-  pair::tc2_kernel<A_MN, B_MN><<<grid, THREADS, pair::SMEM, st>>>(ma, mb, mc, a);
+  pair::tc2_kernel<MS, A_MN, B_MN><<<grid, THREADS, PC::SMEM, st>>>(ma, mb, mc, a);
   prof_end(tok, name, 2.0 * a.M * a.N * static_cast<double>(a.K) * a.groups, st);
   POETX_LAUNCHED(name);
   return POETX_OK;
+}
+template <int MS>
+int launch_pair_ms(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
+                   const Args& a, const char* name, cudaStream_t st) {
+  if (a_mn) return b_mn ? launch_pair<MS, true, true>(ma, mb, mc, a, name, st) : launch_pair<MS, true, false>(ma, mb, mc, a, name, st);
+  return b_mn ? launch_pair<MS, false, true>(ma, mb, mc, a, name, st) : launch_pair<MS, false, false>(ma, mb, mc, a, name, st);
 }
 }  // namespace tc
 
@@ -725,7 +826,9 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
     int64_t kps = (p.K + a.splits - 1) / a.splits;
     kps = (kps + BK - 1) / BK * BK;
     a.kps = static_cast<int>(kps > 0 ? kps : BK);
-    a.m_tiles = static_cast<int>((p.M + 255) / 256);
+    // 512-row pair tiles for single products tall enough to use them
+    const int ms = pair_ms(p, nblk);
+    a.m_tiles = static_cast<int>((p.M + 256 * ms - 1) / (256 * ms));
     a.n_tiles = static_cast<int>(p.N / 256);
     a.a_g0 = p.a_g0; a.a_g1 = p.a_g1; a.b_g0 = p.b_g0; a.b_g1 = p.b_g1;
     a.C = p.C;
@@ -740,8 +843,8 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
     const int64_t rows = (p.groups - 1) * a.c_grow + (a.splits - 1) * a.c_srow + p.M;
     POETX_TRY(p.out_f32 ? make_map_f32(&pc, p.C, p.N, rows, p.ldc, 32, 32) : make_map(&pc, p.C, p.N, rows, p.ldc, 64, 32));
     const char* nm = p.name ? p.name : "tc_gemm";
-    if (A.mn_major) return B.mn_major ? launch_pair<true, true>(pa, pb, pc, a, nm, st) : launch_pair<true, false>(pa, pb, pc, a, nm, st);
-    return B.mn_major ? launch_pair<false, true>(pa, pb, pc, a, nm, st) : launch_pair<false, false>(pa, pb, pc, a, nm, st);
+    return ms == 2 ? launch_pair_ms<2>(A.mn_major, B.mn_major, pa, pb, pc, a, nm, st)
+                   : launch_pair_ms<1>(A.mn_major, B.mn_major, pa, pb, pc, a, nm, st);
   }
   CUtensorMap ma, mb;
   const int ms = p.ms == 2 ? 2 : 1;
@@ -843,4 +946,5 @@ int tc_outer_splits(int64_t T, int64_t nb, int64_t b) {
 extern "C" int poetx_tc_enabled(void) { return poetx::g_tc_on; }
 extern "C" int poetx_gemm_pair_enabled(void) { return poetx::g_pair_on; }
 extern "C" void poetx_set_gemm_pair_enabled(int on) { poetx::g_pair_on = on ? 1 : 0; }
+extern "C" void poetx_set_gemm_pair_ms(int ms) { poetx::g_pair_ms = ms; }
 extern "C" void poetx_set_tc_enabled(int on) { poetx::g_tc_on = on ? 1 : 0; }

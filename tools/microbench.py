@@ -37,15 +37,22 @@ def gemm():
             def ours():
                 N.call("poetx_matmul", N.BF16, M, Nn, K, a.data_ptr(), K, 0, b.data_ptr(), b.shape[1], tb,
                        c.data_ptr(), Nn, 0, N.stream_ptr())
+            N.lib().poetx_set_gemm_pair_ms(2)
             ms = timeit(ours)
+            ref = torch.matmul(a.float(), (b.t() if tb else b).float())
+            err2 = float((c.float() - ref).abs().max() / ref.abs().max())
+            N.lib().poetx_set_gemm_pair_ms(1)
+            ms_p1 = timeit(ours)
+            N.lib().poetx_set_gemm_pair_ms(0)
             N.lib().poetx_set_gemm_pair_enabled(0)
             ms1 = timeit(ours)
             N.lib().poetx_set_gemm_pair_enabled(1)
             bt = b.t() if tb else b
             ms_cublas = timeit(lambda: torch.matmul(a, bt))
             fl = 2.0 * M * Nn * K
-            print(f"M={M} N={Nn} K={K} transB={tb}: ours(pair) {ms:.3f} ms {fl / ms / 1e9:.0f} TF/s | "
-                  f"ours(1cta) {fl / ms1 / 1e9:.0f} TF/s | cuBLAS {ms_cublas:.3f} ms {fl / ms_cublas / 1e9:.0f} TF/s")
+            print(f"M={M} N={Nn} K={K} transB={tb}: ours(pair 512x256) {ms:.3f} ms {fl / ms / 1e9:.0f} TF/s "
+                  f"(rel err {err2:.1e}) | pair 256x256 {fl / ms_p1 / 1e9:.0f} TF/s | 1cta {fl / ms1 / 1e9:.0f} TF/s | "
+                  f"cuBLAS {ms_cublas:.3f} ms {fl / ms_cublas / 1e9:.0f} TF/s")
 
 
 def layer():
