@@ -194,6 +194,15 @@ int poetx_segmented_outer(int dtype, int64_t T, int64_t nb, int64_t b, const voi
 int poetx_matmul(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
                  int transA, const void* B, int64_t ldb, int transB, void* C, int64_t ldc,
                  int accumulate, void* stream);
+/* POET-XQ product with the frozen weight's int8 codes dequantized inside the
+ * GEMM producer (layer.py:188-210 with quant.py's per-row scales): BF16
+ * C[M,N] = A[M,K] . W, W = codes[K,N] * scales[k] (transB = 0) or
+ * W = (codes[N,K] * scales[n])^T (transB = 1); each element rounded to bf16
+ * once, exactly as poetx_dequantize_rows, so the result is bit-identical to
+ * dequantize + poetx_matmul.  CTA-pair tcgen05 kernel only (N % 256 == 0,
+ * 16-byte aligned pitches), else POETX_ESHAPE. */
+int poetx_matmul_q8(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const int8_t* codes, int64_t ldb,
+                    int transB, const float* scales, void* C, int64_t ldc, void* stream);
 
 /* ---------------------------------------------------------------- layer --
  * PoetLinearLayer forward/backward (layer.py:214-256) as one call each.  */

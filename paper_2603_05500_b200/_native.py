@@ -140,6 +140,7 @@ _SIGS = {
     "poetx_layer_backward": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I64, VP, VP, VP,
                                    VP, VP, VP, I32, VP, SZ, VP]),
     "poetx_merge_workspace_bytes": (SZ, [C.POINTER(LayerDesc)]),
+    "poetx_matmul_q8": (I32, [I64, I64, I64, VP, I64, VP, I64, I32, VP, VP, I64, VP]),
     "poetx_merge_tc_supported": (I32, [I64]),
     "poetx_merge_tc": (I32, [I64, I64, I64, VP, VP, VP, VP, VP, I64, VP, I32, I64, VP]),
     "poetx_layer_weight_fold": (I32, [C.POINTER(LayerDesc), C.POINTER(LayerFactors), I32, VP, VP, SZ, VP]),

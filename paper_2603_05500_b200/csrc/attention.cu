@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                     __nv_bfloat16* __restrict__ dq, __nv_bfloat16* __restrict__ dk,
                     __nv_bfloat16* __restrict__ dv, int H, int64_t ld, float scale) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+  uint8_t* sm = /* 1024-byte aligned, kept in the shared address space (STS/LDS) */ smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + OFF_BAR);
   uint64_t *s_full = bars + 1, *p_full = bars + 2, *acc_full = bars + 3, *acc_empty = bars + 4, *fin = bars + 5;
   uint64_t* ldb = bars + 8;  // 4 load stages: dO+O (for D), K0 V0 Q0, Q1, K1 V1

@@ -16,6 +16,11 @@ int apply_features(int dt, int64_t T, int64_t nb, int64_t b, const void* g, int 
                    const void* x, void* y, cudaStream_t st);
 int apply_weight_rows(int dt, int64_t nb, int64_t b, int64_t cols, const void* g, int transpose,
                       const void* w, void* y, cudaStream_t st);
+int apply_weight_rows_q8(int64_t nb, int64_t b, int64_t cols, const void* g, const int8_t* codes,
+                         const float* scales, void* y, cudaStream_t st);
+int tc_matmul_q8(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA, const int8_t* B,
+                 int64_t ldb, int transB, const float* scales, void* C, int64_t ldc, cudaStream_t st);
+constexpr int kNotSupported = -100;  // POETX_ENOTSUPPORTED (tc_gemm.cuh)
 int segmented_outer(int dt, int64_t T, int64_t nb, int64_t b, const void* x, const void* y,
                     void* out, int accumulate, Workspace& ws, cudaStream_t st);
 size_t cnp_ws_bytes(int dt, int64_t nb, int64_t b, int k);
@@ -65,20 +70,87 @@ bool reassoc(const poetx_layer_desc* d) {
   return on && d->fold_weight && d->dtype == POETX_BF16 && d->b % 64 == 0 && d->b <= 256 && d->n % 256 == 0;
 }
 
-// the premerged weight for a GEMM: the bf16/fp32/fp64 copy, or the int8
-// codes dequantized into a workspace scratch (POET-XQ)
-const void* layer_pm(const poetx_layer_desc* d, Workspace& w, cudaStream_t st, int& rc) {
-  rc = POETX_OK;
-  if (!quantized(d)) return d->premerged;
-  void* s = w.take_bytes(static_cast<size_t>(d->m * d->n) * elt_size(d->dtype));
-  if (!s) {
-    set_error("layer: workspace too small for the dequantized weight");
-    rc = POETX_ESHAPE;
-    return nullptr;
-  }
-  rc = quant_dequant(d->dtype, d->m, d->n, d->pm_codes, d->pm_scales, nullptr, nullptr, s, st);
-  return s;
+// POET-XQ: scratch for the dequantized premerged weight, reserved up front
+// in the call's workspace (so the layout never depends on which products end
+// up needing it); nullptr for a float base
+int reserve_deq(const poetx_layer_desc* d, Workspace& w, void*& out) {
+  out = nullptr;
+  if (!quantized(d)) return POETX_OK;
+  out = w.take_bytes(static_cast<size_t>(d->m * d->n) * elt_size(d->dtype));
+  POETX_REQUIRE(out, POETX_ESHAPE, "layer: workspace too small for the dequantized weight");
+  return POETX_OK;
 }
+
+// POET-XQ products that take the int8 codes straight into the pair GEMM's
+// producer (dequantized on chip, bit-identical to the dequantizer + bf16
+// GEMM): mm2, the adjoint and the W2 = bd(G_R) PM fold.  Only products that
+// cannot (W1 = PM bd(G_P), non-pair shapes) dequantize PM into workspace
+// scratch -- lazily, once per call.  POETX_Q8_GEMM=0: always dequantize (A/B).
+bool q8_gemm(const poetx_layer_desc* d) {
+  static int on = [] {
+    const char* e = getenv("POETX_Q8_GEMM");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return on && quantized(d) && d->dtype == POETX_BF16 && d->n % 16 == 0;
+}
+// the main products (mm2 / adjoint) take codes only when POETX_Q8_GEMM=2:
+// the on-chip converter does not keep up with the MMA rate there yet
+// (tools/q8bench.py), so they dequantize by default
+bool q8_main() {
+  static int on = [] {
+    const char* e = getenv("POETX_Q8_GEMM");
+    return e && e[0] == '2' ? 1 : 0;
+  }();
+  return on != 0;
+}
+struct PmSource {
+  const poetx_layer_desc* d;
+  void* scratch;  // reserve_deq
+  cudaStream_t st;
+  bool filled = false;
+  // the bf16 (or fp32/fp64) premerged weight; POET-XQ codes dequantized into
+  // the scratch on first use (the device analogue of quant.py's dequantizer)
+  int get(const void*& out) {
+    if (!quantized(d)) {
+      out = d->premerged;
+      return POETX_OK;
+    }
+    if (!filled) {
+      POETX_TRY(quant_dequant(d->dtype, d->m, d->n, d->pm_codes, d->pm_scales, nullptr, nullptr, scratch, st));
+      filled = true;
+    }
+    out = scratch;
+    return POETX_OK;
+  }
+  // c[T, N] = a[T, K] . PM (transB 0: PM is [K, N]) or a . PM^T (transB 1: PM is [N, K])
+  int matmul(int64_t T, int64_t N, int64_t K, const void* a, int transB, void* c) {
+    if (q8_gemm(d) && q8_main()) {
+      int rc = tc_matmul_q8(T, N, K, a, K, 0, d->pm_codes, d->n, transB, static_cast<const float*>(d->pm_scales), c,
+                            N, st);
+      if (rc != kNotSupported) return rc;
+    }
+    const void* pm;
+    POETX_TRY(get(pm));
+    return poetx_matmul(d->dtype, T, N, K, a, K, 0, pm, d->n, transB, c, N, 0, st);
+  }
+  // W2 = bd(G_R) PM
+  int fold_in(const void* g_r, void* out) {
+    if (q8_gemm(d)) {
+      int rc = apply_weight_rows_q8(d->m / d->b, d->b, d->n, g_r, d->pm_codes, static_cast<const float*>(d->pm_scales),
+                                    out, st);
+      if (rc != kNotSupported) return rc;
+    }
+    const void* pm;
+    POETX_TRY(get(pm));
+    return apply_weight_rows(d->dtype, d->m / d->b, d->b, d->n, g_r, 0, pm, out, st);
+  }
+  // W1 = PM bd(G_P)
+  int fold_out(const void* g_p, void* out) {
+    const void* pm;
+    POETX_TRY(get(pm));
+    return apply_features(d->dtype, d->m, d->n / d->b, d->b, g_p, 0, pm, out, st);
+  }
+};
 
 // BF16 layers with k = 3, b in {128, 256} and NO Q^2 cache in the factor
 // struct run the CNP as the fused tensor-core kernels (csrc/cnp_fused.cu);
@@ -252,9 +324,9 @@ int poetx_layer_forward_ex(const poetx_layer_desc* d, const poetx_layer_factors_
   void* b2 = wsp.take_bytes(T * w * e);
   void* b3 = wsp.take_bytes(T * w * e);
   POETX_REQUIRE(b1 && b2 && b3, POETX_ESHAPE, "layer_forward: workspace too small");
-  int qrc;
-  const void* pm = layer_pm(d, wsp, st, qrc);
-  POETX_TRY(qrc);
+  void* deq;
+  POETX_TRY(reserve_deq(d, wsp, deq));
+  PmSource pm{d, deq, st};
   void* t = saved_t ? saved_t : b3;
   // u = x[:, pi_in]  (permute_features 'inverse', layer.py:220) -- or supplied
   const void* u = x;
@@ -268,7 +340,7 @@ int poetx_layer_forward_ex(const poetx_layer_desc* d, const poetx_layer_factors_
     if (!w2) {
       void* w = wsp.take_bytes(d->m * d->n * e);
       POETX_REQUIRE(w, POETX_ESHAPE, "layer_forward: workspace too small");
-      POETX_TRY(apply_weight_rows(dt, d->m / d->b, d->b, d->n, act_g(d, f->g_r, f->g_r_lowp), 0, pm, w, st));
+      POETX_TRY(pm.fold_in(act_g(d, f->g_r, f->g_r_lowp), w));
       w2 = w;
     }
     POETX_TRY(poetx_matmul(dt, T, d->n, d->m, u, d->m, 0, w2, d->n, 0, t, d->n, 0, stream));
@@ -276,7 +348,7 @@ int poetx_layer_forward_ex(const poetx_layer_desc* d, const poetx_layer_factors_
     // a = u blockdiag(G_R)  (mm1, layer.py:221)
     POETX_TRY(apply_features(dt, T, d->m / d->b, d->b, act_g(d, f->g_r, f->g_r_lowp), 0, u, b2, st));
     // t = a PM  (mm2, layer.py:222)
-    POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b2, d->m, 0, pm, d->n, 0, t, d->n, 0, stream));
+    POETX_TRY(pm.matmul(T, d->n, d->m, b2, 0, t));
   }
   // v = t blockdiag(G_P)  (mm3, layer.py:223)
   void* v = out_raw ? z : b1;
@@ -311,9 +383,9 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   void* dgp = dg_mode ? dg_p_out : wsp.take_bytes(nbp * b * b * acc);
   POETX_REQUIRE(b1 && b2 && b3 && b4 && dgr && dgp, POETX_ESHAPE,
                 "layer_backward: workspace too small");
-  int qrc;
-  const void* pm = layer_pm(d, wsp, st, qrc);
-  POETX_TRY(qrc);
+  void* deq;
+  POETX_TRY(reserve_deq(d, wsp, deq));
+  PmSource pm{d, deq, st};
   const int dg_acc = dg_mode ? accumulate : 0;
   const void* gr = act_g(d, f->g_r, f->g_r_lowp);
   const void* gp = act_g(d, f->g_p, f->g_p_lowp);
@@ -340,12 +412,12 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
       u0 = b2;
     }
     if (ra) {
-      if (own_w2) POETX_TRY(apply_weight_rows(dt, nbr, b, d->n, gr, 0, pm, w2, st));
+      if (own_w2) POETX_TRY(pm.fold_in(gr, w2));
       const void* wi = own_w2 ? w2 : f->w_in_fold;
       POETX_TRY(poetx_matmul(dt, T, d->n, d->m, u0, d->m, 0, wi, d->n, 0, b4, d->n, 0, stream));
     } else {
       POETX_TRY(apply_features(dt, T, nbr, b, gr, 0, u0, b3, st));
-      POETX_TRY(poetx_matmul(dt, T, d->n, d->m, b3, d->m, 0, pm, d->n, 0, b4, d->n, 0, stream));
+      POETX_TRY(pm.matmul(T, d->n, d->m, b3, 0, b4));
     }
     t = b4;
   }
@@ -361,14 +433,14 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   POETX_TRY(segmented_outer(dt, T, nbp, b, t, dv, dgp, dg_acc, tail, so));
   if (ra) {
     // da = dv (PM bd(G_P))^T  (layer.py:248-249 with dt folded into the weight)
-    if (own_w1) POETX_TRY(apply_features(dt, d->m, nbp, b, gp, 0, pm, w1, st));
+    if (own_w1) POETX_TRY(pm.fold_out(gp, w1));
     const void* wo = own_w1 ? w1 : f->w_out_fold;
     POETX_TRY(poetx_matmul(dt, T, d->m, d->n, dv, d->n, 0, wo, d->n, 1, b3, d->m, 0, stream));
   } else {
     // dt = dv blockdiag(G_P)^T  (layer.py:248)
     POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, dv, b2, st));
     // da = dt PM^T  (layer.py:249)
-    POETX_TRY(poetx_matmul(dt, T, d->m, d->n, b2, d->n, 0, pm, d->n, 1, b3, d->m, 0, stream));
+    POETX_TRY(pm.matmul(T, d->m, d->n, b2, 1, b3));
   }
   // u = x[:, pi_in]  (layer.py:250) -- or the supplied pre-gathered input
   const void* u = x;
@@ -447,11 +519,10 @@ int poetx_layer_weight_fold(const poetx_layer_desc* d, const poetx_layer_factors
   POETX_REQUIRE(f->g_r_lowp && f->g_p_lowp, POETX_ESHAPE, "layer_weight_fold: bf16 factors required");
   cudaStream_t st = as_stream(stream);
   Workspace wsp(ws, ws_bytes);
-  int qrc;
-  const void* pm = layer_pm(d, wsp, st, qrc);
-  POETX_TRY(qrc);
-  if (which == 0) return apply_weight_rows(d->dtype, d->m / d->b, d->b, d->n, f->g_r_lowp, 0, pm, out, st);
-  return apply_features(d->dtype, d->m, d->n / d->b, d->b, f->g_p_lowp, 0, pm, out, st);
+  void* deq;
+  POETX_TRY(reserve_deq(d, wsp, deq));
+  PmSource pm{d, deq, st};
+  return which == 0 ? pm.fold_in(f->g_r_lowp, out) : pm.fold_out(f->g_p_lowp, out);
 }
 
 size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d) {

@@ -592,6 +592,24 @@ int apply_features(int dt, int64_t T, int64_t nb, int64_t b, const void* g, int 
   return gemm(dt, dt, d, st);
 }
 
+// POET-XQ: y[s-rows, :] = g[s] (codes[s-rows, :] * scales[s-rows]) with the
+// int8 codes dequantized inside the pair GEMM's producer (bf16 g, bf16 y)
+int apply_weight_rows_q8(int64_t nb, int64_t b, int64_t cols, const void* g, const int8_t* codes,
+                         const float* scales, void* y, cudaStream_t st) {
+  if (nb <= 0 || cols <= 0) return POETX_OK;
+  if (!tc_enabled() || b != 256 || cols % 256) return POETX_ENOTSUPPORTED;
+  TcOperand A{g, nb * b, b, b, false};
+  TcOperand B{codes, nb * b, cols, cols, true, scales};
+  TcProblem p{};
+  p.M = b; p.N = cols; p.K = b; p.groups = static_cast<int>(nb); p.splits = 1;
+  p.bn = 256;
+  p.a_g1 = static_cast<int>(b);
+  p.b_g1 = static_cast<int>(b);
+  p.C = y; p.ldc = cols; p.c_goff = b * cols;
+  p.alpha = 1.0f; p.name = "tc_wfold_q8"; p.tma_epi = 1;
+  return tc_grouped(A, B, p, st);
+}
+
 int apply_weight_rows(int dt, int64_t nb, int64_t b, int64_t cols, const void* g, int transpose,
                       const void* w, void* y, cudaStream_t st) {
   if (nb <= 0 || cols <= 0) return POETX_OK;
@@ -977,6 +995,16 @@ int poetx_matmul(int dtype, int64_t M, int64_t N, int64_t K, const void* A, int6
   d.C = C; d.sCb = 0; d.sCm = ldc; d.sCn = 1;
   d.alpha = 1.0; d.beta = accumulate ? 1.0 : 0.0;
   return gemm(dtype, dtype, d, st);
+}
+
+int poetx_matmul_q8(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, const int8_t* codes, int64_t ldb,
+                    int transB, const float* scales, void* C, int64_t ldc, void* stream) {
+  POETX_REQUIRE(M >= 0 && N >= 0 && K >= 0 && A && codes && scales && C, POETX_ESHAPE, "matmul_q8: bad arguments");
+  const int rc = tc_enabled() ? tc_matmul_q8(M, N, K, A, lda, 0, codes, ldb, transB, scales, C, ldc, as_stream(stream))
+                              : POETX_ENOTSUPPORTED;
+  POETX_REQUIRE(rc != POETX_ENOTSUPPORTED, POETX_ESHAPE,
+                "matmul_q8: shape not handled by the fused int8 pair GEMM (N %% 256, 16-byte pitches)");
+  return rc;
 }
 
 size_t poetx_sqnorm_workspace_bytes(int ntensors, const int64_t* numel) {

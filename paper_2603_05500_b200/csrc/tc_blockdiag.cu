@@ -55,8 +55,7 @@ __global__ void __launch_bounds__(BD_THREADS, 1)
               const __grid_constant__ CUtensorMap map_y, BdArgs args) {
   using CF = BdCfg<BN>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = /* 1024-byte aligned, kept in the shared address space (STS/LDS) */ smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sg = smem;                                   // resident G[s]
   uint8_t* ring = sg + CF::B_BYTES;                     // x tiles
   uint8_t* epi = ring + BD_STAGES * BD_A_BYTES;         // store staging

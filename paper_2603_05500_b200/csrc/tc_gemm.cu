@@ -80,6 +80,7 @@ struct Args {
   int tma_epi;     // 1: epilogue through smem staging + TMA bulk store (reduce-add if accumulate)
   int64_t c_row0;  // row of C (in map_c) where group 0 / split 0 starts ... per-group/split rows:
   int64_t c_grow, c_srow;
+  const float* bscale;  // int8 B (pair kernel Q8): fp32 scale per row of the B tensor view
 };
 
 // ------------------------------------------------------------------ kernel --
@@ -90,8 +91,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   using CF = Cfg<BN, MS>;
   constexpr int STAGES = CF::STAGES, NACC = CF::NACC, TM = BM * MS;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = /* 1024-byte aligned, kept in the shared address space (STS/LDS) */ smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* epi = smem + STAGES * CF::STAGE_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(epi + CF::EPI_BYTES);
   uint64_t* empty = full + STAGES;
@@ -368,29 +368,46 @@ constexpr int EPI = 4 * 2 * 32 * 128;
 // profiles/r02/ncu_gemm_vs_cublas.txt); the two accumulators fill TMEM, so
 // the next tile starts its first stages on sub-tile 0 while the epilogue
 // still drains sub-tile 1.
-template <int MS>
+// Q8: B arrives as int8 codes (POET-XQ).  Warp 3 streams the codes (8 KB
+// per CTA and K block, unswizzled) and their fp32 row scales into a raw
+// ring that runs up to RAW_STAGES blocks ahead of the bf16 operand ring;
+// converter warps (2 and 8..11) turn a raw block into the bf16 SW128 B
+// operand of a free stage (code * row scale, ONE bf16 rounding: bit-identical
+// to the standalone dequantizer) and arrive on the leader's full barrier.
+constexpr int RAW_B = HALF * BK;                // 8 KB of int8 per CTA and K block
+constexpr int RAW_S = HALF * 4;                 // + the block's row scales (<= 128 fp32)
+constexpr int RAW_SLOT = RAW_B + RAW_S;
+template <int MS, bool Q8 = false>
 struct PCfg {
   static constexpr int STAGE = MS * A_B + B_B;
   static constexpr int FIT = (227 * 1024 - EPI - 2048) / STAGE;
-  static constexpr int STAGES = FIT > POETX_PAIR_STAGES ? POETX_PAIR_STAGES : FIT;  // 6 (MS 1), 4 (MS 2)
-  static constexpr int SMEM = STAGES * STAGE + EPI + 1024 + 256;
+  static constexpr int NQ = FIT > POETX_PAIR_STAGES ? POETX_PAIR_STAGES : FIT;   // 6 (MS 1), 4 (MS 2)
+  static constexpr int STAGES = Q8 ? (MS == 1 ? 4 : 3) : NQ;
+  static constexpr int RAW_FIT = (227 * 1024 - EPI - 2048 - STAGES * STAGE) / RAW_SLOT;
+  static constexpr int RAW_STAGES = Q8 ? (RAW_FIT > 8 ? 8 : RAW_FIT) : 0;       // 7 (MS 1), 5 (MS 2)
+  static constexpr int SMEM = STAGES * STAGE + RAW_STAGES * RAW_SLOT + EPI + 1024 + 256;
   static constexpr int TILE_M = 256 * MS;
 };
-template <int MS, bool A_MN, bool B_MN>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+// Q8 CTAs carry 4 more warps (8..11): warp 3 loads codes, warps 2 and 8..11 convert
+constexpr int Q8_THREADS = THREADS + 128, Q8_CONV_WARPS = 5;
+template <int MS, bool A_MN, bool B_MN, bool Q8 = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : THREADS, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                const __grid_constant__ CUtensorMap map_c, Args args) {
-  using PC = PCfg<MS>;
+  using PC = PCfg<MS, Q8>;
   constexpr int STAGES = PC::STAGES, STAGE = PC::STAGE;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* smem = /* 1024-byte aligned, kept in the shared address space (STS/LDS) */ smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* epi = smem + STAGES * STAGE;
-  uint64_t* full = reinterpret_cast<uint64_t*>(epi + EPI);
+  constexpr int RSTG = PC::RAW_STAGES;
+  uint8_t* rawring = epi + EPI;  // Q8 only: RSTG x (codes + scales)
+  uint64_t* full = reinterpret_cast<uint64_t*>(rawring + RSTG * RAW_SLOT);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* rawfull = tempty + 2;  // Q8 only: RSTG each
+  uint64_t* rawempty = rawfull + RSTG;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rawempty + RSTG);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = cta_rank();
@@ -415,8 +432,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < STAGES; ++st) {
-      mbar_init(&full[st], 1);
+      mbar_init(&full[st], Q8 ? 1 + 2 * Q8_CONV_WARPS : 1);  // Q8: + the converter warps of both CTAs
       mbar_init(&empty[st], 1);
+    }
+    for (int st = 0; st < RSTG; ++st) {
+      mbar_init(&rawfull[st], 1);
+      mbar_init(&rawempty[st], Q8_CONV_WARPS);
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
@@ -436,7 +457,87 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp == 0) {
+  if (Q8 && warp == 3) {
+    // codes + row scales of every K block of this CTA's B half, RSTG blocks ahead
+    if (lane == 0) {
+      int rs = 0;
+      uint32_t rph = 0;
+      for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+        int g, sp, m0, n0, kb0, kbn;
+        decode(tile, g, sp, m0, n0, kb0, kbn);
+        const int bn = n0 + rank * HALF;
+        const int bg0 = args.b_g0 * g, bg1 = args.b_g1 * g;
+        for (int kb = kb0; kb < kb0 + kbn; ++kb) {
+          mbar_wait(&rawempty[rs], rph ^ 1);
+          uint8_t* raw = rawring + rs * RAW_SLOT;
+          const int k = kb * BK;
+          const int srow = B_MN ? bg1 + k : bg1 + bn;  // first B row of the block
+          const int nsc = B_MN ? BK : HALF;
+          mbar_expect_tx(&rawfull[rs], RAW_B + nsc * 4);
+          if constexpr (B_MN)
+            tma_load_2d(raw, &map_b, &rawfull[rs], bg0 + bn, bg1 + k);
+          else
+            tma_load_2d(raw, &map_b, &rawfull[rs], bg0 + k, bg1 + bn);
+          bulk_load_1d(raw + RAW_B, args.bscale + srow, nsc * 4, &rawfull[rs]);
+          if (++rs == RSTG) { rs = 0; rph ^= 1; }
+        }
+      }
+    }
+  } else if (Q8 && (warp == 2 || warp >= 8)) {
+    // int8 -> bf16 B converter: this CTA's half (128 B columns) of every stage
+    const int ct = (warp == 2 ? 0 : warp - 7) * 32 + lane;  // 0 .. 32 * Q8_CONV_WARPS - 1
+    int stage = 0, rs = 0;
+    uint32_t phase = 0, rph = 0;
+    for (int tile = cluster; tile < num_tiles; tile += nclusters) {
+      int g, sp, m0, n0, kb0, kbn;
+      decode(tile, g, sp, m0, n0, kb0, kbn);
+      for (int kb = kb0; kb < kb0 + kbn; ++kb) {
+        mbar_wait(&rawfull[rs], rph);
+        mbar_wait(&empty[stage], phase ^ 1);  // the bf16 stage is free (MMAs done with it)
+        const uint8_t* raw = rawring + rs * RAW_SLOT;
+        const float* scl = reinterpret_cast<const float*>(raw + RAW_B);
+        uint8_t* sb = smem + stage * STAGE + MS * A_B;
+#pragma unroll 2
+        for (int u = ct; u < HALF * BK / 8; u += 32 * Q8_CONV_WARPS) {
+          int r, c;  // raw row / first of 8 columns (raw rows are 128 B (MN) or 64 B (K-major))
+          uint32_t dst;
+          if constexpr (B_MN) {  // raw [64 K rows][128 N cols], scale per K row
+            r = u >> 4;
+            c = (u & 15) * 8;
+            dst = static_cast<uint32_t>((c >> 6) * (BK * 128) + r * 128 + ((((c & 63) >> 3) ^ (r & 7)) << 4));
+          } else {               // raw [128 N rows][64 K cols], scale per N row
+            r = u >> 3;
+            c = (u & 7) * 8;
+            dst = static_cast<uint32_t>(r * 128 + (((c >> 3) ^ (r & 7)) << 4));
+          }
+          const float sc = scl[r];
+          const uint2 q = *reinterpret_cast<const uint2*>(raw + r * (B_MN ? HALF : BK) + c);
+          // int8 -> fp32 without I2F: byte b (biased by +128) into the mantissa
+          // of 2^23 (PRMT), minus 2^23 + 128 (exact); then code * scale and ONE
+          // bf16 rounding, as the standalone dequantizer
+          const uint32_t w[2] = {q.x ^ 0x80808080u, q.y ^ 0x80808080u};
+          uint32_t h[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const uint32_t src = w[x >> 1], sel0 = 0x7540u | ((x & 1) * 2), sel1 = 0x7541u | ((x & 1) * 2);
+            const float f0 = (__uint_as_float(__byte_perm(src, 0x4B000000u, sel0)) - 8388736.0f) * sc;
+            const float f1 = (__uint_as_float(__byte_perm(src, 0x4B000000u, sel1)) - 8388736.0f) * sc;
+            __nv_bfloat162 v = __floats2bfloat162_rn(f0, f1);
+            h[x] = *reinterpret_cast<uint32_t*>(&v);
+          }
+          *reinterpret_cast<uint4*>(sb + dst) = make_uint4(h[0], h[1], h[2], h[3]);
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          arrive_leader(&full[stage]);
+          mbar_arrive(&rawempty[rs]);
+        }
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        if (++rs == RSTG) { rs = 0; rph ^= 1; }
+      }
+    }
+  } else if (warp == 0) {
     if (lane == 0) {
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_a)) : "memory");
       asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&map_b)) : "memory");
@@ -452,7 +553,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
           uint8_t* sa = smem + stage * STAGE;
           uint8_t* sb = sa + MS * A_B;
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
-          if (leader) mbar_expect_tx(&full[stage], 2 * STAGE);
+          if (leader) mbar_expect_tx(&full[stage], 2 * (Q8 ? MS * A_B : STAGE));
           const int k = kb * BK;
 #pragma unroll
           for (int h = 0; h < MS; ++h) {
@@ -465,7 +566,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
               tma_load_2sm(sa + h * A_B, &map_a, fb, ag0 + k, ag1 + am);
             }
           }
-          if constexpr (B_MN) {
+          if constexpr (Q8) {
+            // B: the converter warps fill it from the raw ring (warp 3 loads the codes)
+          } else if constexpr (B_MN) {
 #pragma unroll
             for (int j = 0; j < HALF / 64; ++j) tma_load_2sm(sb + j * (BK * 128), &map_b, fb, bg0 + bn + j * 64, bg1 + k);
           } else {
@@ -705,6 +808,23 @@ int make_map_f32(CUtensorMap* map, const void* base, uint64_t cols, uint64_t row
   return POETX_OK;
 }
 
+// 2-D int8 tensor map (unswizzled) over a row-major [rows, cols] view, pitch in bytes
+int make_map_u8(CUtensorMap* map, const void* base, uint64_t cols, uint64_t rows, uint64_t pitch,
+                uint32_t box_cols, uint32_t box_rows) {
+  ensure_context();
+  auto fn = encode_fn();
+  POETX_REQUIRE(fn != nullptr, POETX_ECUDA, "cuTensorMapEncodeTiled unavailable");
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  POETX_REQUIRE(r == CUDA_SUCCESS, POETX_ECUDA, "cuTensorMapEncodeTiled (u8) failed (%d)", (int)r);
+  return POETX_OK;
+}
+
 int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -768,13 +888,13 @@ static int pair_ms(const TcProblem& p, int nblk) {
 }
 
 namespace tc {
-template <int MS, bool A_MN, bool B_MN>
+template <int MS, bool A_MN, bool B_MN, bool Q8 = false>
 int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc, const Args& a,
                 const char* name, cudaStream_t st) {
-  using PC = pair::PCfg<MS>;
+  using PC = pair::PCfg<MS, Q8>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(pair::tc2_kernel<MS, A_MN, B_MN>, cudaFuncAttributeMaxDynamicSharedMemorySize, PC::SMEM);
+    cudaFuncSetAttribute(pair::tc2_kernel<MS, A_MN, B_MN, Q8>, cudaFuncAttributeMaxDynamicSharedMemorySize, PC::SMEM);
     attr_set = true;
   }
   const int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles * a.splits * a.groups;
@@ -782,16 +902,19 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
   const int grid = static_cast<int>(2 * (tiles < pairs ? tiles : pairs));
   if (grid <= 0) return POETX_OK;
   void* tok = prof_begin(st);
-  pair::tc2_kernel<MS, A_MN, B_MN><<<grid, THREADS, PC::SMEM, st>>>(ma, mb, mc, a);
+  pair::tc2_kernel<MS, A_MN, B_MN, Q8><<<grid, Q8 ? pair::Q8_THREADS : THREADS, PC::SMEM, st>>>(ma, mb, mc, a);
   prof_end(tok, name, 2.0 * a.M * a.N * static_cast<double>(a.K) * a.groups, st);
   POETX_LAUNCHED(name);
   return POETX_OK;
 }
-template <int MS>
+template <int MS, bool Q8>
 int launch_pair_ms(bool a_mn, bool b_mn, const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc,
                    const Args& a, const char* name, cudaStream_t st) {
-  if (a_mn) return b_mn ? launch_pair<MS, true, true>(ma, mb, mc, a, name, st) : launch_pair<MS, true, false>(ma, mb, mc, a, name, st);
-  return b_mn ? launch_pair<MS, false, true>(ma, mb, mc, a, name, st) : launch_pair<MS, false, false>(ma, mb, mc, a, name, st);
+  if (a_mn)
+    return b_mn ? launch_pair<MS, true, true, Q8>(ma, mb, mc, a, name, st)
+                : launch_pair<MS, true, false, Q8>(ma, mb, mc, a, name, st);
+  return b_mn ? launch_pair<MS, false, true, Q8>(ma, mb, mc, a, name, st)
+              : launch_pair<MS, false, false, Q8>(ma, mb, mc, a, name, st);
 }
 }  // namespace tc
 
@@ -802,8 +925,10 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
   const int BN = p.bn;
   POETX_REQUIRE(BN == 64 || BN == 128 || BN == 256, POETX_ESHAPE, "tc: bad BN %d", BN);
   if (p.M <= 0 || p.N <= 0 || p.groups <= 0) return POETX_OK;
+  const bool q8 = B.row_scale != nullptr;
+  if (A.row_scale) return POETX_ENOTSUPPORTED;
   for (const TcOperand* o : {&A, &B}) {
-    if ((reinterpret_cast<uintptr_t>(o->ptr) & 15) || (o->pitch % 8)) return POETX_ENOTSUPPORTED;
+    if ((reinterpret_cast<uintptr_t>(o->ptr) & 15) || (o->pitch % (o == &B && q8 ? 16 : 8))) return POETX_ENOTSUPPORTED;
   }
   if ((reinterpret_cast<uintptr_t>(p.C) & 15) || (p.ldc % 8) || (p.c_goff % 8) || (p.c_soff % 8))
     return POETX_ENOTSUPPORTED;
@@ -816,7 +941,11 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
       !(p.accumulate && !p.out_f32)) {
     CUtensorMap pa, pb, pc;
     POETX_TRY(make_map(&pa, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : pair::HALF));
-    POETX_TRY(make_map(&pb, B.ptr, B.cols, B.rows, B.pitch, 64, B.mn_major ? BK : pair::HALF));
+    if (q8)  // int8 codes, unswizzled raw boxes: {128 N, 64 K} (MN-major) or {64 K, 128 N}
+      POETX_TRY(make_map_u8(&pb, B.ptr, B.cols, B.rows, B.pitch, B.mn_major ? pair::HALF : BK,
+                            B.mn_major ? BK : pair::HALF));
+    else
+      POETX_TRY(make_map(&pb, B.ptr, B.cols, B.rows, B.pitch, 64, B.mn_major ? BK : pair::HALF));
     Args a{};
     a.M = static_cast<int>(p.M);
     a.N = static_cast<int>(p.N);
@@ -840,12 +969,17 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
     a.c_row0 = 0;
     a.c_grow = p.c_goff / p.ldc;
     a.c_srow = p.c_soff / p.ldc;
+    a.bscale = B.row_scale;
     const int64_t rows = (p.groups - 1) * a.c_grow + (a.splits - 1) * a.c_srow + p.M;
     POETX_TRY(p.out_f32 ? make_map_f32(&pc, p.C, p.N, rows, p.ldc, 32, 32) : make_map(&pc, p.C, p.N, rows, p.ldc, 64, 32));
     const char* nm = p.name ? p.name : "tc_gemm";
-    return ms == 2 ? launch_pair_ms<2>(A.mn_major, B.mn_major, pa, pb, pc, a, nm, st)
-                   : launch_pair_ms<1>(A.mn_major, B.mn_major, pa, pb, pc, a, nm, st);
+    if (q8)
+      return ms == 2 ? launch_pair_ms<2, true>(A.mn_major, B.mn_major, pa, pb, pc, a, nm, st)
+                     : launch_pair_ms<1, true>(A.mn_major, B.mn_major, pa, pb, pc, a, nm, st);
+    return ms == 2 ? launch_pair_ms<2, false>(A.mn_major, B.mn_major, pa, pb, pc, a, nm, st)
+                   : launch_pair_ms<1, false>(A.mn_major, B.mn_major, pa, pb, pc, a, nm, st);
   }
+  if (q8) return POETX_ENOTSUPPORTED;  // int8 B: pair kernel only
   CUtensorMap ma, mb;
   const int ms = p.ms == 2 ? 2 : 1;
   POETX_TRY(make_map(&ma, A.ptr, A.cols, A.rows, A.pitch, 64, A.mn_major ? BK : BM * ms));
@@ -901,6 +1035,18 @@ int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int t
   TcProblem p{};
   p.M = M; p.N = N; p.K = K; p.groups = 1; p.splits = 1; p.bn = 256;
   p.C = C; p.ldc = ldc; p.alpha = 1.0f; p.name = "tc_gemm"; p.tma_epi = 1;
+  return tc_grouped(a, b, p, st);
+}
+
+int tc_matmul_q8(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA, const int8_t* B,
+                 int64_t ldb, int transB, const float* scales, void* C, int64_t ldc, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return POETX_OK;
+  if (K <= 0 || M > INT32_MAX || N > INT32_MAX || K > INT32_MAX || !scales) return POETX_ENOTSUPPORTED;
+  TcOperand a{A, transA ? K : M, transA ? M : K, lda, transA != 0};
+  TcOperand b{B, transB ? N : K, transB ? K : N, ldb, transB == 0, scales};
+  TcProblem p{};
+  p.M = M; p.N = N; p.K = K; p.groups = 1; p.splits = 1; p.bn = 256;
+  p.C = C; p.ldc = ldc; p.alpha = 1.0f; p.name = "tc_gemm_q8"; p.tma_epi = 1;
   return tc_grouped(a, b, p, st);
 }
 

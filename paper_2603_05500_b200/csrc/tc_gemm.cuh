@@ -18,6 +18,10 @@ struct TcOperand {
   const void* ptr;
   int64_t rows, cols, pitch;
   bool mn_major;
+  // POET-XQ B operand: int8 codes (pitch in bytes = elements) whose ROW r of
+  // this [rows, cols] view carries the fp32 scale row_scale[r]; converted to
+  // bf16 (code * scale, one rounding, as the dequantizer) on chip
+  const float* row_scale = nullptr;
 };
 
 // Grouped/split-K problem: for g < groups, s < splits,
@@ -43,6 +47,12 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
 // C[M,N] = op(A) op(B), BF16 in, fp32 accumulate (TMEM), BF16 out.
 int tc_matmul(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
               const void* B, int64_t ldb, int transB, void* C, int64_t ldc, cudaStream_t st);
+// same with B = int8 codes [K, N] (transB = 0: row k scaled by scales[k]) or
+// [N, K] (transB = 1: row n scaled by scales[n]), i.e. the POET-XQ premerged
+// weight dequantized inside the GEMM producer; ENOTSUPPORTED off the pair path
+int tc_matmul_q8(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA,
+                 const int8_t* B, int64_t ldb, int transB, const float* scales, void* C, int64_t ldc,
+                 cudaStream_t st);
 
 // y_s = x_s g[s] (or g[s]^T) for every length-b segment s; BF16.
 int tc_blockdiag(const GemmDesc& d, cudaStream_t st);

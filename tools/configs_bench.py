@@ -24,19 +24,19 @@ CASES = {
     "cfg1-layer": dict(kind="layer"),
     "60m-poetx": dict(kind="poet", model="llama-60m", mb=32),
     "60m-adamw": dict(kind="adamw", model="llama-60m", mb=32),
-    "60m-lora": dict(kind="lora", model="llama-60m", mb=32, rank=31),
+    "60m-lora": dict(kind="lora", model="llama-60m", mb=32, rank=32),
     "350m-poetx-merge5": dict(kind="poet", model="llama-350m", mb=32, merge_gap=5),
     "350m-poetx": dict(kind="poet", model="llama-350m", mb=32),
     "1b-poetx-fast": dict(kind="poet", model="llama-1b", mb=32),
     "1b-poetx-mem": dict(kind="poet", model="llama-1b", mb=32, variant="mem"),
     "1b-poetxq-mem": dict(kind="poet", model="llama-1b", mb=32, variant="mem", quantized=True),
     "1b-adamw": dict(kind="adamw", model="llama-1b", mb=32),
-    "1b-lora": dict(kind="lora", model="llama-1b", mb=32, rank=127),
+    "1b-lora": dict(kind="lora", model="llama-1b", mb=32, rank=128),
     "8b-poetx-fast": dict(kind="poet", model="llama-8b", mb=1),
     "8b-poetx-mem": dict(kind="poet", model="llama-8b", mb=1, variant="mem"),
     "8b-poetxq-mem": dict(kind="poet", model="llama-8b", mb=1, variant="mem", quantized=True),
     "8b-adamw": dict(kind="adamw", model="llama-8b", mb=1),
-    "8b-lora": dict(kind="lora", model="llama-8b", mb=1, rank=127),
+    "8b-lora": dict(kind="lora", model="llama-8b", mb=1, rank=128),
     "8b-poetx-fast-mb8": dict(kind="poet", model="llama-8b", mb=8),
 }
 
@@ -82,7 +82,9 @@ def run_layer():
     b, T = 64, 1024
     r = np.random.default_rng(0)
     base = (r.standard_normal((m, n)) / np.sqrt(m)).astype(np.float32)
-    lay = P.PoetLinearLayer(base, b, P.Rng.keyed(0, "cfg1"))
+    # a torch-constructed layer keeps device state (numpy-constructed ones mirror
+    # the reference's numpy attributes and copy in and out every call)
+    lay = P.PoetLinearLayer(torch.from_numpy(base), b, P.Rng.keyed(0, "cfg1"))
     lay.q_r.packed.normal_(0, 0.01)
     lay.q_p.packed.normal_(0, 0.01)
     x = torch.randn((T, m), device="cuda")

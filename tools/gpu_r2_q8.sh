@@ -1,0 +1,8 @@
+# POET-XQ fused int8 GEMM: bitwise tests, quant suite, XQ throughput vs mem
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_q8_gemm.py tests/test_gpu_quant.py tests/test_gpu_tc.py -q -m gpu -rf > gpurun_out/q8_tests.log 2>&1; echo tests $?
+for c in 1b-poetx-mem 1b-poetxq-mem 8b-poetx-mem 8b-poetxq-mem; do timeout 600 python tools/configs_bench.py --one $c >> gpurun_out/q8_configs.jsonl 2>>gpurun_out/q8_configs.err; done
+tail -5 gpurun_out/q8_tests.log; python -c "
+import json
+for l in open('gpurun_out/q8_configs.jsonl'):
+    d=json.loads(l); print(d['case'], round(d.get('tokens_per_s_median_step',0)), d.get('peak_hbm_gb'), d.get('error','')[:300])"
