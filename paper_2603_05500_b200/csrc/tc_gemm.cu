@@ -382,9 +382,9 @@ struct PCfg {
   static constexpr int STAGE = MS * A_B + B_B;
   static constexpr int FIT = (227 * 1024 - EPI - 2048) / STAGE;
   static constexpr int NQ = FIT > POETX_PAIR_STAGES ? POETX_PAIR_STAGES : FIT;   // 6 (MS 1), 4 (MS 2)
-  static constexpr int STAGES = Q8 ? (MS == 1 ? 4 : 3) : NQ;
+  static constexpr int STAGES = Q8 ? (MS == 1 ? 5 : 3) : NQ;
   static constexpr int RAW_FIT = (227 * 1024 - EPI - 2048 - STAGES * STAGE) / RAW_SLOT;
-  static constexpr int RAW_STAGES = Q8 ? (RAW_FIT > 8 ? 8 : RAW_FIT) : 0;       // 7 (MS 1), 5 (MS 2)
+  static constexpr int RAW_STAGES = Q8 ? (RAW_FIT > 8 ? 8 : RAW_FIT) : 0;       // 3 (MS 1), 5 (MS 2)
   static constexpr int SMEM = STAGES * STAGE + RAW_STAGES * RAW_SLOT + EPI + 1024 + 256;
   static constexpr int TILE_M = 256 * MS;
 };
@@ -432,7 +432,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
 
   if (threadIdx.x == 0) {
     for (int st = 0; st < STAGES; ++st) {
-      mbar_init(&full[st], Q8 ? 1 + 2 * Q8_CONV_WARPS : 1);  // Q8: + the converter warps of both CTAs
+      mbar_init(&full[st], Q8 ? 3 : 1);  // Q8: + one elected converter thread in each CTA
       mbar_init(&empty[st], 1);
     }
     for (int st = 0; st < RSTG; ++st) {
@@ -529,10 +529,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
         }
         fence_async_smem();
         __syncwarp();
-        if (lane == 0) {
-          arrive_leader(&full[stage]);
-          mbar_arrive(&rawempty[rs]);
-        }
+        if (lane == 0) mbar_arrive(&rawempty[rs]);
+        // every converter warp's stores are in (named barrier 1 over the
+        // converter warps), then ONE cluster-scope release arrival per CTA
+        asm volatile("bar.sync 1, %0;" ::"n"(32 * Q8_CONV_WARPS) : "memory");
+        if (ct == 0) arrive_leader(&full[stage]);
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++rs == RSTG) { rs = 0; rph ^= 1; }
       }
@@ -881,8 +882,9 @@ static int g_pair_ms = [] {
 }();
 // 512 x 256 pair tiles for one single-split product with M >= 512 (mm2 /
 // adjoint); grouped and split-K products keep 256 x 256
-static int pair_ms(const TcProblem& p, int nblk) {
+static int pair_ms(const TcProblem& p, int nblk, bool q8 = false) {
   if (nblk != 1 || p.M < 512) return 1;
+  (void)q8;  // int8 B: 512-row tiles too (half the conversions per FLOP; tools/q8bench.py)
   if (g_pair_ms == 1 || g_pair_ms == 2) return g_pair_ms;
   return 2;
 }
@@ -956,7 +958,7 @@ int tc_grouped(const TcOperand& A, const TcOperand& B, const TcProblem& p, cudaS
     kps = (kps + BK - 1) / BK * BK;
     a.kps = static_cast<int>(kps > 0 ? kps : BK);
     // 512-row pair tiles for single products tall enough to use them
-    const int ms = pair_ms(p, nblk);
+    const int ms = pair_ms(p, nblk, q8);
     a.m_tiles = static_cast<int>((p.M + 256 * ms - 1) / (256 * ms));
     a.n_tiles = static_cast<int>(p.N / 256);
     a.a_g0 = p.a_g0; a.a_g1 = p.a_g1; a.b_g0 = p.b_g0; a.b_g1 = p.b_g1;
