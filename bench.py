@@ -38,11 +38,15 @@ METRIC = "POET-X train tokens/s (Llama-1B, 1/2/4/8 B200), peak HBM/GPU, % TC roo
 UNIT = "tokens/s"
 
 
+TRAFFIC_JSON = os.path.join("profiles", "r02", "ncu_gemm_traffic.json")
+
+
 def gemm_traffic():
     """Per-launch DRAM traffic of the dominant kernel from the committed ncu
-    capture (profiles/r01/ncu_gemm_traffic.json, tools/ncu_traffic.sh)."""
+    capture of the current kernel (profiles/r02/ncu_gemm_traffic.json,
+    tools/ncu_traffic.sh + tools/ncu_traffic_json.py)."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_gemm_traffic.json")) as f:
+        with open(os.path.join(ROOT, TRAFFIC_JSON)) as f:
             return json.load(f)["traffic_bytes_per_launch"]
     except Exception:
         return None
@@ -493,7 +497,7 @@ def run_ours(args, rank, world, local_rank):
                 "achieved": round(achieved, 1) if achieved else None, "peak": tf_sus,
                 "unit": "TFLOP/s", "frac": round(achieved / tf_sus, 4) if achieved else None,
                 "traffic": gemm_traffic(), "traffic_unit": "bytes/launch (ncu dram read+write)",
-                "traffic_source": "profiles/r01/ncu_gemm_traffic.json", "launches": cnt.value,
+                "traffic_source": TRAFFIC_JSON, "launches": cnt.value,
                 "share_of_step": round(k_share, 4) if k_share else None,
                 "kernel_ms_per_step": round(tot_ms.value / args.steps, 3) if cnt.value else None,
                 "peak_source": src + " sustained (kernel timed inside a long step)",

@@ -14,7 +14,7 @@ FAMILIES = [
     ("bwd_prep", "CNP glue"), ("pack_dq", "CNP glue"), ("to_bf16", "CNP glue"), ("adamw", "AdamW+norm"),
     ("sqdev", "AdamW+norm"), ("sdpa", "attention"), ("cudnn", "attention"), ("attn_bwd", "attention"),
     ("nvjet", "lm_head GEMMs (cuBLAS)"), ("ce_fwd", "cross-entropy"), ("ce_bwd", "cross-entropy"),
-    ("dequant", "POET-XQ"), ("quant", "POET-XQ"),
+    ("dequant", "POET-XQ"), ("quant", "POET-XQ"), ("cnp_fused", "CNP fused (tcgen05)"), ("merge_tc", "merge (tcgen05)"),
 ]
 
 
