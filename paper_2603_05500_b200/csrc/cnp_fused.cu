@@ -130,47 +130,76 @@ __device__ __forceinline__ int rowp(int i) {
   return i * B - (i * (i + 1)) / 2 - i - 1;
 }
 
-// 32 x 32 tile (rows i0.., columns j0..) of Q, one row per lane:
-// w[x] = Q[i0 + lane, j0 + x].  Lower entries -p(j, i) are read along packed
-// row j (lanes over i: coalesced); upper entries p(i, j) along packed row i
-// with lanes over j (coalesced) into the warp's smem tile, then transposed.
+// Q rows [lo, lo + 128) of one block from the packed parameters staged in
+// shared memory by bulk copies (every global read is a contiguous packed-row
+// segment: no per-element loads on the critical path).  The CTA stages
+//   own:   packed rows [lo, lo + 128) (one contiguous range; 16 B aligned),
+//   front: for a pair's second CTA, columns [lo, lo + 128) of packed rows
+//          j < lo (one 16-byte aligned window per row, pitch FP floats)
+// into `stg` (the free S1/S2 slabs), waits on `bar`, then scatters: element
+// (j, c) of an own row is Q[j, c] (upper) and -Q[c, j] when c is an own row
+// too; a front element is -Q[c, j].  The diagonal is zeroed.
 template <int B>
-__device__ __forceinline__ void q_tile(const float* __restrict__ pk, int i0, int j0, int lane, float* tile,
-                                       float (&w)[32]) {
-  const int i = i0 + lane;
-#pragma unroll
-  for (int x = 0; x < 32; ++x) w[x] = 0.f;
-  if (j0 < i0 + 31) {  // entries below the diagonal: Q[i, j] = -p(j, i)
-#pragma unroll
-    for (int x = 0; x < 32; ++x) {
-      const int j = j0 + x;
-      if (j < i) w[x] = -__ldg(pk + rowp<B>(j) + i);
-    }
+struct Stage {
+  static constexpr int FP = 132;  // front row pitch (floats): 128 + up to 3 of alignment slack, 16 B multiple
+  __device__ static int own_start(int lo) { return rowp<B>(lo) + lo + 1; }
+  __device__ static int own_count(int lo) {
+    const int hi = lo + 128 < B - 1 ? lo + 128 : B - 1;
+    return own_start(hi - 1) + (B - hi) - own_start(lo);  // through the last element of row hi - 1
   }
-  if (j0 + 31 > i0) {  // entries above the diagonal: Q[i, j] = p(i, j)
-#pragma unroll
-    for (int y = 0; y < 32; ++y) {
-      const int ii = i0 + y, jj = j0 + lane;
-      tile[y * 33 + lane] = jj > ii ? __ldg(pk + rowp<B>(ii) + jj) : 0.f;
+};
+template <int B>
+__device__ __forceinline__ void unpack_q_staged(uint8_t* slab, float* stg, const float* __restrict__ pk, int lo,
+                                                uint64_t* bar, uint32_t& bph, int warp, int lane) {
+  using ST = Stage<B>;
+  const int front_rows = lo;  // rows j < lo (pair CTA 1 only)
+  float* own = stg + front_rows * ST::FP;
+  const int os = ST::own_start(lo), oc = ST::own_count(lo);
+  if (warp == 0) {
+    if (lane == 0) {
+      uint32_t bytes = static_cast<uint32_t>(oc) * 4;
+      for (int j = 0; j < front_rows; ++j) {
+        const int g0 = rowp<B>(j) + lo, a = g0 & 3;
+        bytes += static_cast<uint32_t>((a + 128 + 3) / 4 * 16);
+      }
+      mbar_expect_tx(bar, bytes);
     }
     __syncwarp();
-#pragma unroll
-    for (int x = 0; x < 32; ++x) w[x] += tile[lane * 33 + x];
-    __syncwarp();
+    fence_async_smem();  // earlier generic writes to the staging area before the async copies
+    if (lane == 0) {
+      const char* src = reinterpret_cast<const char*>(pk + os);
+      for (uint32_t o = 0; o < static_cast<uint32_t>(oc) * 4; o += 32768) {
+        const uint32_t n = static_cast<uint32_t>(oc) * 4 - o < 32768 ? static_cast<uint32_t>(oc) * 4 - o : 32768;
+        bulk_load_1d(reinterpret_cast<char*>(own) + o, src + o, n, bar);
+      }
+    }
+    for (int j = lane; j < front_rows; j += 32) {
+      const int g0 = rowp<B>(j) + lo, a = g0 & 3;
+      bulk_load_1d(stg + j * ST::FP, pk + (g0 - a), static_cast<uint32_t>((a + 128 + 3) / 4 * 16), bar);
+    }
   }
-}
-
-// Q rows [lo, lo + 128) of one block, bf16, into a slab, one 32 x 32 tile per
-// warp pass (all global reads coalesced, 16-byte swizzled smem stores)
-template <int B>
-__device__ __forceinline__ void unpack_q(uint8_t* slab, const float* __restrict__ pk, int lo, int warp, int lane,
-                                         float* tile) {
-  for (int tt = warp; tt < 4 * (B / 32); tt += 8) {
-    const int i0 = lo + (tt / (B / 32)) * 32, j0 = (tt % (B / 32)) * 32;
-    float w[32];
-    q_tile<B>(pk, i0, j0, lane, tile, w);
-    store32(slab, i0 - lo + lane, j0, w);
+  mbar_wait(bar, bph);
+  bph ^= 1;
+  auto put = [&](int r, int c, float v) {
+    *reinterpret_cast<__nv_bfloat16*>(slab + soff(r, c & ~7) + (c & 7) * 2) = __float2bfloat16_rn(v);
+  };
+  // own packed rows: upper entries of own rows, and their transposes when the column is an own row
+  const int hi = lo + 128 < B - 1 ? lo + 128 : B - 1;
+  for (int j = lo + warp; j < hi; j += 8) {
+    const float* row = own + (rowp<B>(j) - os);
+    for (int c = j + 1 + lane; c < B; c += 32) {
+      const float v = row[c];
+      put(j - lo, c, v);
+      if (c < lo + 128) put(c - lo, j, -v);
+    }
   }
+  // front rows (j < lo): -Q[c, j] for the own columns c
+  for (int j = warp; j < front_rows; j += 8) {
+    const float* row = stg + j * ST::FP + ((rowp<B>(j) + lo) & 3) - lo;
+#pragma unroll 4
+    for (int c = lo + lane; c < lo + 128; c += 32) put(c - lo, j, -row[c]);
+  }
+  if (threadIdx.x < 128) put(threadIdx.x, lo + threadIdx.x, 0.f);
 }
 
 // 32 x 32 tile of N1 = dG, one row per lane: a[x] = N1[i0 + lane, j0 + x]
@@ -253,7 +282,8 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   float* tile = reinterpret_cast<float*>(smem + 3 * CF::SLAB) + warp * (32 * 33);
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * CF::SLAB + 8 * CF::TILE);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 1);
+  uint64_t* sbar = bar + 1;  // packed-parameter staging (bulk copies)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
 
   const uint32_t rank = CF::PAIR ? pair::cta_rank() : 0;
   const bool issuer = rank == 0 && threadIdx.x == 0;
@@ -265,6 +295,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(bar, 1);
+    mbar_init(sbar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 2) {
@@ -287,8 +318,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t A0 = tmem, A1 = tmem + B;                           // accumulators (columns)
   const uint32_t tl = static_cast<uint32_t>((warp & 3) * 32) << 16;  // this warp's TMEM lanes
   const uint32_t s0 = smem_u32(S0), s1 = smem_u32(S1), s2 = smem_u32(S2);
-  uint32_t phase = 0;
+  uint32_t phase = 0, sphase = 0;
   constexpr int64_t PAIRS = static_cast<int64_t>(B) * (B - 1) / 2;
+  float* stg = reinterpret_cast<float*>(S1);  // packed staging over S1 / S2 (free at unpack time)
+  // largest staging: pair CTA 1 (front 128 x FP + own 8,128) or CTA 0 / b = 128 (own only)
+  static_assert((CF::PAIR ? 128 * Stage<B>::FP + 8128 : 8128) * 4 <= 2 * CF::SLAB && 24512 * 4 <= 2 * 128 * 256 * 2,
+                "packed staging must fit in two slabs");
 
   for (int64_t s = unit; s < nb; s += units) {
     const float* pk = packed + s * PAIRS;
@@ -308,7 +343,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if constexpr (FWD) {
       // ---- S0 <- Q
-      unpack_q<B>(S0, pk, lo, warp, lane, tile);
+      unpack_q_staged<B>(S0, stg, pk, lo, sbar, sphase, warp, lane);
       publish<B>();
       if (issuer) {
         mma<B>(A0, s0, s0, NEG_B, false);  // Q Q = S0 (-S0)^T
@@ -370,7 +405,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float* n1 = dg + s * static_cast<int64_t>(B) * B;
       // ---- S0 <- Q ; S1 <- E = N1 - N1^T ; S2 <- F = N1 + N1^T ; A1 <- E (fp32)
       // (warp w owns TMEM lanes [32 (w & 3), +32): its tiles are that row group)
-      unpack_q<B>(S0, pk, lo, warp, lane, tile);
+      unpack_q_staged<B>(S0, stg, pk, lo, sbar, sphase, warp, lane);
+      __syncthreads();  // the staging (S1 / S2) is read before E / F overwrite it
       for (int k = 0; k < B / 64; ++k) {
         const int i0 = lo + (warp & 3) * 32, j0 = ((warp >> 2) * (B / 64) + k) * 32;
         float a[32], t[32];
