@@ -534,7 +534,7 @@ int launch(int64_t nb, const float* packed, const float* dg, __nv_bfloat16* g16,
   const int64_t sms = num_sms();
   unsigned grid;
   if constexpr (CF::PAIR) {
-    const int64_t pairs = balanced_workers(nb, sms / 2);
+    const int64_t pairs = nb < sms / 2 ? nb : sms / 2;
     grid = static_cast<unsigned>(2 * pairs);
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
@@ -557,7 +557,7 @@ int launch(int64_t nb, const float* packed, const float* dg, __nv_bfloat16* g16,
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, THREADS, CF::SMEM);
       return n < 1 ? 1 : n;
     }();
-    const int64_t ctas = balanced_workers(nb, per_sm * sms);
+    const int64_t ctas = nb < per_sm * sms ? nb : per_sm * sms;
     grid = static_cast<unsigned>(ctas);
     void* pf = prof_begin(st);
     kern<<<grid, THREADS, CF::SMEM, st>>>(nb, packed, dg, g16, g32, dpacked, accumulate);

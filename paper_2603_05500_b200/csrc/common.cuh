@@ -107,17 +107,6 @@ __device__ __forceinline__ Dst cvt(Src x) {
   return Conv<Dst>::from_f(static_cast<A>(Conv<Src>::to_f(x)));
 }
 
-// Persistent grids: the fewest workers that still finish `units` equal work
-// items in the same number of rounds as `max_workers` would (e.g. 154 CNP
-// blocks on 74 SM pairs: 3 rounds either way, so 52 pairs; 128 GEMM tiles:
-// 2 rounds, 64 pairs).  The kernel takes as long, and the SMs it does not
-// need stay free for the kernels other streams run concurrently.
-inline int64_t balanced_workers(int64_t units, int64_t max_workers) {
-  if (units <= 0 || max_workers <= 0) return 0;
-  const int64_t rounds = (units + max_workers - 1) / max_workers;
-  return (units + rounds - 1) / rounds;
-}
-
 inline unsigned grid_for(int64_t n, int threads, int64_t cap = 148 * 32) {
   int64_t g = (n + threads - 1) / threads;
   if (g < 1) g = 1;

@@ -356,7 +356,7 @@ int launch(const Args& a, cudaStream_t st) {
   const double flops = 5.0 * 2.0 * B * B * static_cast<double>(B) * tiles;  // 2 + 3 products per tile
   void* pf = prof_begin(st);
   if constexpr (CF::PAIR) {
-    const int64_t pairs = balanced_workers(tiles, sms / 2);
+    const int64_t pairs = tiles < sms / 2 ? tiles : sms / 2;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;

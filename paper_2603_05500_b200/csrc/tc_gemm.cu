@@ -847,7 +847,7 @@ int launch_t(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap& mc
     attr_set = true;
   }
   int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles * a.splits * a.groups;
-  int grid = static_cast<int>(balanced_workers(tiles, num_sms()));
+  int grid = static_cast<int>(tiles < num_sms() ? tiles : num_sms());
   if (grid <= 0) return POETX_OK;
   void* tok = prof_begin(st);
   tc_kernel<BN, A_MN, B_MN, MS><<<grid, THREADS, Cfg<BN, MS>::SMEM_BYTES, st>>>(ma, mb, mc, a);
@@ -900,7 +900,8 @@ int launch_pair(const CUtensorMap& ma, const CUtensorMap& mb, const CUtensorMap&
     attr_set = true;
   }
   const int64_t tiles = static_cast<int64_t>(a.m_tiles) * a.n_tiles * a.splits * a.groups;
-  const int grid = static_cast<int>(2 * balanced_workers(tiles, num_sms() / 2));
+  const int64_t pairs = num_sms() / 2;
+  const int grid = static_cast<int>(2 * (tiles < pairs ? tiles : pairs));
   if (grid <= 0) return POETX_OK;
   void* tok = prof_begin(st);
   pair::tc2_kernel<MS, A_MN, B_MN, Q8><<<grid, Q8 ? pair::Q8_THREADS : THREADS, PC::SMEM, st>>>(ma, mb, mc, a);
