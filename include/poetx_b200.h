@@ -245,15 +245,19 @@ typedef struct {
                           * CNP (the merge uses it for accuracy). */
   void* q2_p;
   /* optional precomputed weight folds of a BF16 layer (else built per call):
-   * w_in_fold = bd(G_R) PM, w_out_fold = PM bd(G_P), both [m, n] bf16 */
+   * w_in_fold = bd(G_R) PM, w_out_fold = PM bd(G_P), both [m, n] bf16 --
+   * for a POET-XQ layer with b = 256 and m % 256 == 0, w_out_fold is stored
+   * transposed ([n, m]), as poetx_layer_weight_fold(which = 1) writes it */
   const void* w_in_fold;
   const void* w_out_fold;
 } poetx_layer_factors_t;
 
 size_t poetx_layer_workspace_bytes(const poetx_layer_desc* d, int64_t T);
 /* BF16 weight folds: which = 0 -> out = bd(G_R) PM, 1 -> out =
- * PM bd(G_P), from the factors' bf16 G (and the dequantized int8 base);
- * out is [m, n] bf16.  ws >= poetx_layer_workspace_bytes(d, 0). */
+ * PM bd(G_P), from the factors' bf16 G; out is [m, n] bf16.  POET-XQ bases:
+ * the int8 codes are dequantized inside the GEMM producer where the pair
+ * kernel takes them (b = 256), and which = 1 then writes (PM bd(G_P))^T,
+ * [n, m], the layout the layer backward reads.  ws >= poetx_layer_workspace_bytes(d, 0). */
 int poetx_layer_weight_fold(const poetx_layer_desc* d, const poetx_layer_factors_t* f, int which, void* out,
                             void* ws, size_t ws_bytes, void* stream);
 int poetx_layer_factors(const poetx_layer_desc* d, poetx_layer_factors_t* f, void* ws,

@@ -18,6 +18,8 @@ int apply_weight_rows(int dt, int64_t nb, int64_t b, int64_t cols, const void* g
                       const void* w, void* y, cudaStream_t st);
 int apply_weight_rows_q8(int64_t nb, int64_t b, int64_t cols, const void* g, const int8_t* codes,
                          const float* scales, void* y, cudaStream_t st);
+int apply_weight_cols_t_q8(int64_t m, int64_t nb, int64_t b, const void* g_p, const int8_t* codes,
+                           const float* scales, void* y, cudaStream_t st);
 int tc_matmul_q8(int64_t M, int64_t N, int64_t K, const void* A, int64_t lda, int transA, const int8_t* B,
                  int64_t ldb, int transB, const float* scales, void* C, int64_t ldc, cudaStream_t st);
 constexpr int kNotSupported = -100;  // POETX_ENOTSUPPORTED (tc_gemm.cuh)
@@ -103,6 +105,12 @@ bool q8_main() {
   }();
   return on != 0;
 }
+// the backward weight fold W1 of a POET-XQ layer is built as W1^T straight
+// from the codes (pair GEMM, b = 256, m % 256 == 0); the adjoint reads it
+// as its K x N operand
+bool w1_transposed(const poetx_layer_desc* d) {
+  return q8_gemm(d) && d->b == 256 && d->m % 256 == 0;
+}
 struct PmSource {
   const poetx_layer_desc* d;
   void* scratch;  // reserve_deq
@@ -144,8 +152,16 @@ struct PmSource {
     POETX_TRY(get(pm));
     return apply_weight_rows(d->dtype, d->m / d->b, d->b, d->n, g_r, 0, pm, out, st);
   }
-  // W1 = PM bd(G_P)
+  // W1 = PM bd(G_P) -- stored TRANSPOSED ([n, m]) for POET-XQ layers that
+  // take codes (w1_transposed), so its producer can read the codes
   int fold_out(const void* g_p, void* out) {
+    if (w1_transposed(d)) {
+      int rc = apply_weight_cols_t_q8(d->m, d->n / d->b, d->b, g_p, d->pm_codes,
+                                      static_cast<const float*>(d->pm_scales), out, st);
+      if (rc != kNotSupported) return rc;
+      set_error("layer: transposed int8 fold unsupported for this shape");
+      return POETX_ESHAPE;
+    }
     const void* pm;
     POETX_TRY(get(pm));
     return apply_features(d->dtype, d->m, d->n / d->b, d->b, g_p, 0, pm, out, st);
@@ -435,7 +451,10 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
     // da = dv (PM bd(G_P))^T  (layer.py:248-249 with dt folded into the weight)
     if (own_w1) POETX_TRY(pm.fold_out(gp, w1));
     const void* wo = own_w1 ? w1 : f->w_out_fold;
-    POETX_TRY(poetx_matmul(dt, T, d->m, d->n, dv, d->n, 0, wo, d->n, 1, b3, d->m, 0, stream));
+    if (w1_transposed(d))  // W1^T [n, m] is the K x N operand
+      POETX_TRY(poetx_matmul(dt, T, d->m, d->n, dv, d->n, 0, wo, d->m, 0, b3, d->m, 0, stream));
+    else
+      POETX_TRY(poetx_matmul(dt, T, d->m, d->n, dv, d->n, 0, wo, d->n, 1, b3, d->m, 0, stream));
   } else {
     // dt = dv blockdiag(G_P)^T  (layer.py:248)
     POETX_TRY(apply_features(dt, T, nbp, b, gp, 1, dv, b2, st));

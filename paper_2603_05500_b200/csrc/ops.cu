@@ -610,6 +610,26 @@ int apply_weight_rows_q8(int64_t nb, int64_t b, int64_t cols, const void* g, con
   return tc_grouped(A, B, p, st);
 }
 
+// POET-XQ: y = W1^T [n, m] for W1 = PM bd(G_P), with the codes dequantized in
+// the pair GEMM's producer: y[t*b + i, j] = sum_k G_P[t][k, i] PM[j, t*b + k]
+// (A = G_P[t] read MN-major, B = the b code columns of block t, K-major, one
+// scale per PM row j).  The adjoint then reads y as its K x N operand.
+int apply_weight_cols_t_q8(int64_t m, int64_t nb, int64_t b, const void* g_p, const int8_t* codes,
+                           const float* scales, void* y, cudaStream_t st) {
+  if (nb <= 0 || m <= 0) return POETX_OK;
+  if (!tc_enabled() || b != 256 || m % 256) return POETX_ENOTSUPPORTED;
+  TcOperand A{g_p, nb * b, b, b, true};
+  TcOperand B{codes, m, nb * b, nb * b, false, scales};
+  TcProblem p{};
+  p.M = b; p.N = m; p.K = b; p.groups = static_cast<int>(nb); p.splits = 1;
+  p.bn = 256;
+  p.a_g1 = static_cast<int>(b);
+  p.b_g0 = static_cast<int>(b);
+  p.C = y; p.ldc = m; p.c_goff = b * m;
+  p.alpha = 1.0f; p.name = "tc_wfold_t_q8"; p.tma_epi = 1;
+  return tc_grouped(A, B, p, st);
+}
+
 int apply_weight_rows(int dt, int64_t nb, int64_t b, int64_t cols, const void* g, int transpose,
                       const void* w, void* y, cudaStream_t st) {
   if (nb <= 0 || cols <= 0) return POETX_OK;

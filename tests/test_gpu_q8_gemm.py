@@ -114,6 +114,29 @@ def test_quantized_weight_fold_bitwise(N):
     assert torch.equal(got, want)
 
 
+def test_quantized_transposed_out_fold(N):
+    """W1^T = (PM bd(G_P))^T straight from the codes (which = 1 of a POET-XQ
+    layer at b = 256) against the transposed fold of the dequantized weight
+    (bf16 output: within one bf16 rounding)."""
+    m, n, b = 768, 1024, 256
+    g = torch.Generator(device="cuda").manual_seed(9)
+    codes = torch.randint(-127, 128, (m, n), device="cuda", generator=g, dtype=torch.int8)
+    scales = torch.rand(m, device="cuda", generator=g) * 0.02 + 1e-3
+    g_p = (torch.eye(b, device="cuda") + 0.05 * torch.randn((n // b, b, b), device="cuda", generator=g)).to(torch.bfloat16)
+    w = dequant(N, codes, scales).float()
+    want = torch.einsum("jsk,ski->jsi", w.view(m, n // b, b), g_p.float()).reshape(m, n).t()
+    d = N.LayerDesc()
+    d.dtype, d.variant, d.neumann_k, d.m, d.n, d.b = N.BF16, N.MEM, 3, m, n, b
+    d.fold_weight = 1
+    d.pm_codes, d.pm_scales = codes.data_ptr(), scales.data_ptr()
+    f = N.LayerFactors(None, None, None, None, g_p.data_ptr(), g_p.data_ptr(), None, None)
+    got = torch.empty((n, m), dtype=torch.bfloat16, device="cuda")
+    ws, wsb = N.workspace(int(N.lib().poetx_layer_workspace_bytes(d, 0)))
+    N.call("poetx_layer_weight_fold", d, f, 1, got.data_ptr(), ws, wsb, N.stream_ptr())
+    torch.cuda.synchronize()
+    assert float((got.float() - want).abs().max()) <= 2 ** -8 * float(want.abs().max())
+
+
 @pytest.mark.parametrize("fold", [True, False], ids=["weight_folded", "activation_side"])
 def test_quantized_bf16_layer_b256_vs_float64_oracle(fold):
     """A POET-XQ bf16 layer at b = 256 (the shapes where the fused int8 GEMM
