@@ -523,8 +523,10 @@ def run_ours(args, rank, world, local_rank):
 
         gc.collect()
         torch.cuda.synchronize(dev)
+        N.WORKSPACE.release_all()  # its graph is gone: its pinned workspaces may go too
         torch.cuda.empty_cache()
         for key, fn in (("mem_variant", lambda: mem_variant(args, dev, tf_burst, tf_sus)),
+                        ("xq_variant", lambda: mem_variant(args, dev, tf_burst, tf_sus, quantized=True)),
                         ("lora_same_box", lambda: lora_same_box(args, dev)),
                         ("cfg1_gpu", lambda: gpu_cfg1(dev))):
             try:
@@ -532,6 +534,8 @@ def run_ours(args, rank, world, local_rank):
             except Exception as e:  # reported, never fatal to the headline line
                 out[key] = {"error": f"{type(e).__name__}: {e}"[:300]}
             gc.collect()
+            torch.cuda.synchronize(dev)
+            N.WORKSPACE.release_all()
             torch.cuda.empty_cache()
         lora, mem = out.get("lora_same_box", {}), out.get("mem_variant", {})
         if "peak_hbm_gb" in lora and "peak_hbm_gb" in mem:
@@ -586,16 +590,17 @@ def _timed_steps(step, batches, n):
     return a.elapsed_time(e)
 
 
-def mem_variant(args, dev, tf_burst, tf_sus):
+def mem_variant(args, dev, tf_burst, tf_sus, quantized=False):
     """The same workload with the mem variant (the reference's memory-saving
     layer, layer.py:244-246: no weight-sized activation is saved; t is
     recomputed in backward): CUDA graph, same steps, peak HBM of an eager step
-    (allocated) like the headline line's eager figure."""
+    (allocated) like the headline line's eager figure.  ``quantized``: the
+    POET-XQ int8 frozen base (layer.py:169-210, quant.py)."""
     import torch
 
     from paper_2603_05500_b200.trainer import Trainer, llama_config
 
-    cfg = llama_config(args.model, variant="mem")
+    cfg = llama_config(args.model, variant="mem", quantized=quantized)
     tr = Trainer(cfg, args.micro_batch, seed=args.seed, merge_gap=0, device=dev)
     B, S = args.micro_batch, cfg.seq
     gen = torch.Generator().manual_seed(2000)

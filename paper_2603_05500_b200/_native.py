@@ -259,6 +259,14 @@ class _WorkspacePool:
             self._pinned.add(buf.data_ptr())
         return buf
 
+    def release_all(self):
+        """Drop every buffer, pinned and retired ones included.  Only for when
+        no captured graph that used them can replay again (e.g. after the
+        Trainer that captured it is gone): otherwise use ``clear``."""
+        self._bufs.clear()
+        self._pinned.clear()
+        self._retired.clear()
+
     def clear(self):
         """Drop the unpinned buffers (pinned ones stay: a graph may replay them)."""
         keep = {k: b for k, b in self._bufs.items() if b.data_ptr() in self._pinned}

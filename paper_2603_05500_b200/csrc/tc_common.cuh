@@ -194,6 +194,13 @@ __device__ __forceinline__ void arrive_leader(uint64_t* bar) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & PEER_MASK)
                : "memory");
 }
+// arrive on the leader CTA's copy of a barrier with the default (CTA-scope)
+// release, as CUTLASS's ClusterBarrier::arrive(cta_id) does: no GPU-scope
+// membar on the signalling path (the writes it publishes are this CTA's own
+// shared-memory operand stores, already fenced to the async proxy)
+__device__ __forceinline__ void arrive_leader_cta(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(smem_u32(bar) & PEER_MASK) : "memory");
+}
 __device__ __forceinline__ void wait_cluster(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   uint32_t spins = 0;

@@ -388,6 +388,14 @@ struct PCfg {
   static constexpr int SMEM = STAGES * STAGE + RAW_STAGES * RAW_SLOT + EPI + 1024 + 256;
   static constexpr int TILE_M = 256 * MS;
 };
+// POETX_Q8_ARRIVE=cluster: converters publish with a cluster-scope release (A/B)
+__device__ __forceinline__ bool q8_cta_arrive() {
+#ifdef POETX_Q8_CLUSTER_ARRIVE
+  return false;
+#else
+  return true;
+#endif
+}
 // Q8 CTAs carry 4 more warps (8..11): warp 3 loads codes, warps 2 and 8..11 convert
 constexpr int Q8_THREADS = THREADS + 128, Q8_CONV_WARPS = 5;
 template <int MS, bool A_MN, bool B_MN, bool Q8 = false>
@@ -533,7 +541,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
         // every converter warp's stores are in (named barrier 1 over the
         // converter warps), then ONE cluster-scope release arrival per CTA
         asm volatile("bar.sync 1, %0;" ::"n"(32 * Q8_CONV_WARPS) : "memory");
-        if (ct == 0) arrive_leader(&full[stage]);
+        if (ct == 0) {
+          if (q8_cta_arrive()) arrive_leader_cta(&full[stage]);
+          else arrive_leader(&full[stage]);
+        }
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
         if (++rs == RSTG) { rs = 0; rph ^= 1; }
       }
