@@ -87,7 +87,8 @@ int reserve_deq(const poetx_layer_desc* d, Workspace& w, void*& out) {
 // producer (dequantized on chip, bit-identical to the dequantizer + bf16
 // GEMM): mm2, the adjoint and the W2 = bd(G_R) PM fold.  Only products that
 // cannot (W1 = PM bd(G_P), non-pair shapes) dequantize PM into workspace
-// scratch -- lazily, once per call.  POETX_Q8_GEMM=0: always dequantize (A/B).
+// scratch -- lazily, once per call.  POETX_Q8_GEMM=0: always dequantize,
+// =1: folds only (A/B).
 bool q8_gemm(const poetx_layer_desc* d) {
   static int on = [] {
     const char* e = getenv("POETX_Q8_GEMM");
@@ -95,13 +96,13 @@ bool q8_gemm(const poetx_layer_desc* d) {
   }();
   return on && quantized(d) && d->dtype == POETX_BF16 && d->n % 16 == 0;
 }
-// the main products (mm2 / adjoint) take codes only when POETX_Q8_GEMM=2:
-// the on-chip converter does not keep up with the MMA rate there yet
-// (tools/q8bench.py), so they dequantize by default
+// the main products (mm2 / adjoint) take codes too unless POETX_Q8_GEMM=1
+// (folds only; tools/q8bench.py: at or below dequantize + GEMM at the
+// Llama-8B shapes, within 5% at the 1B ones)
 bool q8_main() {
   static int on = [] {
     const char* e = getenv("POETX_Q8_GEMM");
-    return e && e[0] == '2' ? 1 : 0;
+    return e && e[0] == '1' ? 0 : 1;
   }();
   return on != 0;
 }

@@ -396,8 +396,11 @@ __device__ __forceinline__ bool q8_cta_arrive() {
   return true;
 #endif
 }
-// Q8 CTAs carry 4 more warps (8..11): warp 3 loads codes, warps 2 and 8..11 convert
-constexpr int Q8_THREADS = THREADS + 128, Q8_CONV_WARPS = 5;
+// Q8 CTAs carry POETX_Q8_EXTRA_WARPS more warps (8..): warp 3 loads codes, warps 2 and 8.. convert
+#ifndef POETX_Q8_EXTRA_WARPS
+#define POETX_Q8_EXTRA_WARPS 8  /* 9 converter warps: the conversion keeps up with the MMAs (tools/q8bench.py) */
+#endif
+constexpr int Q8_THREADS = THREADS + 32 * POETX_Q8_EXTRA_WARPS, Q8_CONV_WARPS = 1 + POETX_Q8_EXTRA_WARPS;
 template <int MS, bool A_MN, bool B_MN, bool Q8 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : THREADS, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
