@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define POETX_ABI_VERSION 2
+#define POETX_ABI_VERSION 3
 
 /* element types */
 enum { POETX_F32 = 0, POETX_F64 = 1, POETX_BF16 = 2 };
@@ -218,14 +218,20 @@ typedef struct {
   const void* premerged;       /* device [m, n] = W[pi_in(i), pi_out(j)] */
   /* POET-XQ (mem variant only, quant.py): when pm_codes != NULL the frozen
    * weight is int8 codes [m, n] of the premerged matrix with per-row scales
-   * [m] (F64 for F64 layers, else F32) and premerged is ignored; each call
-   * dequantizes into its workspace right before the mm2 / adjoint GEMM. */
+   * [m] (F64 for F64 layers, else F32) and premerged is ignored.  BF16
+   * layers at b = 256 feed the codes straight into the pair GEMM's producer
+   * (dequantized on chip); other shapes dequantize into the call's workspace
+   * right before the product. */
   const int8_t* pm_codes;
   const void* pm_scales;
   /* BF16 layers: nonzero -> reassociated products, the block factors folded
    * into the frozen weight (bd(G_R) PM, PM bd(G_P)) -- fewer bytes
    * when T is large against n*b; zero -> factors applied to the activations. */
   int fold_weight;
+  /* optional caller-owned stream (cudaStream_t) for the backward's two
+   * segmented outer products, forked and joined with per-call events; NULL:
+   * everything on the call's stream.  Must differ from the call's stream. */
+  void* side_stream;
 } poetx_layer_desc;
 
 /* factor state produced by poetx_layer_factors and consumed by fwd/bwd.

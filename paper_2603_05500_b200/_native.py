@@ -21,7 +21,7 @@ from .errors import ConfigError, NumericsError, PoetxError, ShapeError, StateErr
 LIB_PATH = os.environ.get("POETX_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
                                                            "libpoetx_b200.so")
 
-ABI_VERSION = 2  # must equal POETX_ABI_VERSION (include/poetx_b200.h) of the loaded build
+ABI_VERSION = 3  # must equal POETX_ABI_VERSION (include/poetx_b200.h) of the loaded build
 F32, F64, BF16 = 0, 1, 2
 FAST, MEM = 0, 1
 IN_GATHERED, OUT_UNSCATTERED, DZ_GATHERED, DX_UNSCATTERED = 1, 2, 4, 8
@@ -60,6 +60,7 @@ class LayerDesc(C.Structure):
         ("pm_codes", VP),
         ("pm_scales", VP),
         ("fold_weight", C.c_int),
+        ("side_stream", VP),
     ]
 
 

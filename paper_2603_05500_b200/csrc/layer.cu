@@ -2,8 +2,6 @@
 // factors (CNP on both sides), forward chain, backward chain, merge.
 // Kernels are stream-ordered; nothing here synchronises the host.
 #include <cstdlib>
-#include <mutex>
-#include <unordered_map>
 
 #include "common.cuh"
 #include "simt_gemm.cuh"
@@ -239,15 +237,12 @@ int gather_to(int src_dt, int dst_dt, int64_t rows, int64_t cols, const int32_t*
   return POETX_ESHAPE;
 }
 
-// Side stream per calling stream for the backward's segmented outer
-// products (dG_P = t^T dv, dG_R = u^T da), which only READ buffers the main
-// chain (dt -> adjoint GEMM -> du) reads too: forked and joined with events,
-// so they fill the SMs the main chain's kernel tails leave idle.  Inside a
-// CUDA-graph capture the fork/join become graph edges.
-struct Side {
-  cudaStream_t s = nullptr;
-  cudaEvent_t e0 = nullptr, e1 = nullptr, e2 = nullptr;
-};
+// The backward's two segmented outer products (dG_P = t^T dv, dG_R = u^T da)
+// only READ buffers the main chain (dt -> adjoint GEMM -> du) reads too, so
+// they fork onto the caller-owned desc->side_stream with events and join at
+// the end: they fill the SMs the main chain's kernel tails leave idle.
+// Inside a CUDA-graph capture the fork/join become graph edges.  The events
+// live for one call; the library keeps no stream or event of its own.
 bool side_enabled() {
   static int on = [] {
     const char* e = getenv("POETX_LAYER_SIDE");
@@ -255,24 +250,29 @@ bool side_enabled() {
   }();
   return on != 0;
 }
-Side* side_for(cudaStream_t st) {
-  static std::mutex mu;
-  static std::unordered_map<cudaStream_t, Side> sides;
-  std::lock_guard<std::mutex> lk(mu);
-  auto it = sides.find(st);
-  if (it != sides.end()) return &it->second;
-  Side sd;
-  int prio = 0;
-  cudaStreamGetPriority(st, &prio);
-  if (cudaStreamCreateWithPriority(&sd.s, cudaStreamNonBlocking, prio) != cudaSuccess ||
-      cudaEventCreateWithFlags(&sd.e0, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&sd.e1, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&sd.e2, cudaEventDisableTiming) != cudaSuccess) {
-    cudaGetLastError();
-    return nullptr;
+struct Side {
+  cudaStream_t s = nullptr;
+  cudaEvent_t e[3] = {nullptr, nullptr, nullptr};
+  explicit Side(void* stream) {
+    if (!stream) return;
+    for (auto& ev : e) {
+      if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        release();
+        return;
+      }
+    }
+    s = as_stream(stream);
   }
-  return &sides.emplace(st, sd).first->second;
-}
+  void release() {
+    for (auto& ev : e) {
+      if (ev) cudaEventDestroy(ev);  // deferred by the driver until the event completes
+      ev = nullptr;
+    }
+    s = nullptr;
+  }
+  ~Side() { release(); }
+};
 
 }  // namespace
 
@@ -440,11 +440,12 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   }
   // the two segmented outer products run on a side stream unless the main
   // chain would overwrite dv's buffer with u (b1) while the first one reads it
-  Side* sd = (side_enabled() && (dz_gathered || in_gathered)) ? side_for(st) : nullptr;
+  Side side((side_enabled() && (dz_gathered || in_gathered)) ? d->side_stream : nullptr);
+  Side* sd = side.s ? &side : nullptr;
   cudaStream_t so = sd ? sd->s : st;
   if (sd) {
-    cudaEventRecord(sd->e0, st);
-    cudaStreamWaitEvent(so, sd->e0, 0);
+    cudaEventRecord(sd->e[0], st);
+    cudaStreamWaitEvent(so, sd->e[0], 0);
   }
   // dG_P = segmented_outer(t, dv)  (layer.py:247)
   POETX_TRY(segmented_outer(dt, T, nbp, b, t, dv, dgp, dg_acc, tail, so));
@@ -471,8 +472,8 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
   // dG_R = segmented_outer(u, da)  (layer.py:251)
   Workspace tail2(static_cast<char*>(ws) + wsp.used, ws_bytes - wsp.used);
   if (sd) {
-    cudaEventRecord(sd->e1, st);
-    cudaStreamWaitEvent(so, sd->e1, 0);
+    cudaEventRecord(sd->e[1], st);
+    cudaStreamWaitEvent(so, sd->e[1], 0);
   }
   POETX_TRY(segmented_outer(dt, T, nbr, b, u, b3, dgr, dg_acc, tail2, so));
   if (dx) {
@@ -485,8 +486,8 @@ static int layer_backward_impl(const poetx_layer_desc* d, const poetx_layer_fact
     }
   }
   if (sd) {  // join: everything after this call sees dG_R / dG_P
-    cudaEventRecord(sd->e2, so);
-    cudaStreamWaitEvent(st, sd->e2, 0);
+    cudaEventRecord(sd->e[2], so);
+    cudaStreamWaitEvent(st, sd->e[2], 0);
   }
   if (dg_mode) return POETX_OK;
   // packed grads = P(cnp_backward(.))  (layer.py:254-255)

@@ -279,6 +279,15 @@ class PoetLinearLayer:
 
     # -- descriptor ----------------------------------------------------------------
 
+    def _side_stream(self) -> int | None:
+        """This layer's own stream for the backward's segmented outer products
+        (csrc/layer.cu forks onto it), created on first use."""
+        if self.device.type != "cuda":
+            return None
+        if getattr(self, "_side", None) is None:
+            self._side = torch.cuda.Stream(self.device)
+        return self._side.cuda_stream
+
     def _desc(self) -> N.LayerDesc:
         fi, ii = self.perm_in.device(self.device)
         fo, io = self.perm_out.device(self.device)
@@ -290,6 +299,7 @@ class PoetLinearLayer:
         d.perm_in_fwd, d.perm_in_inv = fi.data_ptr(), ii.data_ptr()
         d.perm_out_fwd, d.perm_out_inv = fo.data_ptr(), io.data_ptr()
         d.fold_weight = int(getattr(self, "fold_weight", True))
+        d.side_stream = self._side_stream()
         if self.quantized:
             d.premerged = None
             d.pm_codes = self._pm.codes.data_ptr()

@@ -286,6 +286,8 @@ class PoetLinear(torch.nn.Module):
         d.perm_in_fwd, d.perm_in_inv = fi.data_ptr(), ii.data_ptr()
         d.perm_out_fwd, d.perm_out_inv = fo.data_ptr(), io.data_ptr()
         d.fold_weight = int(getattr(self, "fold_weight", True))
+        side = getattr(self, "side_stream", None)  # set by the model: one per projection kind
+        d.side_stream = side.cuda_stream if side is not None else None
         if self.quantized:
             d.pm_codes, d.pm_scales = self.codes.data_ptr(), self.scales.data_ptr()
         else:
@@ -759,6 +761,15 @@ class PoetLlama(torch.nn.Module):
                                      variant=cfg.variant, neumann_k=cfg.neumann_k, device=dev,
                                      quantized=cfg.quantized)
             self.layers.append(mods)
+        # one stream per projection kind for the layers' backward segmented
+        # outer products (csrc/layer.cu forks them there): kinds that run
+        # concurrently never share one, blocks (sequential) do
+        if dev.type == "cuda":
+            self.outer_streams = {p: torch.cuda.Stream(dev) for p in self.PROJ}
+            for mods in self.layers:
+                for p, mod in mods.items():
+                    mod.side_stream = self.outer_streams[p]
+                    mod._set_desc()
         hd = cfg.head_dim
         inv = 1.0 / (10000 ** (torch.arange(0, hd, 2, device=dev, dtype=torch.float32) / hd))
         ang = torch.outer(torch.arange(cfg.seq, device=dev, dtype=torch.float32), inv)

@@ -32,7 +32,7 @@ def test_library_exports_every_header_symbol():
         assert hasattr(lib, s), s
     # and the Python binding declares a signature for every one of them
     assert set(syms) == set(N.EXPORTED_SYMBOLS)
-    assert lib.poetx_abi_version() == N.ABI_VERSION == 2
+    assert lib.poetx_abi_version() == N.ABI_VERSION == 3
 
 
 def test_library_is_sm100a():
