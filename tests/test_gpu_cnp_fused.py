@@ -88,3 +88,37 @@ def test_fused_cnp_rejects_unsupported_block(N):
     assert N.lib().poetx_cnp_fused_supported(64) == 0 and N.lib().poetx_cnp_fused_supported(256) == 1
     with pytest.raises(ShapeError):
         N.call("poetx_cnp_forward_fused", 1, 64, 1, 1, None, N.stream_ptr())
+
+
+def test_fused_cnp_llama1b_stack_vs_unfused_tensor_core_path(N):
+    """The whole Llama-1B block stack (3,696 blocks of 256: 50 persistent
+    rounds of the CTA pairs, L2 prefetch and bulk-copy staging across
+    blocks) against the unfused tensor-core CNP (csrc/cnp_tc.cu) on the same
+    inputs, and every G orthogonal to the CNP's truncation order."""
+    nb, b = 3696, 256
+    pairs = b * (b - 1) // 2
+    g = torch.Generator(device="cuda").manual_seed(3696)
+    pk = torch.randn((nb, pairs), device="cuda", generator=g) * 0.01
+    dg = torch.randn((nb, b, b), device="cuda", generator=g)
+    st = N.stream_ptr()
+    g16 = torch.empty((nb, b, b), dtype=torch.bfloat16, device="cuda")
+    g32 = torch.empty((nb, b, b), dtype=torch.float32, device="cuda")
+    N.call("poetx_cnp_forward_fused", nb, b, pk.data_ptr(), g16.data_ptr(), g32.data_ptr(), st)
+    gp = torch.empty((nb, pairs), device="cuda")
+    N.call("poetx_cnp_backward_fused", nb, b, pk.data_ptr(), dg.data_ptr(), gp.data_ptr(), 0, st)
+    ws, wsb = N.workspace(N.lib().poetx_cnp_tc_workspace_bytes(nb, b))
+    qq2 = torch.empty((nb, b, 2 * b), dtype=torch.bfloat16, device="cuda")
+    g_tc = torch.empty((nb, b, b), dtype=torch.float32, device="cuda")
+    N.call("poetx_cnp_forward_tc", nb, b, pk.data_ptr(), qq2.data_ptr(), None, g_tc.data_ptr(), ws, wsb, st)
+    gp_tc = torch.empty_like(gp)
+    N.call("poetx_cnp_backward_tc", nb, b, qq2.data_ptr(), dg.data_ptr(), gp_tc.data_ptr(), 0, ws, wsb, st)
+    torch.cuda.synchronize()
+    assert float((g32 - g_tc).abs().max()) <= 2e-2
+    rel = float((gp - gp_tc).norm() / gp_tc.norm())
+    assert rel < 1e-2, rel
+    # per-block worst error against the unfused path: no block skipped or mixed up
+    per_block = (gp - gp_tc).norm(dim=1) / gp_tc.norm(dim=1)
+    assert float(per_block.max()) < 2e-2, float(per_block.max())
+    eye = torch.eye(b, device="cuda")
+    orth = (g32.transpose(1, 2) @ g32 - eye).flatten(1).norm(dim=1)
+    assert float(orth.max()) < 1e-2, float(orth.max())
