@@ -20,11 +20,13 @@
 // bit), for Q^2 (symmetric) they are rows of Q^2.
 //
 // Forward (G = I + 2(Q + Q^2 + Q^3) + Q^4, cnp.py:109-116):
-//   S0 <- Q                       (unpack)
-//   A0  = Q Q                     (= Q^2)
-//   S1 <- Q^2, S2 <- Q^2 - 2Q     (= rows of H^T, H = 2Q + Q^2)
+//   S0 <- 2Q                      (staged packed parameters; x2 is exact)
+//   A0  = (2Q)(2Q)                (= 4 Q^2)
+//   S1 <- Q^2 = A0 / 4, S0 <- Q^2 - 2Q   (= rows of H^T, H = 2Q + Q^2; in place)
 //   A1  = Q^2 H                   (= 2 Q^3 + Q^4)
-//   G   = I + 2Q + 2 A0 + A1      (Q in fp32 from the packed parameters)
+//   G   = I + (Q^2 - S0) + A0 / 2 + A1
+// Two operand slabs, so the NEXT block's packed parameters are bulk-copied
+// into the third slab's space while this block computes.
 //
 // Backward: with N1 = dG, E = N1 - N1^T (skew), F = N1 + N1^T (symmetric),
 // the packed gradient g_ij = dQ_ij - dQ_ji (cnp.py:81-86) of the closed-form
@@ -61,7 +63,12 @@ struct Cfg {
   static constexpr bool PAIR = B == 256;
   static constexpr int SLAB = 128 * B * 2;       // 128 rows x b bf16 (K-major, SW128)
   static constexpr int TILE = 32 * 33 * 4;       // per-warp 32 x 32 fp32 transpose tile
-  static constexpr int SMEM = 3 * SLAB + 8 * TILE + 1024 + 64;
+  // forward: two slabs (2Q, Q^2) + the next block's packed staging; backward:
+  // three slabs + the per-warp transpose tiles (staging over S1 / S2)
+  static constexpr int STG_BYTES = PAIR ? (128 * 132 + 8128) * 4 : 8128 * 4;  // CTA 1 of a pair is the larger
+  static constexpr int BAR_OFF = (2 * SLAB + STG_BYTES) > (3 * SLAB + 8 * TILE) ? (2 * SLAB + STG_BYTES)
+                                                                                : (3 * SLAB + 8 * TILE);
+  static constexpr int SMEM = BAR_OFF + 1024 + 64;
   static constexpr int TMEM_COLS = 2 * B;
   static constexpr uint32_t IDESC = idesc_bf16(PAIR ? 256 : 128, B, false, false);
   static constexpr int HALF = B / 2;             // columns per thread in thread-per-row phases
@@ -148,36 +155,44 @@ struct Stage {
     return own_start(hi - 1) + (B - hi) - own_start(lo);  // through the last element of row hi - 1
   }
 };
+// warp 0: bulk copies of this CTA's packed rows into `stg`, completion on `bar`
 template <int B>
-__device__ __forceinline__ void unpack_q_staged(uint8_t* slab, float* stg, const float* __restrict__ pk, int lo,
-                                                uint64_t* bar, uint32_t& bph, int warp, int lane) {
+__device__ __forceinline__ void stage_issue(float* stg, const float* __restrict__ pk, int lo, uint64_t* bar,
+                                            int lane) {
   using ST = Stage<B>;
   const int front_rows = lo;  // rows j < lo (pair CTA 1 only)
   float* own = stg + front_rows * ST::FP;
   const int os = ST::own_start(lo), oc = ST::own_count(lo);
-  if (warp == 0) {
-    if (lane == 0) {
-      uint32_t bytes = static_cast<uint32_t>(oc) * 4;
-      for (int j = 0; j < front_rows; ++j) {
-        const int g0 = rowp<B>(j) + lo, a = g0 & 3;
-        bytes += static_cast<uint32_t>((a + 128 + 3) / 4 * 16);
-      }
-      mbar_expect_tx(bar, bytes);
-    }
-    __syncwarp();
-    fence_async_smem();  // earlier generic writes to the staging area before the async copies
-    if (lane == 0) {
-      const char* src = reinterpret_cast<const char*>(pk + os);
-      for (uint32_t o = 0; o < static_cast<uint32_t>(oc) * 4; o += 32768) {
-        const uint32_t n = static_cast<uint32_t>(oc) * 4 - o < 32768 ? static_cast<uint32_t>(oc) * 4 - o : 32768;
-        bulk_load_1d(reinterpret_cast<char*>(own) + o, src + o, n, bar);
-      }
-    }
-    for (int j = lane; j < front_rows; j += 32) {
+  if (lane == 0) {
+    uint32_t bytes = static_cast<uint32_t>(oc) * 4;
+    for (int j = 0; j < front_rows; ++j) {
       const int g0 = rowp<B>(j) + lo, a = g0 & 3;
-      bulk_load_1d(stg + j * ST::FP, pk + (g0 - a), static_cast<uint32_t>((a + 128 + 3) / 4 * 16), bar);
+      bytes += static_cast<uint32_t>((a + 128 + 3) / 4 * 16);
+    }
+    mbar_expect_tx(bar, bytes);
+  }
+  __syncwarp();
+  fence_async_smem();  // earlier generic accesses of the staging area before the async copies
+  if (lane == 0) {
+    const char* src = reinterpret_cast<const char*>(pk + os);
+    for (uint32_t o = 0; o < static_cast<uint32_t>(oc) * 4; o += 32768) {
+      const uint32_t n = static_cast<uint32_t>(oc) * 4 - o < 32768 ? static_cast<uint32_t>(oc) * 4 - o : 32768;
+      bulk_load_1d(reinterpret_cast<char*>(own) + o, src + o, n, bar);
     }
   }
+  for (int j = lane; j < front_rows; j += 32) {
+    const int g0 = rowp<B>(j) + lo, a = g0 & 3;
+    bulk_load_1d(stg + j * ST::FP, pk + (g0 - a), static_cast<uint32_t>((a + 128 + 3) / 4 * 16), bar);
+  }
+}
+// every thread: wait for the staging, then scatter sc * Q into the K-major slab
+template <int B>
+__device__ __forceinline__ void stage_scatter(uint8_t* slab, const float* stg, int lo, uint64_t* bar, uint32_t& bph,
+                                              int warp, int lane, float sc) {
+  using ST = Stage<B>;
+  const int front_rows = lo;
+  const float* own = stg + front_rows * ST::FP;
+  const int os = ST::own_start(lo);
   mbar_wait(bar, bph);
   bph ^= 1;
   auto put = [&](int r, int c, float v) {
@@ -188,7 +203,7 @@ __device__ __forceinline__ void unpack_q_staged(uint8_t* slab, float* stg, const
   for (int j = lo + warp; j < hi; j += 8) {
     const float* row = own + (rowp<B>(j) - os);
     for (int c = j + 1 + lane; c < B; c += 32) {
-      const float v = row[c];
+      const float v = sc * row[c];
       put(j - lo, c, v);
       if (c < lo + 128) put(c - lo, j, -v);
     }
@@ -197,9 +212,15 @@ __device__ __forceinline__ void unpack_q_staged(uint8_t* slab, float* stg, const
   for (int j = warp; j < front_rows; j += 8) {
     const float* row = stg + j * ST::FP + ((rowp<B>(j) + lo) & 3) - lo;
 #pragma unroll 4
-    for (int c = lo + lane; c < lo + 128; c += 32) put(c - lo, j, -row[c]);
+    for (int c = lo + lane; c < lo + 128; c += 32) put(c - lo, j, -sc * row[c]);
   }
   if (threadIdx.x < 128) put(threadIdx.x, lo + threadIdx.x, 0.f);
+}
+template <int B>
+__device__ __forceinline__ void unpack_q_staged(uint8_t* slab, float* stg, const float* __restrict__ pk, int lo,
+                                                uint64_t* bar, uint32_t& bph, int warp, int lane) {
+  if (warp == 0) stage_issue<B>(stg, pk, lo, bar, lane);
+  stage_scatter<B>(slab, stg, lo, bar, bph, warp, lane, 1.f);
 }
 
 // 32 x 32 tile of N1 = dG, one row per lane: a[x] = N1[i0 + lane, j0 + x]
@@ -281,7 +302,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   float* stage = reinterpret_cast<float*>(smem);  // fp32 staging over the slabs (final phase)
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   float* tile = reinterpret_cast<float*>(smem + 3 * CF::SLAB) + warp * (32 * 33);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 3 * CF::SLAB + 8 * CF::TILE);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + CF::BAR_OFF);
   uint64_t* sbar = bar + 1;  // packed-parameter staging (bulk copies)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
 
@@ -320,18 +341,25 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t s0 = smem_u32(S0), s1 = smem_u32(S1), s2 = smem_u32(S2);
   uint32_t phase = 0, sphase = 0;
   constexpr int64_t PAIRS = static_cast<int64_t>(B) * (B - 1) / 2;
-  float* stg = reinterpret_cast<float*>(S1);  // packed staging over S1 / S2 (free at unpack time)
-  // largest staging: pair CTA 1 (front 128 x FP + own 8,128) or CTA 0 / b = 128 (own only)
-  static_assert((CF::PAIR ? 128 * Stage<B>::FP + 8128 : 8128) * 4 <= 2 * CF::SLAB && 24512 * 4 <= 2 * 128 * 256 * 2,
-                "packed staging must fit in two slabs");
+  // packed staging: backward over S1 / S2 (free at unpack time); forward
+  // behind S0 / S1, filled for the NEXT block while this one computes
+  float* stg = reinterpret_cast<float*>(FWD ? S2 : S1);
+  static_assert(CF::STG_BYTES <= 2 * CF::SLAB && 24512 * 4 <= CF::STG_BYTES + (B == 256 ? 0 : 1 << 30),
+                "packed staging must fit");
+  if constexpr (FWD) {
+    if (warp == 0 && unit < nb) stage_issue<B>(stg, packed + unit * PAIRS, lo, sbar, lane);
+  }
 
   for (int64_t s = unit; s < nb; s += units) {
     const float* pk = packed + s * PAIRS;
-    if (threadIdx.x == 0 && s + units < nb) {
-      // the next block's inputs into L2 while this one computes (each CTA of a
-      // pair fetches half): its unpack then waits on L2, not DRAM, latency
+    // the forward already stages the next block's parameters during this one:
+    // its L2 prefetch runs one block further ahead
+    const int64_t pre = FWD ? s + 2 * units : s + units;
+    if (threadIdx.x == 0 && pre < nb) {
+      // upcoming inputs into L2 while this block computes (each CTA of a pair
+      // fetches half): their staging / loads then wait on L2, not DRAM, latency
       constexpr uint32_t PB = static_cast<uint32_t>(PAIRS) * 4, HB = PB / 32 * 16;
-      const char* nx = reinterpret_cast<const char*>(packed + (s + units) * PAIRS);
+      const char* nx = reinterpret_cast<const char*>(packed + pre * PAIRS);
       if (CF::PAIR)
         prefetch_l2(nx + rank * HB, rank ? PB - HB : HB);
       else
@@ -342,42 +370,50 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     if constexpr (FWD) {
-      // ---- S0 <- Q
-      unpack_q_staged<B>(S0, stg, pk, lo, sbar, sphase, warp, lane);
+      // ---- S0 <- 2Q (the staged packed parameters, scaled exactly by 2)
+      stage_scatter<B>(S0, stg, lo, sbar, sphase, warp, lane, 2.f);
+      __syncthreads();  // the staging is consumed: the next block's copies may land
       publish<B>();
       if (issuer) {
-        mma<B>(A0, s0, s0, NEG_B, false);  // Q Q = S0 (-S0)^T
+        mma<B>(A0, s0, s0, NEG_B, false);  // 4 Q^2 = (2Q) (-(2Q))^T
         commit<B>(bar);
       }
+      if (warp == 0 && s + units < nb) stage_issue<B>(stg, packed + (s + units) * PAIRS, lo, sbar, lane);
       wait_mma(bar, phase);
-      // ---- S1 <- Q^2 ; S2 <- Q^2 - 2Q (rows of H^T, H = 2Q + Q^2)
+      // ---- S1 <- Q^2 = A0 / 4 (exact scaling) ; S0 <- Q^2 - 2Q (rows of H^T,
+      // H = 2Q + Q^2), in place over this thread's own 2Q row chunk
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
-        float q2[32], q[32];
+        float q2[32], tq[32];
         tmem_ld(A0 + tl + c, q2);
-        load32(S0, r, c, q);
-        store32(S1, r, c, q2);
+        load32(S0, r, c, tq);
 #pragma unroll
-        for (int k = 0; k < 32; ++k) q[k] = q2[k] - 2.f * q[k];
-        store32(S2, r, c, q);
+        for (int k = 0; k < 32; ++k) {
+          q2[k] *= 0.25f;
+          tq[k] = q2[k] - tq[k];
+        }
+        store32(S1, r, c, q2);
+        store32(S0, r, c, tq);
       }
       publish<B>();
       if (issuer) {
-        mma<B>(A1, s1, s2, 0, false);  // Q^2 H = 2 Q^3 + Q^4
+        mma<B>(A1, s1, s0, 0, false);  // Q^2 H = 2 Q^3 + Q^4
         commit<B>(bar);
       }
       wait_mma(bar, phase);
-      // ---- G = I + 2 (Q + Q^2) + (2 Q^3 + Q^4), staged bf16 in S1 (free now)
+      // ---- G = I + 2Q + 2Q^2 + (2 Q^3 + Q^4), staged bf16 in S1 (its rows are
+      // this thread's); 2Q = Q^2 - bf16(Q^2 - 2Q), within 2^-8 |Q| of exact
       const int64_t grow = (s * B + lo + r) * B;
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
-        float q[32], q2[32], p[32];
-        load32(S0, r, c, q);  // Q as the bf16 operand (2Q: exact in bf16)
-        tmem_ld(A0 + tl + c, q2);
+        float h[32], q2[32], p[32];
+        load32(S0, r, c, h);       // Q^2 - 2Q (bf16)
+        tmem_ld(A0 + tl + c, q2);  // 4 Q^2 (fp32)
         tmem_ld(A1 + tl + c, p);
 #pragma unroll
         for (int k = 0; k < 32; ++k) {
-          p[k] = 2.f * (q[k] + q2[k]) + p[k];
+          const float qq = 0.25f * q2[k];
+          p[k] = (qq - h[k]) + 2.f * qq + p[k];
           if (c + k == lo + r) p[k] += 1.f;
         }
         if (g16) store32(S1, r, c, p);
