@@ -294,7 +294,9 @@ int poetx_layer_backward_dg(const poetx_layer_desc* d, const poetx_layer_factors
 /* merge_and_reinit numerics (layer.py:260-314): new premerged
  * PM'[i,j] = M[inv_in(new_in(i)), inv_out(new_out(j))] with
  * M = blockdiag(G_R) PM blockdiag(G_P) computed in fp32/fp64 from the
- * given factors; optional W_out = Psi^T M Psi (materialize_weight). */
+ * given factors; optional W_out = Psi^T M Psi (materialize_weight).
+ * premerged_out (codes_out / scales_out) may be the layer's own buffers:
+ * the old weight is read only before the final re-permutation gather. */
 size_t poetx_merge_workspace_bytes(const poetx_layer_desc* d);
 /* Tensor-core merge product (kernel K9; layer.py:260-271, blockdiag.py:76-97):
  * out = blockdiag(G_R) PM blockdiag(G_P) for fp32 factors G_R [m/b, b, b],

@@ -23,11 +23,28 @@ struct GemmDesc {
 
 constexpr int kSimtBM = 64, kSimtBN = 64, kSimtBK = 16, kSimtThreads = 256;
 
+// 4 consecutive accumulators of a shared row (16-byte aligned): one vector load
+template <typename Acc>
+__device__ __forceinline__ void ld4(const Acc* p, Acc (&v)[4]) {
+  if constexpr (sizeof(Acc) == 4) {
+    const float4 x = *reinterpret_cast<const float4*>(p);
+    v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+  } else {
+    const double2 x = *reinterpret_cast<const double2*>(p), y = *reinterpret_cast<const double2*>(p + 2);
+    v[0] = x.x; v[1] = x.y; v[2] = y.x; v[3] = y.y;
+  }
+}
+
+// 64 x 64 output tile, 256 threads, each a 4 x 4 block of CONSECUTIVE rows and
+// columns, so a k step reads its 4 + 4 operands with two vector shared loads
+// (the old strided mapping needed eight scalar ones per 16 FMAs); next
+// k-tile's global loads are held in registers while the current one computes.
 template <typename TA, typename TB, typename TC>
 __global__ void __launch_bounds__(kSimtThreads) simt_gemm_kernel(GemmDesc d) {
   using Acc = typename AccOf<TC>::type;
-  __shared__ Acc As[kSimtBK][kSimtBM + 1];
-  __shared__ Acc Bs[kSimtBK][kSimtBN + 1];
+  constexpr int PAD = 16 / sizeof(Acc);  // rows stay 16-byte aligned
+  __shared__ __align__(16) Acc As[kSimtBK][kSimtBM + PAD];
+  __shared__ __align__(16) Acc Bs[kSimtBK][kSimtBN + PAD];
 
   const int64_t bz = blockIdx.z;
   const TA* A = static_cast<const TA*>(d.A) + bz * d.sAb;
@@ -36,7 +53,7 @@ __global__ void __launch_bounds__(kSimtThreads) simt_gemm_kernel(GemmDesc d) {
   const int64_t m0 = static_cast<int64_t>(blockIdx.y) * kSimtBM;
   const int64_t n0 = static_cast<int64_t>(blockIdx.x) * kSimtBN;
   const int tid = threadIdx.x;
-  const int tx = tid % 16, ty = tid / 16;
+  const int tx = tid % 16, ty = tid / 16;  // rows 4ty.., columns 4tx..
 
   Acc acc[4][4];
 #pragma unroll
@@ -44,33 +61,46 @@ __global__ void __launch_bounds__(kSimtThreads) simt_gemm_kernel(GemmDesc d) {
 #pragma unroll
     for (int j = 0; j < 4; ++j) acc[i][j] = Acc(0);
 
+  // element e of a 64 x 16 tile: consecutive threads walk the contiguous index
+  auto a_idx = [&](int e, int& am, int& ak) {
+    if (d.sAm == 1) { am = e % kSimtBM; ak = e / kSimtBM; } else { ak = e % kSimtBK; am = e / kSimtBK; }
+  };
+  auto b_idx = [&](int e, int& bk, int& bn) {
+    if (d.sBn == 1) { bn = e % kSimtBN; bk = e / kSimtBN; } else { bk = e % kSimtBK; bn = e / kSimtBK; }
+  };
+  Acc ra[4], rb[4];
+  auto fetch = [&](int64_t k0) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int e = tid + r * kSimtThreads;  // 0..1023
+      int am, ak, bk, bn;
+      a_idx(e, am, ak);
+      b_idx(e, bk, bn);
+      const int64_t gm = m0 + am, gk = k0 + ak, gn = n0 + bn, gk2 = k0 + bk;
+      ra[r] = (gm < d.M && gk < d.K) ? Conv<TA>::to_f(A[gm * d.sAm + gk * d.sAk]) : Acc(0);
+      rb[r] = (gn < d.N && gk2 < d.K) ? Conv<TB>::to_f(B[gk2 * d.sBk + gn * d.sBn]) : Acc(0);
+    }
+  };
   // k-tiles are visited in ascending order and, inside a tile, k ascends:
   // every output element accumulates over k in the same fixed order.
+  if (d.K > 0) fetch(0);
   for (int64_t k0 = 0; k0 < d.K; k0 += kSimtBK) {
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
-      int e = tid + r * kSimtThreads;  // 0..1023
-      // A tile: 64 (m) x 16 (k); consecutive threads walk m when A is
-      // m-contiguous, k otherwise (keeps loads coalesced for both layouts)
-      int am, ak;
-      if (d.sAm == 1) { am = e % kSimtBM; ak = e / kSimtBM; }
-      else { ak = e % kSimtBK; am = e / kSimtBK; }
-      int64_t gm = m0 + am, gk = k0 + ak;
-      As[ak][am] = (gm < d.M && gk < d.K) ? Conv<TA>::to_f(A[gm * d.sAm + gk * d.sAk]) : Acc(0);
-      int bk, bn;
-      if (d.sBn == 1) { bn = e % kSimtBN; bk = e / kSimtBN; }
-      else { bk = e % kSimtBK; bn = e / kSimtBK; }
-      int64_t gn = n0 + bn, gk2 = k0 + bk;
-      Bs[bk][bn] = (gn < d.N && gk2 < d.K) ? Conv<TB>::to_f(B[gk2 * d.sBk + gn * d.sBn]) : Acc(0);
+      const int e = tid + r * kSimtThreads;
+      int am, ak, bk, bn;
+      a_idx(e, am, ak);
+      b_idx(e, bk, bn);
+      As[ak][am] = ra[r];
+      Bs[bk][bn] = rb[r];
     }
     __syncthreads();
+    if (k0 + kSimtBK < d.K) fetch(k0 + kSimtBK);
 #pragma unroll
     for (int kk = 0; kk < kSimtBK; ++kk) {
       Acc a[4], b[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty + 16 * i];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx + 16 * j];
+      ld4(&As[kk][4 * ty], a);
+      ld4(&Bs[kk][4 * tx], b);
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -82,11 +112,11 @@ __global__ void __launch_bounds__(kSimtThreads) simt_gemm_kernel(GemmDesc d) {
   const Acc alpha = static_cast<Acc>(d.alpha), beta = static_cast<Acc>(d.beta);
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
-    int64_t gm = m0 + ty + 16 * i;
+    const int64_t gm = m0 + 4 * ty + i;
     if (gm >= d.M) continue;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      int64_t gn = n0 + tx + 16 * j;
+      const int64_t gn = n0 + 4 * tx + j;
       if (gn >= d.N) continue;
       TC* c = C + gm * d.sCm + gn * d.sCn;
       Acc r = acc[i][j];

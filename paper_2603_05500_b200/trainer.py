@@ -309,43 +309,48 @@ class PoetLinear(torch.nn.Module):
         z = _PoetFn.apply(x.reshape(-1, self.m).contiguous(), self)
         return z.view(*shp[:-1], self.n)
 
-    def merge_and_reinit(self, rng: Rng, audit_out: torch.Tensor | None = None):
+    def merge_and_reinit(self, rng: Rng, audit_out: torch.Tensor | None = None, factors=None, perms=None):
         """layer.py:279-314 on the device: fold G_R PM G_P (fp32 factors from the
         CUDA-core CNP for merge accuracy), resample perms, zero packed in place.
         ``audit_out`` (device float64 [2]) receives ||G^T G - I||_F of both
-        sides (layer.py:287-295), without a host sync."""
+        sides (layer.py:287-295), without a host sync.  ``factors`` (fp32 G_R,
+        G_P) and ``perms`` ((pi_in, pi_out) PermutationMaps whose device
+        copies are already cached) let the trainer batch those across layers."""
         b = self.b
-        g_r = torch.empty((self.m // b, b, b), dtype=torch.float32, device=self.device)
-        g_p = torch.empty((self.n // b, b, b), dtype=torch.float32, device=self.device)
-        # Q^2 caches supplied: the fp32 CUDA-core CNP (not the fused bf16 one)
-        q2_r, q2_p = torch.empty_like(g_r), torch.empty_like(g_p)
-        f = N.LayerFactors(self.packed_r.data_ptr(), self.packed_p.data_ptr(), g_r.data_ptr(), g_p.data_ptr(),
-                           self.g_r16.data_ptr(), self.g_p16.data_ptr(), q2_r.data_ptr(), q2_p.data_ptr())
-        ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(N.F32, max(self.m, self.n) // b, b, self.k),
-                              self.device)
-        N.call("poetx_layer_factors", self.desc, f, ws, wsb, N.stream_ptr(self.device))
+        if factors is not None:
+            g_r, g_p = factors
+        else:
+            g_r = torch.empty((self.m // b, b, b), dtype=torch.float32, device=self.device)
+            g_p = torch.empty((self.n // b, b, b), dtype=torch.float32, device=self.device)
+            # Q^2 caches supplied: the fp32 CUDA-core CNP (not the fused bf16 one)
+            q2_r, q2_p = torch.empty_like(g_r), torch.empty_like(g_p)
+            f = N.LayerFactors(self.packed_r.data_ptr(), self.packed_p.data_ptr(), g_r.data_ptr(), g_p.data_ptr(),
+                               self.g_r16.data_ptr(), self.g_p16.data_ptr(), q2_r.data_ptr(), q2_p.data_ptr())
+            ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(N.F32, max(self.m, self.n) // b, b, self.k),
+                                  self.device)
+            N.call("poetx_layer_factors", self.desc, f, ws, wsb, N.stream_ptr(self.device))
         if audit_out is not None:
             for k, g in enumerate((g_r, g_p)):
                 nb = g.shape[0]
                 ws, wsb = N.workspace(nb * b * b * 4 + 512 * 8 + 8192, self.device)
                 N.call("poetx_orthogonality_error", N.F32, nb, b, g.data_ptr(), audit_out[k:].data_ptr(), ws, wsb,
                        N.stream_ptr(self.device))
-        new_in = sample_permutation(self.m, rng)
-        new_out = sample_permutation(self.n, rng)
+        if perms is not None:
+            new_in, new_out = perms
+        else:
+            new_in = sample_permutation(self.m, rng)
+            new_out = sample_permutation(self.n, rng)
         ws, wsb = N.workspace(N.lib().poetx_merge_workspace_bytes(self.desc), self.device)
+        # the merged weight is written straight over the old one (the merge
+        # reads the old weight only before its final re-permutation gather)
         if self.quantized:
-            codes, scales = torch.empty_like(self.codes), torch.empty_like(self.scales)
             N.call("poetx_layer_merge_quant", self.desc, g_r.data_ptr(), g_p.data_ptr(),
                    new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
-                   codes.data_ptr(), scales.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
-            self.codes.copy_(codes)
-            self.scales.copy_(scales)
+                   self.codes.data_ptr(), self.scales.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
         else:
-            pm_new = torch.empty_like(self.premerged)
             N.call("poetx_layer_merge", self.desc, g_r.data_ptr(), g_p.data_ptr(),
                    new_in.device(self.device)[0].data_ptr(), new_out.device(self.device)[0].data_ptr(),
-                   pm_new.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
-            self.premerged.copy_(pm_new)
+                   self.premerged.data_ptr(), None, ws, wsb, N.stream_ptr(self.device))
         self.perm_in, self.perm_out = new_in, new_out
         for dst, src in zip(self.pin_dev + self.pout_dev, new_in.device(self.device) + new_out.device(self.device)):
             dst.copy_(src)
@@ -1305,10 +1310,40 @@ class Trainer:
         RNGs, fresh AdamW moments for the POET group, and a merge audit per
         layer (orthogonality errors of the folded factors, read back once)."""
         self.check_numerics()  # never fold a non-finite step into the frozen weights
-        layers = self.model.poet_layers()
+        model = self.model
+        layers = model.poet_layers()
         audit = torch.zeros((len(layers), 2), dtype=torch.float64, device=self.device)
-        for i, (lay, rng) in enumerate(zip(layers, merge_rngs(self.seed, self.step_idx, len(layers)))):
-            lay.merge_and_reinit(rng, audit_out=audit[i])
+        rngs = merge_rngs(self.seed, self.step_idx, len(layers))
+        # every layer's new permutations (keyed streams: the order across layers
+        # does not change them), uploaded in ONE pinned copy and cached on the maps
+        perms = [(sample_permutation(lay.m, r), sample_permutation(lay.n, r)) for lay, r in zip(layers, rngs)]
+        flat = np.concatenate([a for pi, po in perms for a in (pi.forward, pi.inverse, po.forward, po.inverse)])
+        dev_flat = torch.from_numpy(flat).pin_memory().to(self.device, non_blocking=True)
+        o = 0
+        for pi, po in perms:
+            for pm in (pi, po):
+                fwd, inv = dev_flat[o:o + pm.n], dev_flat[o + pm.n:o + 2 * pm.n]
+                pm._dev[(self.device.type, self.device.index)] = (fwd, inv)
+                o += 2 * pm.n
+        # fp32 CUDA-core CNP (merge accuracy) once per decoder block: its seven
+        # layers' blocks are contiguous in the flat parameter buffer
+        b, pairs, k = model.stack.b, model.stack.pairs, model.cfg.neumann_k
+        nb_max = max(nb for _, nb in model.block_ranges)
+        g32 = torch.empty((nb_max, b, b), dtype=torch.float32, device=self.device)
+        q2 = torch.empty_like(g32)
+        ws, wsb = N.workspace(N.lib().poetx_cnp_workspace_bytes(N.F32, nb_max, b, k), self.device)
+        li = 0
+        for i, mods in enumerate(model.layers):
+            off, nb = model.block_ranges[i]
+            N.call("poetx_cnp_forward", N.F32, nb, b, k, None, model.poet.param[off * pairs:].data_ptr(),
+                   g32.data_ptr(), None, q2.data_ptr(), ws, wsb, N.stream_ptr(self.device))
+            for p in model.PROJ:
+                lay = mods[p]
+                r0 = model.stack.block_off[lay.name + ".r"] - off
+                p0 = model.stack.block_off[lay.name + ".p"] - off
+                g_r, g_p = g32[r0:r0 + lay.m // b], g32[p0:p0 + lay.n // b]
+                lay.merge_and_reinit(rngs[li], audit_out=audit[li], factors=(g_r, g_p), perms=perms[li])
+                li += 1
         self.model.refresh_maps()
         self.model.poet.reset_moments()
         self.since_merge = 0
