@@ -574,15 +574,18 @@ class _Embedding(torch.autograd.Function):
         out = torch.empty((T, d), dtype=torch.bfloat16, device=table.device)
         N.call("poetx_embedding_fwd", T, V, d, tok.data_ptr(), table.data_ptr(), out.data_ptr(),
                N.stream_ptr(table.device))
-        ctx.save_for_backward(tok)
+        # the backward's token sort depends on the tokens only: done here, at the
+        # step start, where it overlaps the first decoder block's CNP instead of
+        # sitting between the last backward kernel and the optimizer
+        srt, order = torch.sort(tok, stable=True)
+        ctx.save_for_backward(tok, srt, order)
         ctx.grad_view = grad_view
         return out
 
     @staticmethod
     def backward(ctx, dh):
-        (tok,) = ctx.saved_tensors
+        tok, srt, order = ctx.saved_tensors
         dh = dh.contiguous()
-        srt, order = torch.sort(tok, stable=True)
         N.call("poetx_embedding_bwd", tok.numel(), ctx.grad_view.shape[0], dh.shape[1], srt.data_ptr(),
                order.data_ptr(), dh.data_ptr(), ctx.grad_view.data_ptr(), N.stream_ptr(dh.device))
         return None, None, None
