@@ -900,7 +900,14 @@ static int pair_ms(const TcProblem& p, int nblk, bool q8 = false) {
   if (nblk != 1 || p.M < 512) return 1;
   (void)q8;  // int8 B: 512-row tiles too (half the conversions per FLOP; tools/q8bench.py)
   if (g_pair_ms == 1 || g_pair_ms == 2) return g_pair_ms;
-  return 2;
+  // whole tile rounds on the SM pairs, a 512-row tile costing two 256-row
+  // ones less the ~5% its halved L2 -> SM traffic buys: e.g. 8192 x 2816
+  // (352 vs 176 tiles on 74 pairs: 5 rounds vs 3 x 1.9) keeps 256 rows,
+  // 8192 x 5632 (10 vs 5 x 1.9) and 8192 x 2048 (4 vs 2 x 1.9) take 512
+  const int64_t pairs = tc::num_sms() / 2, nt = p.N / 256;
+  const int64_t r1 = ((p.M + 255) / 256 * nt + pairs - 1) / pairs;
+  const int64_t r2 = ((p.M + 511) / 512 * nt + pairs - 1) / pairs;
+  return 1.9 * r2 < r1 ? 2 : 1;
 }
 
 namespace tc {
