@@ -409,6 +409,12 @@ int poetx_swiglu_gather(int64_t T, int64_t f, const void* vg, const void* vu, co
 int poetx_swiglu_gather_bwd(int64_t T, int64_t f, const void* vg, const void* vu, const void* du,
                             const int32_t* A, const int32_t* B, const int32_t* C, const int32_t* D,
                             void* dvg, void* dvu, void* stream);
+/* the same with 16-bit maps (f <= 65536): half the index bytes through L1 */
+int poetx_swiglu_gather16(int64_t T, int64_t f, const void* vg, const void* vu, const uint16_t* cg,
+                          const uint16_t* cu, void* out, void* stream);
+int poetx_swiglu_gather_bwd16(int64_t T, int64_t f, const void* vg, const void* vu, const void* du,
+                              const uint16_t* A, const uint16_t* B, const uint16_t* C, const uint16_t* D,
+                              void* dvg, void* dvu, void* stream);
 /* out = RoPE(v[:, inv]) per head (pairs c, c + hd/2; position t % S) */
 int poetx_rope_scatter(int64_t T, int64_t S, int64_t H, int64_t hd, const void* v,
                        const int32_t* inv, const float* cosb, const float* sinb, void* out,

@@ -115,6 +115,8 @@ _SIGS = {
     "poetx_rmsnorm_gather_bwd": (I32, [I64, I64, VP, VP, VP, I32, VP, VP, VP, VP, VP, I32, VP, SZ, VP]),
     "poetx_swiglu_gather": (I32, [I64, I64, VP, VP, VP, VP, VP, VP]),
     "poetx_swiglu_gather_bwd": (I32, [I64, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP]),
+    "poetx_swiglu_gather16": (I32, [I64, I64, VP, VP, VP, VP, VP, VP]),
+    "poetx_swiglu_gather_bwd16": (I32, [I64, I64, VP, VP, VP, VP, VP, VP, VP, VP, VP, VP]),
     "poetx_rope_scatter": (I32, [I64, I64, I64, I64, VP, VP, VP, VP, VP, VP]),
     "poetx_rope_scatter_bwd": (I32, [I64, I64, I64, I64, VP, VP, VP, VP, VP, VP]),
     "poetx_scatter_add": (I32, [I64, I64, VP, VP, VP, VP, VP]),

@@ -63,6 +63,17 @@ __device__ __forceinline__ void load_idx8(const int32_t* idx, int j0, int (&o)[8
   const int4 b = __ldg(reinterpret_cast<const int4*>(idx + j0 + 4));
   o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w; o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
 }
+// 16-bit index maps (features < 65536): half the index bytes through L1,
+// which is what the SwiGLU kernels' L1/shared pipe saturates on
+__device__ __forceinline__ void load_idx8(const uint16_t* idx, int j0, int (&o)[8]) {
+  const uint4 a = __ldg(reinterpret_cast<const uint4*>(idx + j0));
+  const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    o[2 * q] = static_cast<int>(w[q] & 0xFFFFu);
+    o[2 * q + 1] = static_cast<int>(w[q] >> 16);
+  }
+}
 __device__ __forceinline__ void load_f8(const float* p, float (&o)[8]) {
   const float4 a = __ldg(reinterpret_cast<const float4*>(p));
   const float4 b = __ldg(reinterpret_cast<const float4*>(p) + 1);
@@ -464,10 +475,10 @@ __global__ void __launch_bounds__(256) colsum_split_kernel(int64_t rows, int64_t
 // reduction spreads over (d / 32) x kColsumSplits CTAs
 int colsum2(int64_t rows, int64_t d, const float* part, float* mid, float* out, int accumulate, cudaStream_t st);
 
-template <int RT>
+template <int RT, typename IdxT = int32_t>
 __global__ void __launch_bounds__(kThreads) swiglu_gather_kernel(
     int64_t T, int f, const __nv_bfloat16* __restrict__ vg, const __nv_bfloat16* __restrict__ vu,
-    const int32_t* __restrict__ cg, const int32_t* __restrict__ cu, __nv_bfloat16* __restrict__ out) {
+    const IdxT* __restrict__ cg, const IdxT* __restrict__ cu, __nv_bfloat16* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* gs = reinterpret_cast<__nv_bfloat16*>(sm);
   __nv_bfloat16* us = gs + RT * f;
@@ -503,11 +514,11 @@ __global__ void __launch_bounds__(kThreads) swiglu_gather_kernel(
 // dv_u is first formed in gate order (du[A[k]] silu(v_g[k]), no extra gather)
 // over the thread's own v_g vector in place, then gathered through D: three
 // gathers per element instead of four.
-template <int RT>
+template <int RT, typename IdxT>
 __device__ __forceinline__ void swiglu_bwd_tile(int64_t r0, int nr, int f, __nv_bfloat16* gs,
                                                 const __nv_bfloat16* us, const __nv_bfloat16* ds,
-                                                const int32_t* __restrict__ A, const int32_t* __restrict__ B,
-                                                const int32_t* __restrict__ D, __nv_bfloat16* __restrict__ dvg,
+                                                const IdxT* __restrict__ A, const IdxT* __restrict__ B,
+                                                const IdxT* __restrict__ D, __nv_bfloat16* __restrict__ dvg,
                                                 __nv_bfloat16* __restrict__ dvu) {
   const int nvec = f / 8;
   for (int i = threadIdx.x; i < nvec; i += kThreads) {
@@ -544,11 +555,11 @@ __device__ __forceinline__ void swiglu_bwd_tile(int64_t r0, int nr, int f, __nv_
   }
 }
 
-template <int RT>
+template <int RT, typename IdxT = int32_t>
 __global__ void __launch_bounds__(kThreads) swiglu_gather_bwd_kernel(
     int64_t T, int f, const __nv_bfloat16* __restrict__ vg, const __nv_bfloat16* __restrict__ vu,
-    const __nv_bfloat16* __restrict__ du, const int32_t* __restrict__ A,
-    const int32_t* __restrict__ B, const int32_t* __restrict__ Cc, const int32_t* __restrict__ D,
+    const __nv_bfloat16* __restrict__ du, const IdxT* __restrict__ A,
+    const IdxT* __restrict__ B, const IdxT* __restrict__ Cc, const IdxT* __restrict__ D,
     __nv_bfloat16* __restrict__ dvg, __nv_bfloat16* __restrict__ dvu) {
   extern __shared__ __align__(16) unsigned char sm[];
   __nv_bfloat16* gs = reinterpret_cast<__nv_bfloat16*>(sm);
@@ -562,7 +573,7 @@ __global__ void __launch_bounds__(kThreads) swiglu_gather_bwd_kernel(
     stage_rows(ds, du + r0 * f, nr, f);
     cp_wait_all();
     __syncthreads();
-    swiglu_bwd_tile<RT>(r0, nr, f, gs, us, ds, A, B, D, dvg, dvu);
+    swiglu_bwd_tile<RT, IdxT>(r0, nr, f, gs, us, ds, A, B, D, dvg, dvu);
     __syncthreads();
   }
 }
@@ -1054,6 +1065,56 @@ int poetx_swiglu_gather_bwd(int64_t T, int64_t f, const void* vg, const void* vu
                         static_cast<const __nv_bfloat16*>(du), A, B, Cc, D,
                         static_cast<__nv_bfloat16*>(dvg), static_cast<__nv_bfloat16*>(dvu)));
   POETX_LAUNCHED("swiglu_gather_bwd");
+  return POETX_OK;
+}
+
+int poetx_swiglu_gather16(int64_t T, int64_t f, const void* vg, const void* vu, const uint16_t* cg,
+                          const uint16_t* cu, void* out, void* stream) {
+  POETX_REQUIRE(f <= 65536, POETX_ESHAPE, "swiglu_gather16: f = %lld needs 32-bit maps", (long long)f);
+  const int rt = pick_rt(2 * f * 2);
+  const size_t smem = rt * 2 * f * 2;
+  POETX_TRY(check_rows(T, f, smem));
+  if (T == 0) return POETX_OK;
+  switch (rt) {
+#define POETX_SW16(R)                                                                                          \
+  case R: {                                                                                                    \
+    auto k = swiglu_gather_kernel<R, uint16_t>;                                                                \
+    set_smem(k, smem);                                                                                         \
+    k<<<row_grid(T, rt), kThreads, smem, as_stream(stream)>>>(T, f, static_cast<const __nv_bfloat16*>(vg),    \
+                                                             static_cast<const __nv_bfloat16*>(vu), cg, cu,    \
+                                                             static_cast<__nv_bfloat16*>(out));                \
+    break;                                                                                                     \
+  }
+    POETX_SW16(8) POETX_SW16(4) POETX_SW16(2) default: POETX_SW16(1)
+#undef POETX_SW16
+  }
+  POETX_LAUNCHED("swiglu_gather16");
+  return POETX_OK;
+}
+
+int poetx_swiglu_gather_bwd16(int64_t T, int64_t f, const void* vg, const void* vu, const void* du,
+                              const uint16_t* A, const uint16_t* B, const uint16_t* Cc, const uint16_t* D,
+                              void* dvg, void* dvu, void* stream) {
+  POETX_REQUIRE(f <= 65536, POETX_ESHAPE, "swiglu_gather_bwd16: f = %lld needs 32-bit maps", (long long)f);
+  const int rt = pick_rt(3 * f * 2);
+  const size_t smem = rt * 3 * f * 2;
+  POETX_TRY(check_rows(T, f, smem));
+  if (T == 0) return POETX_OK;
+  switch (rt) {
+#define POETX_SWB16(R)                                                                                         \
+  case R: {                                                                                                    \
+    auto k = swiglu_gather_bwd_kernel<R, uint16_t>;                                                            \
+    set_smem(k, smem);                                                                                         \
+    k<<<row_grid(T, rt), kThreads, smem, as_stream(stream)>>>(                                                \
+        T, f, static_cast<const __nv_bfloat16*>(vg), static_cast<const __nv_bfloat16*>(vu),                   \
+        static_cast<const __nv_bfloat16*>(du), A, B, Cc, D, static_cast<__nv_bfloat16*>(dvg),                 \
+        static_cast<__nv_bfloat16*>(dvu));                                                                    \
+    break;                                                                                                     \
+  }
+    POETX_SWB16(8) POETX_SWB16(4) POETX_SWB16(2) default: POETX_SWB16(1)
+#undef POETX_SWB16
+  }
+  POETX_LAUNCHED("swiglu_gather_bwd16");
   return POETX_OK;
 }
 

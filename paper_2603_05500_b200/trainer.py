@@ -415,12 +415,20 @@ def _rmsnorm_regather(h, w, idx):
     return out
 
 
-def _swiglu_regather(vg, vu, maps):
+def _swiglu_fwd(vg, vu, maps, out):
+    """out = silu(vg[:, cg]) * vu[:, cu], 16-bit maps when the model has them."""
     T, f = vg.shape
-    out = torch.empty_like(vg)
-    N.call("poetx_swiglu_gather", T, f, vg.data_ptr(), vu.data_ptr(), maps["cg"].data_ptr(),
-           maps["cu"].data_ptr(), out.data_ptr(), N.stream_ptr(vg.device))
+    if "cg16" in maps and os.environ.get("POETX_MAPS16", "1") != "0":
+        N.call("poetx_swiglu_gather16", T, f, vg.data_ptr(), vu.data_ptr(), maps["cg16"].data_ptr(),
+               maps["cu16"].data_ptr(), out.data_ptr(), N.stream_ptr(vg.device))
+    else:
+        N.call("poetx_swiglu_gather", T, f, vg.data_ptr(), vu.data_ptr(), maps["cg"].data_ptr(),
+               maps["cu"].data_ptr(), out.data_ptr(), N.stream_ptr(vg.device))
     return out
+
+
+def _swiglu_regather(vg, vu, maps):
+    return _swiglu_fwd(vg, vu, maps, torch.empty_like(vg))
 
 
 class _CnpBackwardHook(torch.autograd.Function):
@@ -520,10 +528,7 @@ class _SwiGLUGather(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, vg, vu, maps):
-        T, f = vg.shape
-        out = torch.empty_like(vg)
-        N.call("poetx_swiglu_gather", T, f, vg.data_ptr(), vu.data_ptr(), maps["cg"].data_ptr(),
-               maps["cu"].data_ptr(), out.data_ptr(), N.stream_ptr(vg.device))
+        out = _swiglu_fwd(vg, vu, maps, torch.empty_like(vg))
         ctx.maps = maps
         ctx.save_for_backward(vg, vu)
         return out
@@ -534,8 +539,9 @@ class _SwiGLUGather(torch.autograd.Function):
         T, f = vg.shape
         m = ctx.maps
         dvg, dvu = torch.empty_like(vg), torch.empty_like(vu)
-        N.call("poetx_swiglu_gather_bwd", T, f, vg.data_ptr(), vu.data_ptr(), du.contiguous().data_ptr(),
-               m["A"].data_ptr(), m["B"].data_ptr(), m["C"].data_ptr(), m["D"].data_ptr(),
+        w = "16" if "A16" in m and os.environ.get("POETX_MAPS16", "1") != "0" else ""
+        N.call("poetx_swiglu_gather_bwd" + w, T, f, vg.data_ptr(), vu.data_ptr(), du.contiguous().data_ptr(),
+               m["A" + w].data_ptr(), m["B" + w].data_ptr(), m["C" + w].data_ptr(), m["D" + w].data_ptr(),
                dvg.data_ptr(), dvu.data_ptr(), N.stream_ptr(vg.device))
         return dvg, dvu, None
 
@@ -838,6 +844,8 @@ class PoetLlama(torch.nn.Module):
             fu, iu = mods["up"].perm_out.forward, mods["up"].perm_out.inverse
             fd, idn = mods["down"].perm_in.forward, mods["down"].perm_in.inverse
             maps = {"cg": ig[fd], "cu": iu[fd], "A": idn[fg], "B": iu[fg], "C": idn[fu], "D": ig[fu]}
+            if len(fd) <= 65536:  # 16-bit maps: half the index bytes through the kernels' L1
+                maps.update({k + "16": v.astype(np.uint16) for k, v in list(maps.items())})
             dev = mods["gate"].device
             self.swiglu_maps.append({k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in maps.items()})
         if getattr(self, "_maps_dev", None) is None:

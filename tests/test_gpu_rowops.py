@@ -175,3 +175,28 @@ def test_embedding_fwd_bwd(N, T, V, d):
     gbuf.copy_(base)
     _Embedding.apply(tok, t, gbuf).backward(dh)
     assert torch.equal(gbuf, first)  # deterministic: bitwise the same result again
+
+
+@pytest.mark.parametrize("T,d,f", SHAPES)
+def test_swiglu_16bit_maps_bitwise_equal_to_32bit(N, T, d, f):
+    """The 16-bit-map SwiGLU kernels (half the index bytes) produce exactly
+    the 32-bit-map results, forward and backward."""
+    from paper_2603_05500_b200.trainer import _SwiGLUGather
+
+    g = torch.Generator().manual_seed(f + T + 1)
+    fg, fu, fd = _perm(f, g).long(), _perm(f, g).long(), _perm(f, g).long()
+    ig, iu, idn = torch.argsort(fg), torch.argsort(fu), torch.argsort(fd)
+    m32 = {"cg": ig[fd], "cu": iu[fd], "A": idn[fg], "B": iu[fg], "C": idn[fu], "D": ig[fu]}
+    m32 = {k: v.int().contiguous() for k, v in m32.items()}
+    m16 = dict(m32, **{k + "16": torch.from_numpy(v.cpu().numpy().astype("uint16")).cuda() for k, v in m32.items()})
+    vg = _bf(torch.randn(T, f)).cuda()
+    vu = _bf(torch.randn(T, f)).cuda()
+    du = _bf(torch.randn(T, f)).cuda()
+    res = []
+    for maps in (m32, m16):
+        a, b = vg.clone().requires_grad_(True), vu.clone().requires_grad_(True)
+        out = _SwiGLUGather.apply(a, b, maps)
+        out.backward(du)
+        res.append((out, a.grad, b.grad))
+    for x, y in zip(*res):
+        assert torch.equal(x, y)
