@@ -807,6 +807,7 @@ class PoetLlama(torch.nn.Module):
             hi = self.stack.block_off[f"{i}.down.p"] + d // b
             self.block_ranges.append((lo, hi - lo))
         self.cnp_pipelined = False  # set per step by the trainer
+        self.cnp_bwd_whole = False
         # bf16 weight folds of one decoder block (forward bd(G_R) PM, backward
         # PM bd(G_P)), double-buffered by block parity and built on the CNP
         # stream one block ahead of their use
@@ -920,9 +921,16 @@ class PoetLlama(torch.nn.Module):
         main = torch.cuda.current_stream() if pipe else None
         folds = pipe and self.folds_supported()
         self._use_folds(folds)
+        whole_fwd = pipe and os.environ.get("POETX_CNP_FWD_WHOLE", "0") == "1"
+        # whole-stack CNP backward after the decoder backward instead of one
+        # launch per block from the block-input hooks (A/B: POETX_CNP_BWD_WHOLE)
+        self.cnp_bwd_whole = pipe and os.environ.get("POETX_CNP_BWD_WHOLE", "0") == "1"
         if pipe:
             self.cnp_stream.wait_stream(main)  # fork (also joins it into a graph capture)
-            self.stack.forward_factors_range(*self.block_ranges[0])
+            if whole_fwd:  # every block's G in one launch (full waves, no per-block tail)
+                self.stack.forward_factors_range(0, self.stack.nb)
+            else:
+                self.stack.forward_factors_range(*self.block_ranges[0])
             if folds:
                 self.launch_in_folds(0)
         for i, mods in enumerate(self.layers):
@@ -934,10 +942,12 @@ class PoetLlama(torch.nn.Module):
                 if i + 1 < len(self.layers):                # block i+1's G overlaps block i
                     self.cnp_stream.wait_stream(main)
                     with torch.cuda.stream(self.cnp_stream):
-                        self.stack.forward_factors_range(*self.block_ranges[i + 1])
+                        if not whole_fwd:
+                            self.stack.forward_factors_range(*self.block_ranges[i + 1])
                         if folds:
                             self.launch_in_folds(i + 1)
-                h = _CnpBackwardHook.apply(h, self, i)
+                if not self.cnp_bwd_whole:
+                    h = _CnpBackwardHook.apply(h, self, i)
             if self.fused:
                 h = self._block_fused(i, mods, h, n1, n2, B, S)
                 if folds:
@@ -1168,6 +1178,13 @@ class Trainer:
             model.dp_group, model.dp_works = self.pg, []
             loss = model(tokens, targets)
             model.backward_dense_grads(loss)
+            if model.cnp_bwd_whole:
+                cs = model.cnp_stream
+                cs.wait_stream(torch.cuda.current_stream())
+                with torch.cuda.stream(cs):
+                    model.stack.backward_factors()
+                    if model.dp_group is not None:
+                        model.dp_works.append(_all_reduce_async(model.poet.grad, model.dp_group))
             torch.cuda.current_stream().wait_stream(model.cnp_stream)
             if getattr(model, "head_side_used", False):
                 torch.cuda.current_stream().wait_stream(model.head_stream)
