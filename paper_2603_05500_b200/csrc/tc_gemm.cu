@@ -401,6 +401,24 @@ __device__ __forceinline__ bool q8_cta_arrive() {
 #define POETX_Q8_EXTRA_WARPS 8  /* 9 converter warps: the conversion keeps up with the MMAs (tools/q8bench.py) */
 #endif
 constexpr int Q8_THREADS = THREADS + 32 * POETX_Q8_EXTRA_WARPS, Q8_CONV_WARPS = 1 + POETX_Q8_EXTRA_WARPS;
+// build-time timeline probe (-DPOETX_GEMM_TRACE, tools/gemmtrace.py): globaltimer
+// stamps per CTA -- entry, setup done, end, and per tile: first / last MMA
+// stage, epilogue start / end, first TMA issue
+#ifdef POETX_GEMM_TRACE
+__device__ unsigned long long g_gtrace[512 * 64];
+__device__ __forceinline__ void gtr(int slot) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  if (slot < 64) g_gtrace[blockIdx.x * 64 + slot] = t;
+}
+#define GTR(slot) gtr(slot)
+#else
+#define GTR(slot) ((void)(slot))
+#endif
+// timeline probe knob (-DPOETX_EPI_PROBE=1: no TMA stores); results invalid
+#ifndef POETX_EPI_PROBE
+#define POETX_EPI_PROBE 0
+#endif
 template <int MS, bool A_MN, bool B_MN, bool Q8 = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : THREADS, 1)
     tc2_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
@@ -442,6 +460,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
   };
 
   if (threadIdx.x == 0) {
+    GTR(0);
     for (int st = 0; st < STAGES; ++st) {
       mbar_init(&full[st], Q8 ? 3 : 1);  // Q8: + one elected converter thread in each CTA
       mbar_init(&empty[st], 1);
@@ -467,6 +486,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
   cluster_sync();
   fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  if (threadIdx.x == 0) GTR(1);
 
   if (Q8 && warp == 3) {
     // codes + row scales of every K block of this CTA's B half, RSTG blocks ahead
@@ -563,8 +583,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
         decode(tile, g, sp, m0, n0, kb0, kbn);
         const int bn = n0 + rank * HALF;  // this CTA's half of B
         const int ag0 = args.a_g0 * g, ag1 = args.a_g1 * g, bg0 = args.b_g0 * g, bg1 = args.b_g1 * g;
+        const int tj = (tile - cluster) / nclusters;
         for (int kb = kb0; kb < kb0 + kbn; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
+          if (kb == kb0) GTR(4 + tj * 5 + 4);
           uint8_t* sa = smem + stage * STAGE;
           uint8_t* sb = sa + MS * A_B;
           const uint32_t fb = smem_u32(&full[stage]) & PEER_MASK;
@@ -615,13 +637,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
           wait_cluster(&tempty[acc], acc_phase ^ 1);
           fence_after();
           const uint32_t tmem_d = tmem_base + acc * 256;
+          const int tj = (tile - cluster) / nclusters;
           for (int kb = 0; kb < kbn; ++kb) {
             mbar_wait(&full[stage], phase);
             fence_after();
             if (lane == 0) {
+              if (kb == 0) GTR(4 + tj * 5 + 0);
               mma_stage(stage, 0, tmem_d, kb != 0);
               commit2(&empty[stage]);
-              if (kb == kbn - 1) commit2(&tfull[acc]);
+              if (kb == kbn - 1) { commit2(&tfull[acc]); GTR(4 + tj * 5 + 1); }
             }
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -636,6 +660,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
           int g, sp, m0, n0, kb0, kbn;
           decode(tile, g, sp, m0, n0, kb0, kbn);
           const int lead = kbn < STAGES ? kbn : STAGES;
+          const int tj = (tile - cluster) / nclusters;
           // sub-tile 0 starts on the first `lead` stages as soon as its
           // accumulator is drained; sub-tile 1 follows on the same (held)
           // stages once the epilogue has drained its accumulator too
@@ -646,6 +671,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
           for (int kb = 0; kb < lead; ++kb) {
             mbar_wait(&full[stage], phase);
             fence_after();
+            if (kb == 0 && lane == 0) GTR(4 + tj * 5 + 0);
             if (lane == 0) mma_stage(stage, 0, tmem_base, kb != 0);
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -670,7 +696,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
               mma_stage(stage, 0, tmem_base, true);
               mma_stage(stage, 1, tmem_base + 256, true);
               commit2(&empty[stage]);
-              if (kb == kbn - 1) commit2(&tfull[0]);
+              if (kb == kbn - 1) { commit2(&tfull[0]); GTR(4 + tj * 5 + 1); }
             }
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -693,6 +719,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
       const int tf = MS == 1 ? acc : 0;
       mbar_wait(&tfull[tf], acc_phase);
       fence_after();
+      const int tj = (tile - cluster) / nclusters;
+      if (ew == 0 && lane == 0) GTR(4 + tj * 5 + 2);
 #pragma unroll 1
       for (int h = 0; h < MS; ++h) {
         const int row0 = m0 + h * 256 + rank * HALF + ew * 32;  // this warp's 32 rows (within the group)
@@ -729,7 +757,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
           }
           fence_async_smem();
           __syncwarp();
-          if (lane == 0 && row0 < args.M && n0 + c < args.N) {
+          if (POETX_EPI_PROBE != 1 && lane == 0 && row0 < args.M && n0 + c < args.N) {
             if (args.accumulate)
               tma_reduce_add_2d(&map_c, stg + buf * (32 * 128), n0 + c, static_cast<int>(crow));
             else
@@ -741,7 +769,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
         fence_before();
         __syncwarp();
         if (lane == 0) arrive_leader(&tempty[MS == 1 ? acc : h]);
+        if (tj == 0 && ew == 0 && lane == 0) GTR(60 + h);
       }
+      if (ew == 0 && lane == 0) GTR(4 + tj * 5 + 3);
       if (MS == 1) {
         if (++acc == 2) { acc = 0; acc_phase ^= 1; }
       } else {
@@ -754,6 +784,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
   fence_before();
   cluster_sync();
   fence_after();
+  if (threadIdx.x == 0) GTR(2);
   if (warp == 2) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512) : "memory");
   }
@@ -1117,3 +1148,15 @@ extern "C" int poetx_gemm_pair_enabled(void) { return poetx::g_pair_on; }
 extern "C" void poetx_set_gemm_pair_enabled(int on) { poetx::g_pair_on = on ? 1 : 0; }
 extern "C" void poetx_set_gemm_pair_ms(int ms) { poetx::g_pair_ms = ms; }
 extern "C" void poetx_set_tc_enabled(int on) { poetx::g_tc_on = on ? 1 : 0; }
+
+#ifdef POETX_GEMM_TRACE
+extern "C" int poetx_gemm_trace_copy(unsigned long long* host, int n) {
+  if (n > 512 * 64) n = 512 * 64;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, poetx::tc::pair::g_gtrace, n * sizeof(unsigned long long)));
+}
+extern "C" int poetx_gemm_trace_reset() {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, poetx::tc::pair::g_gtrace) != cudaSuccess) return 1;
+  return static_cast<int>(cudaMemset(p, 0, sizeof(poetx::tc::pair::g_gtrace)));
+}
+#endif
