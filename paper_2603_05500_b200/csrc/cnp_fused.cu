@@ -286,6 +286,21 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
   fence_after();
 }
 
+// build-time phase probe (-DPOETX_CNP_TRACE, tools/cnptrace.py): globaltimer
+// stamps of thread 0 per phase for the first 5 blocks of every CTA
+#ifdef POETX_CNP_TRACE
+__device__ unsigned long long g_ctrace[512 * 64];
+__device__ __forceinline__ void ctr(int it, int ph) {
+  if (threadIdx.x != 0 || it >= 5) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_ctrace[blockIdx.x * 64 + it * 12 + ph] = t;
+}
+#define CTR(ph) ctr(it, ph)
+#else
+#define CTR(ph) ((void)(ph))
+#endif
+
 template <int B, bool FWD>
 __global__ void __launch_bounds__(THREADS, 1)
     cnp_fused_kernel(int64_t nb, const float* __restrict__ packed, const float* __restrict__ dg,
@@ -350,7 +365,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp == 0 && unit < nb) stage_issue<B>(stg, packed + unit * PAIRS, lo, sbar, lane);
   }
 
+  int it = -1;
   for (int64_t s = unit; s < nb; s += units) {
+    ++it;
+    (void)it;
+    CTR(0);
     const float* pk = packed + s * PAIRS;
     // the forward already stages the next block's parameters during this one:
     // its L2 prefetch runs one block further ahead
@@ -373,6 +392,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // ---- S0 <- 2Q (the staged packed parameters, scaled exactly by 2)
       stage_scatter<B>(S0, stg, lo, sbar, sphase, warp, lane, 2.f);
       __syncthreads();  // the staging is consumed: the next block's copies may land
+      CTR(1);
       publish<B>();
       if (issuer) {
         mma<B>(A0, s0, s0, NEG_B, false);  // 4 Q^2 = (2Q) (-(2Q))^T
@@ -380,6 +400,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       if (warp == 0 && s + units < nb) stage_issue<B>(stg, packed + (s + units) * PAIRS, lo, sbar, lane);
       wait_mma(bar, phase);
+      CTR(2);
       // ---- S1 <- Q^2 = A0 / 4 (exact scaling) ; S0 <- Q^2 - 2Q (rows of H^T,
       // H = 2Q + Q^2), in place over this thread's own 2Q row chunk
 #pragma unroll 1
@@ -395,12 +416,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         store32(S1, r, c, q2);
         store32(S0, r, c, tq);
       }
+      CTR(3);
       publish<B>();
       if (issuer) {
         mma<B>(A1, s1, s0, 0, false);  // Q^2 H = 2 Q^3 + Q^4
         commit<B>(bar);
       }
       wait_mma(bar, phase);
+      CTR(4);
       // ---- G = I + 2Q + 2Q^2 + (2 Q^3 + Q^4), staged bf16 in S1 (its rows are
       // this thread's); 2Q = Q^2 - bf16(Q^2 - 2Q), within 2^-8 |Q| of exact
       const int64_t grow = (s * B + lo + r) * B;
@@ -424,6 +447,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 make_float4(p[4 * q4], p[4 * q4 + 1], p[4 * q4 + 2], p[4 * q4 + 3]);
         }
       }
+      CTR(5);
       if (g16) {
         __syncthreads();
         // one 16-byte unit per lane: each warp instruction writes a coalesced row
@@ -437,12 +461,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       // the next block's unpack overwrites S0 / S1 only after this CTA's
       // threads passed the publish barrier, i.e. after these reads
       __syncthreads();
+      CTR(6);
     } else {
       const float* n1 = dg + s * static_cast<int64_t>(B) * B;
       // ---- S0 <- Q ; S1 <- E = N1 - N1^T ; S2 <- F = N1 + N1^T ; A1 <- E (fp32)
       // (warp w owns TMEM lanes [32 (w & 3), +32): its tiles are that row group)
       unpack_q_staged<B>(S0, stg, pk, lo, sbar, sphase, warp, lane);
       __syncthreads();  // the staging (S1 / S2) is read before E / F overwrite it
+      CTR(1);
       for (int k = 0; k < B / 64; ++k) {
         const int i0 = lo + (warp & 3) * 32, j0 = ((warp >> 2) * (B / 64) + k) * 32;
         float a[32], t[32];
@@ -458,6 +484,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         store32(S2, i0 - lo + lane, j0, a);  // F
       }
       tmem_st_wait();
+      CTR(2);
       publish<B>();
       if (issuer) {
         mma<B>(A0, s0, s1, NEG_B, false);  // Q E = S0 (-S1)^T          (E = -E^T)
@@ -466,6 +493,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         commit<B>(bar);
       }
       wait_mma(bar, phase);
+      CTR(3);
       // ---- S2 <- Q E ; S1 <- Z = E - V/2 = (A1 + E) / 2   (A1 = E - V)
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
@@ -478,6 +506,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < 32; ++k) e[k] = 0.5f * (e[k] + v[k]);
         store32(S1, r, c, e);
       }
+      CTR(4);
       publish<B>();
       if (issuer) {
         mma<B>(A0, s0, s0, NEG_B, false);  // Q Q
@@ -485,6 +514,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         commit<B>(bar);
       }
       wait_mma(bar, phase);
+      CTR(5);
       // ---- S0 <- Q^2
 #pragma unroll 1
       for (int c = c_lo; c < c_lo + CF::HALF; c += 32) {
@@ -492,6 +522,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         tmem_ld(A0 + tl + c, v);
         store32(S0, r, c, v);
       }
+      CTR(6);
       publish<B>();
       if (issuer) {
         mma<B>(A1, s1, s0, 0, true);      // += Z Q^2        (Q^2 = (Q^2)^T)
@@ -499,6 +530,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         commit<B>(bar);
       }
       wait_mma(bar, phase);
+      CTR(7);
       // ---- stage A1 = E + R (fp32, thread per row, odd pitch: conflict-free
       // for row and column reads) over the slabs, then per 32 x 32 tile of the
       // upper triangle g_ij = 2 A1_ij written as coalesced runs of packed rows.
@@ -515,6 +547,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int k = 0; k < 32; ++k) stage[r * CF::PITCH + c + k] = v[k];
       }
       __syncthreads();
+      CTR(8);
       float* out = dpacked + s * PAIRS;
       {
         constexpr int NT = B / 32, QT = 4;  // tiles per side; per 128-row quadrant
@@ -544,6 +577,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       // the next block's unpack overwrites this CTA's staging only after every
       // warp is done reading it (the peer never reads it)
       __syncthreads();
+      CTR(9);
     }
   }
 
@@ -635,3 +669,15 @@ int poetx_cnp_backward_fused(int64_t nb, int64_t b, const float* packed, const f
 }
 
 }  // extern "C"
+
+#ifdef POETX_CNP_TRACE
+extern "C" int poetx_cnp_trace_copy(unsigned long long* host, int n) {
+  if (n > 512 * 64) n = 512 * 64;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, poetx::cnpf::g_ctrace, n * sizeof(unsigned long long)));
+}
+extern "C" int poetx_cnp_trace_reset() {
+  void* p = nullptr;
+  if (cudaGetSymbolAddress(&p, poetx::cnpf::g_ctrace) != cudaSuccess) return 1;
+  return static_cast<int>(cudaMemset(p, 0, sizeof(poetx::cnpf::g_ctrace)));
+}
+#endif
