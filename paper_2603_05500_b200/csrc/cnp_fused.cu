@@ -65,7 +65,7 @@ struct Cfg {
   static constexpr int TILE = 32 * 33 * 4;       // per-warp 32 x 32 fp32 transpose tile
   // forward: two slabs (2Q, Q^2) + the next block's packed staging; backward:
   // three slabs + the per-warp transpose tiles (staging over S1 / S2)
-  static constexpr int STG_BYTES = PAIR ? (128 * 132 + 8128) * 4 : 8128 * 4;  // CTA 1 of a pair is the larger
+  static constexpr int STG_BYTES = PAIR ? 24512 * 4 : 8128 * 4;  // own packed rows (CTA 0 of a pair is the larger)
   static constexpr int BAR_OFF = (2 * SLAB + STG_BYTES) > (3 * SLAB + 8 * TILE) ? (2 * SLAB + STG_BYTES)
                                                                                 : (3 * SLAB + 8 * TILE);
   static constexpr int SMEM = BAR_OFF + 1024 + 64;
@@ -137,18 +137,40 @@ __device__ __forceinline__ int rowp(int i) {
   return i * B - (i * (i + 1)) / 2 - i - 1;
 }
 
+// build-time phase probe (-DPOETX_CNP_TRACE, tools/cnptrace.py): globaltimer
+// stamps of thread 0 per phase for the first 5 blocks of every CTA
+#ifdef POETX_CNP_TRACE
+__device__ unsigned long long g_ctrace[512 * 64];
+__device__ __forceinline__ void ctr(int it, int ph) {
+  if (threadIdx.x != 0 || it >= 5) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_ctrace[blockIdx.x * 64 + it * 12 + ph] = t;
+}
+#define CTR(ph) ctr(it, ph)
+__device__ unsigned long long g_ctrace_w[512 * 16];  // block 1: per-warp scatter start / end
+__device__ __forceinline__ void ctrw(int it, int slot) {
+  if ((threadIdx.x & 31) != 0 || it != 1) return;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  g_ctrace_w[blockIdx.x * 16 + slot] = t;
+}
+#define CTRW(slot) ctrw(it, slot)
+#else
+#define CTRW(slot) ((void)(slot))
+#define CTR(ph) ((void)(ph))
+#endif
+
 // Q rows [lo, lo + 128) of one block from the packed parameters staged in
 // shared memory by bulk copies (every global read is a contiguous packed-row
-// segment: no per-element loads on the critical path).  The CTA stages
-//   own:   packed rows [lo, lo + 128) (one contiguous range; 16 B aligned),
-//   front: for a pair's second CTA, columns [lo, lo + 128) of packed rows
-//          j < lo (one 16-byte aligned window per row, pitch FP floats)
-// into `stg` (the free S1/S2 slabs), waits on `bar`, then scatters: element
-// (j, c) of an own row is Q[j, c] (upper) and -Q[c, j] when c is an own row
-// too; a front element is -Q[c, j].  The diagonal is zeroed.
+// segment: no per-element loads on the critical path).  Each CTA stages its
+// own packed rows [lo, lo + 128) (one contiguous range, 16 B aligned) into
+// `stg` and waits on `bar`; a pair's second CTA reads the entries of rows
+// j < 128 it needs (-Q[c, j], its "front" columns) from the FIRST CTA's
+// staging through distributed shared memory instead of copying 128 separate
+// row windows (their bulk-copy requests cost ~4 us per block on warp 0).
 template <int B>
 struct Stage {
-  static constexpr int FP = 132;  // front row pitch (floats): 128 + up to 3 of alignment slack, 16 B multiple
   __device__ static int own_start(int lo) { return rowp<B>(lo) + lo + 1; }
   __device__ static int own_count(int lo) {
     const int hi = lo + 128 < B - 1 ? lo + 128 : B - 1;
@@ -160,67 +182,97 @@ template <int B>
 __device__ __forceinline__ void stage_issue(float* stg, const float* __restrict__ pk, int lo, uint64_t* bar,
                                             int lane) {
   using ST = Stage<B>;
-  const int front_rows = lo;  // rows j < lo (pair CTA 1 only)
-  float* own = stg + front_rows * ST::FP;
   const int os = ST::own_start(lo), oc = ST::own_count(lo);
-  if (lane == 0) {
-    uint32_t bytes = static_cast<uint32_t>(oc) * 4;
-    for (int j = 0; j < front_rows; ++j) {
-      const int g0 = rowp<B>(j) + lo, a = g0 & 3;
-      bytes += static_cast<uint32_t>((a + 128 + 3) / 4 * 16);
-    }
-    mbar_expect_tx(bar, bytes);
-  }
+  if (lane == 0) mbar_expect_tx(bar, static_cast<uint32_t>(oc) * 4);
   __syncwarp();
   fence_async_smem();  // earlier generic accesses of the staging area before the async copies
   if (lane == 0) {
     const char* src = reinterpret_cast<const char*>(pk + os);
     for (uint32_t o = 0; o < static_cast<uint32_t>(oc) * 4; o += 32768) {
       const uint32_t n = static_cast<uint32_t>(oc) * 4 - o < 32768 ? static_cast<uint32_t>(oc) * 4 - o : 32768;
-      bulk_load_1d(reinterpret_cast<char*>(own) + o, src + o, n, bar);
+      bulk_load_1d(reinterpret_cast<char*>(stg) + o, src + o, n, bar);
     }
   }
-  for (int j = lane; j < front_rows; j += 32) {
-    const int g0 = rowp<B>(j) + lo, a = g0 & 3;
-    bulk_load_1d(stg + j * ST::FP, pk + (g0 - a), static_cast<uint32_t>((a + 128 + 3) / 4 * 16), bar);
-  }
 }
-// every thread: wait for the staging, then scatter sc * Q into the K-major slab
+__device__ __forceinline__ uint32_t dsmem_rank0(uint32_t local) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(r) : "r"(local));
+  return r;
+}
+__device__ __forceinline__ float ld_dsmem(uint32_t a) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+  return v;
+}
+// every thread: wait for the staging (and, in a pair, for both CTAs' staging:
+// the second CTA reads the first's), then scatter sc * Q into the K-major slab.
+// The caller keeps the staging intact until the peer is done (cluster barrier).
 template <int B>
 __device__ __forceinline__ void stage_scatter(uint8_t* slab, const float* stg, int lo, uint64_t* bar, uint32_t& bph,
-                                              int warp, int lane, float sc) {
+                                              int warp, int lane, float sc, int it) {
+  (void)it;
   using ST = Stage<B>;
-  const int front_rows = lo;
-  const float* own = stg + front_rows * ST::FP;
+  const float* own = stg;
   const int os = ST::own_start(lo);
   mbar_wait(bar, bph);
   bph ^= 1;
-  auto put = [&](int r, int c, float v) {
-    *reinterpret_cast<__nv_bfloat16*>(slab + soff(r, c & ~7) + (c & 7) * 2) = __float2bfloat16_rn(v);
-  };
-  // own packed rows: upper entries of own rows, and their transposes when the column is an own row
-  const int hi = lo + 128 < B - 1 ? lo + 128 : B - 1;
-  for (int j = lo + warp; j < hi; j += 8) {
-    const float* row = own + (rowp<B>(j) - os);
-    for (int c = j + 1 + lane; c < B; c += 32) {
-      const float v = sc * row[c];
-      put(j - lo, c, v);
-      if (c < lo + 128) put(c - lo, j, -v);
+  CTR(10);
+  if constexpr (Cfg<B>::PAIR) pair::cluster_sync();  // the first CTA's rows have landed
+  // every 32 x 32 tile of this CTA's 128 x b slab: lane = slab row j, its 32
+  // values gathered from the staged packed rows, then four 16-byte stores
+  // into its own row (4 wavefronts per 512 bytes).  Right of the diagonal a
+  // value is Q[j, c] from packed row j (lanes 2-way bank conflicted at
+  // most); left of it -Q[c, j] from packed row c (lanes over consecutive j:
+  // conflict-free) -- for c < lo from the first CTA's staging (DSMEM); the
+  // diagonal tile mixes both and 0, selected arithmetically (per-element
+  // branches serialised the warp: 3 us per tile).
+  CTRW(2 * warp);
+  constexpr int CT = B / 32;
+  const uint32_t peer = lo ? dsmem_rank0(smem_u32(stg)) : 0u;  // first CTA's own staging (os = 0 there)
+  for (int u = warp; u < 4 * CT; u += 8) {
+    const int tr = u / CT, tc = u % CT;
+    const int j = lo + 32 * tr + lane, j0 = lo + 32 * tr, c0 = 32 * tc;
+    float v[32];
+    if (c0 < lo) {
+#pragma unroll
+      for (int x = 0; x < 32; ++x) v[x] = -sc * ld_dsmem(peer + 4u * static_cast<uint32_t>(rowp<B>(c0 + x) + j));
+    } else if (c0 < j0) {
+#pragma unroll
+      for (int x = 0; x < 32; ++x) v[x] = -sc * own[rowp<B>(c0 + x) - os + j];
+    } else if (c0 > j0) {
+      const float* row = own + (rowp<B>(j) - os);
+#pragma unroll
+      for (int x = 0; x < 32; ++x) v[x] = sc * row[c0 + x];
+    } else {
+      const int rj = rowp<B>(j) - os;
+#pragma unroll
+      for (int x = 0; x < 32; ++x) {
+        const int c = c0 + x;
+        // both offsets computed, selected arithmetically (c == j reads a
+        // harmless in-range neighbour and is multiplied by 0)
+        const int il = rowp<B>(c) - os + j, iu = rj + c;
+        const float val = own[c > j ? iu : il];
+        v[x] = static_cast<float>((c > j) - (c < j)) * sc * val;
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint4 w;
+      w.x = pack_bf16(__float_as_uint(v[8 * q + 0]), __float_as_uint(v[8 * q + 1]));
+      w.y = pack_bf16(__float_as_uint(v[8 * q + 2]), __float_as_uint(v[8 * q + 3]));
+      w.z = pack_bf16(__float_as_uint(v[8 * q + 4]), __float_as_uint(v[8 * q + 5]));
+      w.w = pack_bf16(__float_as_uint(v[8 * q + 6]), __float_as_uint(v[8 * q + 7]));
+      *reinterpret_cast<uint4*>(slab + soff(j - lo, c0 + 8 * q)) = w;
     }
   }
-  // front rows (j < lo): -Q[c, j] for the own columns c
-  for (int j = warp; j < front_rows; j += 8) {
-    const float* row = stg + j * ST::FP + ((rowp<B>(j) + lo) & 3) - lo;
-#pragma unroll 4
-    for (int c = lo + lane; c < lo + 128; c += 32) put(c - lo, j, -sc * row[c]);
-  }
-  if (threadIdx.x < 128) put(threadIdx.x, lo + threadIdx.x, 0.f);
+  CTRW(2 * warp + 1);
+  CTR(11);
 }
 template <int B>
 __device__ __forceinline__ void unpack_q_staged(uint8_t* slab, float* stg, const float* __restrict__ pk, int lo,
-                                                uint64_t* bar, uint32_t& bph, int warp, int lane) {
+                                                uint64_t* bar, uint32_t& bph, int warp, int lane, int it) {
   if (warp == 0) stage_issue<B>(stg, pk, lo, bar, lane);
-  stage_scatter<B>(slab, stg, lo, bar, bph, warp, lane, 1.f);
+  stage_scatter<B>(slab, stg, lo, bar, bph, warp, lane, 1.f, it);
 }
 
 // 32 x 32 tile of N1 = dG, one row per lane: a[x] = N1[i0 + lane, j0 + x]
@@ -286,20 +338,6 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
   fence_after();
 }
 
-// build-time phase probe (-DPOETX_CNP_TRACE, tools/cnptrace.py): globaltimer
-// stamps of thread 0 per phase for the first 5 blocks of every CTA
-#ifdef POETX_CNP_TRACE
-__device__ unsigned long long g_ctrace[512 * 64];
-__device__ __forceinline__ void ctr(int it, int ph) {
-  if (threadIdx.x != 0 || it >= 5) return;
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  g_ctrace[blockIdx.x * 64 + it * 12 + ph] = t;
-}
-#define CTR(ph) ctr(it, ph)
-#else
-#define CTR(ph) ((void)(ph))
-#endif
 
 template <int B, bool FWD>
 __global__ void __launch_bounds__(THREADS, 1)
@@ -390,7 +428,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     if constexpr (FWD) {
       // ---- S0 <- 2Q (the staged packed parameters, scaled exactly by 2)
-      stage_scatter<B>(S0, stg, lo, sbar, sphase, warp, lane, 2.f);
+      stage_scatter<B>(S0, stg, lo, sbar, sphase, warp, lane, 2.f, it);
       __syncthreads();  // the staging is consumed: the next block's copies may land
       CTR(1);
       publish<B>();
@@ -466,8 +504,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float* n1 = dg + s * static_cast<int64_t>(B) * B;
       // ---- S0 <- Q ; S1 <- E = N1 - N1^T ; S2 <- F = N1 + N1^T ; A1 <- E (fp32)
       // (warp w owns TMEM lanes [32 (w & 3), +32): its tiles are that row group)
-      unpack_q_staged<B>(S0, stg, pk, lo, sbar, sphase, warp, lane);
-      __syncthreads();  // the staging (S1 / S2) is read before E / F overwrite it
+      unpack_q_staged<B>(S0, stg, pk, lo, sbar, sphase, warp, lane, it);
+      cta_sync<B>();  // the staging (S1 / S2; the peer reads the first CTA's) is read before E / F overwrite it
       CTR(1);
       for (int k = 0; k < B / 64; ++k) {
         const int i0 = lo + (warp & 3) * 32, j0 = ((warp >> 2) * (B / 64) + k) * 32;
@@ -561,6 +599,31 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (k++ % 8 != warp) continue;
             const int i0 = 32 * ta, j0 = 32 * tb, j = j0 + lane;
             const bool trans = off && rank == 1;  // g_ij = -2 P_ji from own row j
+#ifndef POETX_CNP_OUT_OLD
+            // 16 rows at a time: every shared load (and, accumulating, every
+            // global read) of the group in flight before the stores
+#pragma unroll 1
+            for (int y0 = 0; y0 < 32; y0 += 16) {
+              float gv[16];
+#pragma unroll
+              for (int y = 0; y < 16; ++y) {
+                const int i = i0 + y0 + y;
+                gv[y] = j > i ? 2.f * (trans ? -stage[(j - lo) * CF::PITCH + i] : stage[(i - lo) * CF::PITCH + j]) : 0.f;
+              }
+              if (accumulate) {
+#pragma unroll
+                for (int y = 0; y < 16; ++y) {
+                  const int i = i0 + y0 + y;
+                  if (j > i) gv[y] += out[rowp<B>(i) + j];
+                }
+              }
+#pragma unroll
+              for (int y = 0; y < 16; ++y) {
+                const int i = i0 + y0 + y;
+                if (j > i) out[rowp<B>(i) + j] = gv[y];
+              }
+            }
+#else
 #pragma unroll 4
             for (int y = 0; y < 32; ++y) {
               const int i = i0 + y;
@@ -571,6 +634,7 @@ __global__ void __launch_bounds__(THREADS, 1)
                 *dst = accumulate ? *dst + gv : gv;
               }
             }
+#endif
           }
         }
       }
@@ -674,6 +738,10 @@ int poetx_cnp_backward_fused(int64_t nb, int64_t b, const float* packed, const f
 extern "C" int poetx_cnp_trace_copy(unsigned long long* host, int n) {
   if (n > 512 * 64) n = 512 * 64;
   return static_cast<int>(cudaMemcpyFromSymbol(host, poetx::cnpf::g_ctrace, n * sizeof(unsigned long long)));
+}
+extern "C" int poetx_cnp_trace_copy_w(unsigned long long* host, int n) {
+  if (n > 512 * 16) n = 512 * 16;
+  return static_cast<int>(cudaMemcpyFromSymbol(host, poetx::cnpf::g_ctrace_w, n * sizeof(unsigned long long)));
 }
 extern "C" int poetx_cnp_trace_reset() {
   void* p = nullptr;

@@ -51,7 +51,27 @@ for fwd, names in ((True, FWD), (False, BWD)):
     lib.poetx_cnp_trace_copy(buf, 512 * 64)
     t = np.frombuffer(buf, dtype=np.uint64).reshape(512, 64).astype(np.int64)
     ctas = [i for i in range(512) if t[i, 0] > 0]
+    if hasattr(lib, "poetx_cnp_trace_copy_w"):
+        bw = (C.c_ulonglong * (512 * 16))()
+        lib.poetx_cnp_trace_copy_w(bw, 512 * 16)
+        tw = np.frombuffer(bw, dtype=np.uint64).reshape(512, 16).astype(np.int64)
+        for rk in ((0, 1) if b == 256 else (0,)):
+            sub = [i for i in ctas if (i % 2 == rk or b != 256) and tw[i, 0] > 0]
+            if sub:
+                per = [np.mean([(tw[i, 2 * w + 1] - tw[i, 2 * w]) / 1000.0 for i in sub]) for w in range(8)]
+                print(f"   rank {rk} per-warp scatter (block 1): " + " ".join(f"{x:.2f}" for x in per))
     nph = len(names)
+    for rk in ((0, 1) if b == 256 else (0,)):
+        sub = [i for i in ctas if i % 2 == rk] if b == 256 else ctas
+        w, sc = [], []
+        for i in sub:
+            for it in range(1, 5):
+                t0, tw, t1 = t[i, it * 12], t[i, it * 12 + 10], t[i, it * 12 + 11]
+                if t0 > 0 and tw > 0 and t1 > 0:
+                    w.append((tw - t0) / 1000.0)
+                    sc.append((t1 - tw) / 1000.0)
+        if w:
+            print(f"   rank {rk}: staging wait {np.mean(w):.2f} us, scatter part 1 {np.mean(sc):.2f} us")
     d = []  # [cta, block, phase] durations
     for i in ctas:
         for it in range(1, 5):
@@ -60,6 +80,18 @@ for fwd, names in ((True, FWD), (False, BWD)):
                 d.append(np.diff(row) / 1000.0)
     d = np.array(d)
     blk = d.sum(axis=1)
+    if b == 256:
+        for rk in (0, 1):
+            dd = []
+            for i in ctas:
+                if i % 2 != rk:
+                    continue
+                for it in range(1, 5):
+                    row = t[i, it * 12: it * 12 + nph]
+                    if (row > 0).all():
+                        dd.append(np.diff(row) / 1000.0)
+            dd = np.array(dd)
+            print(f"   rank {rk} phases: " + "  ".join(f"{x:.2f}" for x in dd.mean(axis=0)))
     print(f"== {'forward' if fwd else 'backward'} b={b}, {nb} blocks, {len(ctas)} CTAs: launch {e0.elapsed_time(e1) * 1000:.1f} us, "
           f"{e0.elapsed_time(e1) * 1000 / max(1, nb / (len(ctas) // (2 if b == 256 else 1))):.2f} us per block round")
     print(f"   per block (thread 0, blocks 1-4): mean {blk.mean():.2f} us  (min {blk.min():.2f}, max {blk.max():.2f})")
