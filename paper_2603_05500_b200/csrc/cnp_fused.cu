@@ -148,12 +148,12 @@ __device__ __forceinline__ void ctr(int it, int ph) {
   g_ctrace[blockIdx.x * 64 + it * 12 + ph] = t;
 }
 #define CTR(ph) ctr(it, ph)
-__device__ unsigned long long g_ctrace_w[512 * 16];  // block 1: per-warp scatter start / end
+__device__ unsigned long long g_ctrace_w[512 * 32];  // block 1: per-warp scatter / output start, end
 __device__ __forceinline__ void ctrw(int it, int slot) {
   if ((threadIdx.x & 31) != 0 || it != 1) return;
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  g_ctrace_w[blockIdx.x * 16 + slot] = t;
+  g_ctrace_w[blockIdx.x * 32 + slot] = t;
 }
 #define CTRW(slot) ctrw(it, slot)
 #else
@@ -587,6 +587,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncthreads();
       CTR(8);
       float* out = dpacked + s * PAIRS;
+      CTRW(16 + 2 * warp);
       {
         constexpr int NT = B / 32, QT = 4;  // tiles per side; per 128-row quadrant
         const int q0 = lo / 32;             // this CTA's diagonal quadrant
@@ -605,10 +606,14 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
             for (int y0 = 0; y0 < 32; y0 += 16) {
               float gv[16];
+              // unconditional loads, arithmetic selects (a load under a
+              // per-lane condition compiles to a divergent branch per row)
+              const float sg = trans ? -2.f : 2.f;
 #pragma unroll
               for (int y = 0; y < 16; ++y) {
                 const int i = i0 + y0 + y;
-                gv[y] = j > i ? 2.f * (trans ? -stage[(j - lo) * CF::PITCH + i] : stage[(i - lo) * CF::PITCH + j]) : 0.f;
+                const float val = stage[trans ? (j - lo) * CF::PITCH + i : (i - lo) * CF::PITCH + j];
+                gv[y] = j > i ? sg * val : 0.f;
               }
               if (accumulate) {
 #pragma unroll
@@ -620,7 +625,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int y = 0; y < 16; ++y) {
                 const int i = i0 + y0 + y;
+#if POETX_CNP_OUT_PROBE == 1
+                if (j > i && gv[y] == 12345.f) out[rowp<B>(i) + j] = gv[y];  // probe: stores compiled out
+#else
                 if (j > i) out[rowp<B>(i) + j] = gv[y];
+#endif
               }
             }
 #else
@@ -638,6 +647,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
         }
       }
+      CTRW(17 + 2 * warp);
       // the next block's unpack overwrites this CTA's staging only after every
       // warp is done reading it (the peer never reads it)
       __syncthreads();
@@ -740,7 +750,7 @@ extern "C" int poetx_cnp_trace_copy(unsigned long long* host, int n) {
   return static_cast<int>(cudaMemcpyFromSymbol(host, poetx::cnpf::g_ctrace, n * sizeof(unsigned long long)));
 }
 extern "C" int poetx_cnp_trace_copy_w(unsigned long long* host, int n) {
-  if (n > 512 * 16) n = 512 * 16;
+  if (n > 512 * 32) n = 512 * 32;
   return static_cast<int>(cudaMemcpyFromSymbol(host, poetx::cnpf::g_ctrace_w, n * sizeof(unsigned long long)));
 }
 extern "C" int poetx_cnp_trace_reset() {

@@ -52,14 +52,17 @@ for fwd, names in ((True, FWD), (False, BWD)):
     t = np.frombuffer(buf, dtype=np.uint64).reshape(512, 64).astype(np.int64)
     ctas = [i for i in range(512) if t[i, 0] > 0]
     if hasattr(lib, "poetx_cnp_trace_copy_w"):
-        bw = (C.c_ulonglong * (512 * 16))()
-        lib.poetx_cnp_trace_copy_w(bw, 512 * 16)
-        tw = np.frombuffer(bw, dtype=np.uint64).reshape(512, 16).astype(np.int64)
+        bw = (C.c_ulonglong * (512 * 32))()
+        lib.poetx_cnp_trace_copy_w(bw, 512 * 32)
+        tw = np.frombuffer(bw, dtype=np.uint64).reshape(512, 32).astype(np.int64)
         for rk in ((0, 1) if b == 256 else (0,)):
             sub = [i for i in ctas if (i % 2 == rk or b != 256) and tw[i, 0] > 0]
             if sub:
                 per = [np.mean([(tw[i, 2 * w + 1] - tw[i, 2 * w]) / 1000.0 for i in sub]) for w in range(8)]
                 print(f"   rank {rk} per-warp scatter (block 1): " + " ".join(f"{x:.2f}" for x in per))
+                if not fwd and all(tw[i, 16] > 0 for i in sub):
+                    per = [np.mean([(tw[i, 17 + 2 * w] - tw[i, 16 + 2 * w]) / 1000.0 for i in sub]) for w in range(8)]
+                    print(f"   rank {rk} per-warp output (block 1): " + " ".join(f"{x:.2f}" for x in per))
     nph = len(names)
     for rk in ((0, 1) if b == 256 else (0,)):
         sub = [i for i in ctas if i % 2 == rk] if b == 256 else ctas
