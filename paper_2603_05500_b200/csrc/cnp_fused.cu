@@ -341,9 +341,9 @@ __device__ __forceinline__ void wait_mma(uint64_t* bar, uint32_t& phase) {
 
 template <int B, bool FWD>
 __global__ void __launch_bounds__(THREADS, 1)
-    cnp_fused_kernel(int64_t nb, const float* __restrict__ packed, const float* __restrict__ dg,
-                     __nv_bfloat16* __restrict__ g16, float* __restrict__ g32, float* __restrict__ dpacked,
-                     int accumulate) {
+    cnp_fused_kernel(const __grid_constant__ CUtensorMap gmap, int64_t nb, const float* __restrict__ packed,
+                     const float* __restrict__ dg, __nv_bfloat16* __restrict__ g16, float* __restrict__ g32,
+                     float* __restrict__ dpacked, int accumulate) {
   using CF = Cfg<B>;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment by offsetting the shared array itself (keeps the
@@ -429,6 +429,9 @@ __global__ void __launch_bounds__(THREADS, 1)
     if constexpr (FWD) {
       // ---- S0 <- 2Q (the staged packed parameters, scaled exactly by 2)
       stage_scatter<B>(S0, stg, lo, sbar, sphase, warp, lane, 2.f, it);
+      // S1 is rewritten after the first product: the previous block's G
+      // stores (TMA, from S1) must have read it
+      if (g16 && threadIdx.x == 0) bulk_wait_read<0>();
       __syncthreads();  // the staging is consumed: the next block's copies may land
       CTR(1);
       publish<B>();
@@ -487,13 +490,16 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       CTR(5);
       if (g16) {
+        // the bf16 rows of G leave through TMA stores straight from the
+        // swizzled slab (one 64-column x 128-row box per 128-byte atom column);
+        // they drain while the next block unpacks and multiplies
+        fence_async_smem();
         __syncthreads();
-        // one 16-byte unit per lane: each warp instruction writes a coalesced row
-        __nv_bfloat16* gb = g16 + (s * B + lo) * B;
-        for (int e = threadIdx.x; e < 128 * (B / 8); e += THREADS) {
-          const int row = e / (B / 8), u = e % (B / 8);
-          *reinterpret_cast<uint4*>(gb + static_cast<int64_t>(row) * B + 8 * u) =
-              *reinterpret_cast<const uint4*>(S1 + soff(row, 8 * u));
+        if (threadIdx.x == 0) {
+#pragma unroll
+          for (int k = 0; k < B / 64; ++k)
+            tma_store_2d(&gmap, S1 + k * 16384, 64 * k, static_cast<int>(s * B + lo));
+          bulk_commit();
         }
       }
       // the next block's unpack overwrites S0 / S1 only after this CTA's
@@ -655,6 +661,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
   }
 
+  if (FWD && g16 && threadIdx.x == 0) bulk_wait<0>();  // G stores done with the slab
   fence_before();
   cta_sync<B>();
   fence_after();
@@ -676,6 +683,9 @@ int launch(int64_t nb, const float* packed, const float* dg, __nv_bfloat16* g16,
   }();
   POETX_REQUIRE(attr, POETX_ECUDA, "cnp_fused: cannot opt in to %d B of shared memory", CF::SMEM);
   const int64_t sms = num_sms();
+  CUtensorMap gmap{};
+  if (FWD && g16)  // G as [nb * B rows, B cols] bf16, 64 x 128 boxes, 128-byte swizzle (the slab layout)
+    POETX_TRY(make_map(&gmap, g16, B, static_cast<uint64_t>(nb) * B, B, 64, 128));
   unsigned grid;
   if constexpr (CF::PAIR) {
     const int64_t pairs = nb < sms / 2 ? nb : sms / 2;
@@ -693,7 +703,7 @@ int launch(int64_t nb, const float* packed, const float* dg, __nv_bfloat16* g16,
     cfg.attrs = at;
     cfg.numAttrs = 1;
     void* pf = prof_begin(st);
-    cudaLaunchKernelEx(&cfg, kern, nb, packed, dg, g16, g32, dpacked, accumulate);
+    cudaLaunchKernelEx(&cfg, kern, gmap, nb, packed, dg, g16, g32, dpacked, accumulate);
     prof_end(pf, FWD ? "cnp_fused_fwd" : "cnp_fused_bwd", (FWD ? 2.0 : 7.0) * 2.0 * B * B * B * nb, st);
   } else {
     static int per_sm = [&] {
@@ -704,7 +714,7 @@ int launch(int64_t nb, const float* packed, const float* dg, __nv_bfloat16* g16,
     const int64_t ctas = nb < per_sm * sms ? nb : per_sm * sms;
     grid = static_cast<unsigned>(ctas);
     void* pf = prof_begin(st);
-    kern<<<grid, THREADS, CF::SMEM, st>>>(nb, packed, dg, g16, g32, dpacked, accumulate);
+    kern<<<grid, THREADS, CF::SMEM, st>>>(gmap, nb, packed, dg, g16, g32, dpacked, accumulate);
     prof_end(pf, FWD ? "cnp_fused_fwd" : "cnp_fused_bwd", (FWD ? 2.0 : 7.0) * 2.0 * B * B * B * nb, st);
   }
   POETX_LAUNCHED(FWD ? "cnp_fused_fwd" : "cnp_fused_bwd");
