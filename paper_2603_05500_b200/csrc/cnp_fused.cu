@@ -248,11 +248,12 @@ __device__ __forceinline__ void stage_scatter(uint8_t* slab, const float* stg, i
 #pragma unroll
       for (int x = 0; x < 32; ++x) {
         const int c = c0 + x;
-        // both offsets computed, selected arithmetically (c == j reads a
-        // harmless in-range neighbour and is multiplied by 0)
+        // both offsets computed and selected (c == j reads staged element 0;
+        // the value is selected away, never multiplied: 0 * NaN of a stale
+        // word would poison the diagonal)
         const int il = rowp<B>(c) - os + j, iu = rj + c;
-        const float val = own[c > j ? iu : il];
-        v[x] = static_cast<float>((c > j) - (c < j)) * sc * val;
+        const float val = own[c > j ? iu : (c < j ? il : 0)];
+        v[x] = c > j ? sc * val : (c < j ? -sc * val : 0.f);
       }
     }
 #pragma unroll
