@@ -230,7 +230,9 @@ __device__ __forceinline__ void stage_scatter(uint8_t* slab, const float* stg, i
   constexpr int CT = B / 32;
   const uint32_t peer = lo ? dsmem_rank0(smem_u32(stg)) : 0u;  // first CTA's own staging (os = 0 there)
   for (int u = warp; u < 4 * CT; u += 8) {
-    const int tr = u / CT, tc = u % CT;
+    // pair: rotate the column tile by half a row of tiles on odd row tiles,
+    // so every warp of the second CTA gets two front (DSMEM) tiles, not four
+    const int tr = u / CT, tc = Cfg<B>::PAIR ? (u % CT + (tr & 1) * (CT / 2)) % CT : u % CT;
     const int j = lo + 32 * tr + lane, j0 = lo + 32 * tr, c0 = 32 * tc;
     float v[32];
     if (c0 < lo) {
