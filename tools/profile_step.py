@@ -130,7 +130,8 @@ if args.timeline:
                 only = next(iter(active.values()))
                 alone[tfam(only)] += dt
                 if "cnp_fused" in only["name"]:
-                    cnp_alone.append((last - t0, dt, tfam(only), prev_end["name"][:50] if prev_end else "-"))
+                    cnp_alone.append((last - t0, dt, tfam(only), prev_end["name"][:50] if prev_end else "-",
+                                      f"{ev['name'][:50]} (stream {ev.get('tid')}, cnp on {only.get('tid')})"))
             else:
                 for e2 in active.values():
                     overl[tfam(e2)] += dt / len(active)
@@ -151,9 +152,9 @@ if args.timeline:
     for f, us in sorted(alone.items(), key=lambda x: -x[1]):
         print(f"  {us / 1e3 / args.steps:8.3f}  {f}")
     print(f"  {sum(alone.values()) / 1e3 / args.steps:8.3f}  total")
-    print("CNP kernels running alone (offset in the trace us, duration us, which, last kernel to end before):")
-    for off, dt, f, before in sorted(cnp_alone, key=lambda x: -x[1])[:16]:
-        print(f"  {off:10.1f} {dt:8.1f}  {f:28s} {before}")
+    print("CNP kernels running alone (offset in the trace us, duration us, which, last kernel to end before, next edge):")
+    for off, dt, f, before, after in sorted(cnp_alone, key=lambda x: -x[1])[:16]:
+        print(f"  {off:10.1f} {dt:8.1f}  {f:28s} {before}  ->  {after}")
     print("overlapped time, shared equally among running kernels (ms/step):")
     for f, us in sorted(overl.items(), key=lambda x: -x[1]):
         print(f"  {us / 1e3 / args.steps:8.3f}  {f}")
