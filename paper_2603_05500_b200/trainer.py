@@ -446,18 +446,27 @@ class _CnpBackwardHook(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dh):
         model = ctx.model
+        # every block of decoder blocks >= i has its dG: launch the largest
+        # whole number of CNP waves from the top of what is ready (the rest
+        # joins the next launch; the last hook takes everything left), so no
+        # launch ends on a nearly empty wave (154 blocks = 2.08 waves of 74)
+        off, _ = model.block_ranges[ctx.i]
+        hi = model.cnp_bwd_lo
+        start = off if ctx.i == 0 else hi - ((hi - off) // model.cnp_wave) * model.cnp_wave
+        if start >= hi:
+            return dh, None, None
         cs = model.cnp_stream
         cs.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(cs):
-            off, nb = model.block_ranges[ctx.i]
-            model.stack.backward_factors_range(off, nb)
+            model.stack.backward_factors_range(start, hi - start)
             if model.dp_group is not None:
-                # data parallel: this block's packed gradients are final -- start
-                # their all-reduce now so it overlaps the blocks below (the step
-                # waits on every handle before the optimizer)
+                # data parallel: these packed gradients are final -- start their
+                # all-reduce now so it overlaps the blocks below (the step waits
+                # on every handle before the optimizer)
                 pairs = model.stack.pairs
-                model.dp_works.append(_all_reduce_async(model.poet.grad[off * pairs:(off + nb) * pairs],
+                model.dp_works.append(_all_reduce_async(model.poet.grad[start * pairs:hi * pairs],
                                                         model.dp_group))
+        model.cnp_bwd_lo = start
         return dh, None, None
 
 
@@ -808,6 +817,14 @@ class PoetLlama(torch.nn.Module):
             self.block_ranges.append((lo, hi - lo))
         self.cnp_pipelined = False  # set per step by the trainer
         self.cnp_bwd_whole = False
+        # CNP launches come in whole waves of the persistent kernel (a CTA pair
+        # per b = 256 block, a CTA per b = 128 block on each SM); env
+        # POETX_CNP_WAVES=0: one launch per decoder block
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count if dev.type == "cuda" else 148
+        waves = os.environ.get("POETX_CNP_WAVES", "1") != "0"
+        self.cnp_wave = (sms // 2 if self.stack.b == 256 else sms) if waves else 1
+        self.cnp_fwd_done = 0
+        self.cnp_bwd_lo = 0
         # bf16 weight folds of one decoder block (forward bd(G_R) PM, backward
         # PM bd(G_P)), double-buffered by block parity and built on the CNP
         # stream one block ahead of their use
@@ -881,6 +898,18 @@ class PoetLlama(torch.nn.Module):
         return all(m.desc.fold_weight and m.desc.dtype == N.BF16 and m.b % 64 == 0 and m.b <= 256 and m.n % 256 == 0
                    for m in self.poet_layers())
 
+    def cnp_forward_to(self, end: int):
+        """G of every block below ``end`` is launched on the current stream:
+        extend the computed prefix to ``end`` rounded up to whole CNP waves
+        (blocks of later decoder blocks computed early are final: the packed
+        parameters only change in the optimizer)."""
+        if end <= self.cnp_fwd_done:
+            return
+        w = self.cnp_wave
+        tgt = min(self.stack.nb, -(-end // w) * w)
+        self.stack.forward_factors_range(self.cnp_fwd_done, tgt - self.cnp_fwd_done)
+        self.cnp_fwd_done = tgt
+
     def launch_in_folds(self, i: int):
         """Forward folds bd(G_R) PM of block i, on the current stream."""
         for p in self.PROJ:
@@ -927,10 +956,11 @@ class PoetLlama(torch.nn.Module):
         self.cnp_bwd_whole = pipe and os.environ.get("POETX_CNP_BWD_WHOLE", "0") == "1"
         if pipe:
             self.cnp_stream.wait_stream(main)  # fork (also joins it into a graph capture)
+            self.cnp_fwd_done, self.cnp_bwd_lo = 0, self.stack.nb
             if whole_fwd:  # every block's G in one launch (full waves, no per-block tail)
                 self.stack.forward_factors_range(0, self.stack.nb)
             else:
-                self.stack.forward_factors_range(*self.block_ranges[0])
+                self.cnp_forward_to(sum(self.block_ranges[0]))
             if folds:
                 self.launch_in_folds(0)
         for i, mods in enumerate(self.layers):
@@ -943,7 +973,7 @@ class PoetLlama(torch.nn.Module):
                     self.cnp_stream.wait_stream(main)
                     with torch.cuda.stream(self.cnp_stream):
                         if not whole_fwd:
-                            self.stack.forward_factors_range(*self.block_ranges[i + 1])
+                            self.cnp_forward_to(sum(self.block_ranges[i + 1]))
                         if folds:
                             self.launch_in_folds(i + 1)
                 if not self.cnp_bwd_whole:
