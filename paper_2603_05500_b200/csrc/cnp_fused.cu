@@ -621,7 +621,11 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
               for (int y = 0; y < 16; ++y) {
                 const int i = i0 + y0 + y;
+#if POETX_CNP_OUT_PROBE == 3
+                const float val = static_cast<float>(i * j);  // probe: no staging loads
+#else
                 const float val = stage[trans ? (j - lo) * CF::PITCH + i : (i - lo) * CF::PITCH + j];
+#endif
                 gv[y] = j > i ? sg * val : 0.f;
               }
               if (accumulate) {
@@ -636,6 +640,8 @@ __global__ void __launch_bounds__(THREADS, 1)
                 const int i = i0 + y0 + y;
 #if POETX_CNP_OUT_PROBE == 1
                 if (j > i && gv[y] == 12345.f) out[rowp<B>(i) + j] = gv[y];  // probe: stores compiled out
+#elif POETX_CNP_OUT_PROBE == 2
+                out[((i * 8 + (j0 >> 5)) * 32 + lane) & 16383] = gv[y];  // probe: aligned 128-byte rows
 #else
                 if (j > i) out[rowp<B>(i) + j] = gv[y];
 #endif

@@ -1,4 +1,3 @@
 mkdir -p gpurun_out
-( POETX_LIB_PATH=abtest/lib_ctrace.so timeout 300 python tools/cnptrace.py 3696 256
-  timeout 300 python tools/cnpbench.py; timeout 300 python tools/cnpbench.py 3696 128 ) > gpurun_out/cnptrace8.txt 2>&1
-cat gpurun_out/cnptrace8.txt
+( for v in ctrace ctrace_o2 ctrace_o3; do echo "## $v"; POETX_LIB_PATH=abtest/lib_$v.so timeout 300 python tools/cnptrace.py 3696 256 | grep "per-warp output\|packed output\|== backward"; done ) > gpurun_out/cnptrace_out.txt 2>&1
+cat gpurun_out/cnptrace_out.txt
