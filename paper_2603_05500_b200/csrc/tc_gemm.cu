@@ -415,6 +415,11 @@ __device__ __forceinline__ void gtr(int slot) {
 #else
 #define GTR(slot) ((void)(slot))
 #endif
+// 512-row tiles: K blocks at the end of a tile that run sub-tile 0 first
+// (0: both sub-tiles interleaved to the end, as round 2 first shipped)
+#ifndef POETX_PAIR_TAIL
+#define POETX_PAIR_TAIL 3
+#endif
 // timeline probe knob (-DPOETX_EPI_PROBE=1: no TMA stores); results invalid
 #ifndef POETX_EPI_PROBE
 #define POETX_EPI_PROBE 0
@@ -660,6 +665,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
           int g, sp, m0, n0, kb0, kbn;
           decode(tile, g, sp, m0, n0, kb0, kbn);
           const int lead = kbn < STAGES ? kbn : STAGES;
+          // the last `tail` K blocks run sub-tile 0 first (stages held), so its
+          // accumulator completes -- and the epilogue starts draining it --
+          // while sub-tile 1 finishes: the next tile's first MMA waits for
+          // that drain (single-buffered TMEM), now mostly hidden
+          const int tail = kbn > lead ? (POETX_PAIR_TAIL < kbn - lead ? POETX_PAIR_TAIL : kbn - lead) : 0;
           const int tj = (tile - cluster) / nclusters;
           // sub-tile 0 starts on the first `lead` stages as soon as its
           // accumulator is drained; sub-tile 1 follows on the same (held)
@@ -672,7 +682,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
             mbar_wait(&full[stage], phase);
             fence_after();
             if (kb == 0 && lane == 0) GTR(4 + tj * 5 + 0);
-            if (lane == 0) mma_stage(stage, 0, tmem_base, kb != 0);
+            if (lane == 0) {
+              mma_stage(stage, 0, tmem_base, kb != 0);
+              if (kb == kbn - 1) commit2(&tfull[0]);
+            }
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
@@ -684,24 +697,56 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
             if (lane == 0) {
               mma_stage(stage, 1, tmem_base + 256, kb != 0);
               commit2(&empty[stage]);
-              if (kb == kbn - 1) commit2(&tfull[0]);
+              if (kb == kbn - 1) commit2(&tfull[1]);
             }
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          for (int kb = lead; kb < kbn; ++kb) {
+          for (int kb = lead; kb < kbn - tail; ++kb) {
             mbar_wait(&full[stage], phase);
             fence_after();
             if (lane == 0) {
               mma_stage(stage, 0, tmem_base, true);
               mma_stage(stage, 1, tmem_base + 256, true);
               commit2(&empty[stage]);
-              if (kb == kbn - 1) { commit2(&tfull[0]); GTR(4 + tj * 5 + 1); }
+              if (kb == kbn - 1) {  // no tail
+                commit2(&tfull[0]);
+                commit2(&tfull[1]);
+                GTR(4 + tj * 5 + 1);
+              }
             }
             __syncwarp();
             if (++stage == STAGES) { stage = 0; phase ^= 1; }
           }
-          if (kbn == 0 && lane == 0) commit2(&tfull[0]);  // empty K range
+          if (tail > 0) {
+            const int st1 = stage;
+            const uint32_t ph1 = phase;
+            for (int kb = kbn - tail; kb < kbn; ++kb) {
+              mbar_wait(&full[stage], phase);
+              fence_after();
+              if (lane == 0) {
+                mma_stage(stage, 0, tmem_base, true);
+                if (kb == kbn - 1) commit2(&tfull[0]);
+              }
+              __syncwarp();
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+            stage = st1;
+            phase = ph1;
+            for (int kb = kbn - tail; kb < kbn; ++kb) {
+              if (lane == 0) {
+                mma_stage(stage, 1, tmem_base + 256, true);
+                commit2(&empty[stage]);
+                if (kb == kbn - 1) { commit2(&tfull[1]); GTR(4 + tj * 5 + 1); }
+              }
+              __syncwarp();
+              if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+          }
+          if (kbn == 0 && lane == 0) {  // empty K range
+            commit2(&tfull[0]);
+            commit2(&tfull[1]);
+          }
           __syncwarp();
           tph ^= 1;
         }
@@ -716,13 +761,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Q8 ? Q8_THREADS : TH
     for (int tile = cluster; tile < num_tiles; tile += nclusters) {
       int g, sp, m0, n0, kb0, kbn;
       decode(tile, g, sp, m0, n0, kb0, kbn);
-      const int tf = MS == 1 ? acc : 0;
-      mbar_wait(&tfull[tf], acc_phase);
+      // MS = 1: one accumulator per tile; MS = 2: sub-tile h completes on tfull[h]
+      mbar_wait(&tfull[MS == 1 ? acc : 0], acc_phase);
       fence_after();
       const int tj = (tile - cluster) / nclusters;
       if (ew == 0 && lane == 0) GTR(4 + tj * 5 + 2);
 #pragma unroll 1
       for (int h = 0; h < MS; ++h) {
+        if (MS == 2 && h == 1) {
+          mbar_wait(&tfull[1], acc_phase);
+          fence_after();
+        }
         const int row0 = m0 + h * 256 + rank * HALF + ew * 32;  // this warp's 32 rows (within the group)
         const int64_t crow = args.c_row0 + g * args.c_grow + sp * args.c_srow + row0;
         const uint32_t tbase = tmem_base + (static_cast<uint32_t>(ew * 32) << 16) + (MS == 1 ? acc : h) * 256;
