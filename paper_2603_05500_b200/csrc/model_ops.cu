@@ -19,6 +19,9 @@
 #include "common.cuh"
 #include "tile8.cuh"
 
+#ifndef POETX_ROW_PROBE
+#define POETX_ROW_PROBE 0
+#endif
 namespace poetx {
 namespace {
 
@@ -186,6 +189,22 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
 #pragma unroll
     for (int k = 0; k < K; ++k)
       stage_rows(dus_s + k * RT * d, static_cast<const __nv_bfloat16*>(dus.ptr[k]) + r0 * d, nr, d);
+    // the second pass's global reads (residual gradient, rstd) issued now, so
+    // their latency hides under the staging and the first pass instead of
+    // stalling every row of the second pass
+    uint4 resv[2][RT];
+    float rsv[RT];
+#pragma unroll
+    for (int r = 0; r < RT; ++r) {
+      rsv[r] = r < nr ? rstd_in[r0 + r] : 0.f;
+#pragma unroll
+      for (int slot = 0; slot < 2; ++slot) {
+        const int i = threadIdx.x + slot * kThreads;
+        resv[slot][r] = (dres && r < nr && i < nvec)
+                            ? __ldcs(reinterpret_cast<const uint4*>(dres + (r0 + r) * d) + i)
+                            : make_uint4(0u, 0u, 0u, 0u);
+      }
+    }
     cp_wait_all();
     __syncthreads();
     float dot[RT];
@@ -195,6 +214,12 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
       int iv[K][8];
 #pragma unroll
       for (int k = 0; k < K; ++k) load_idx8(dus.idx[k], 8 * i, iv[k]);
+#if POETX_ROW_PROBE == 1  // timing probe: conflict-free identity gathers (results invalid)
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) iv[k][q] = (8 * i + q) ^ (iv[k][q] & 0);
+#endif
       float wv[8];
       load_f8(w + 8 * i, wv);
 #pragma unroll
@@ -231,16 +256,17 @@ __global__ void __launch_bounds__(kThreads) rmsnorm_gather_bwd_kernel(
       if (i >= nvec) break;
       float wv[8];
       load_f8(w + 8 * i, wv);
-      for (int r = 0; r < nr; ++r) {
+#pragma unroll
+      for (int r = 0; r < RT; ++r) {
+        if (r >= nr) break;
         float tot = 0.f;
 #pragma unroll
         for (int k = 0; k < 8; ++k) tot += red[r * 8 + k];
-        const float rs = rstd_in[r0 + r];
+        const float rs = rsv[r];
         const float coef = rs * rs * rs * tot / static_cast<float>(d);
         float xv[8], o[8], res[8];
         unpack8(reinterpret_cast<const uint4*>(xs + r * d)[i], xv);
-        if (dres)
-          unpack8(__ldcs(reinterpret_cast<const uint4*>(dres + (r0 + r) * d) + i), res);
+        if (dres) unpack8(resv[slot][r], res);
         const float4* dyp = reinterpret_cast<const float4*>(dy + r * d + 8 * i);
         const float4 d0 = dyp[0], d1 = dyp[1];
         const float dv[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
