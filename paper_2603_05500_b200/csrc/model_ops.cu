@@ -551,6 +551,10 @@ __device__ __forceinline__ void swiglu_bwd_tile(int64_t r0, int nr, int f, __nv_
     int ia[8], ib[8];
     load_idx8(A, 8 * i, ia);
     load_idx8(B, 8 * i, ib);
+#if POETX_ROW_PROBE == 1  // timing probe: conflict-free identity gathers (results invalid)
+#pragma unroll
+    for (int q = 0; q < 8; ++q) { ia[q] = (8 * i + q) ^ (ia[q] & 0); ib[q] = (8 * i + q) ^ (ib[q] & 0); }
+#endif
     for (int r = 0; r < nr; ++r) {
       const int o = r * f;
       float gself[8], g[8], ug[8];
@@ -571,6 +575,10 @@ __device__ __forceinline__ void swiglu_bwd_tile(int64_t r0, int nr, int f, __nv_
   for (int i = threadIdx.x; i < nvec; i += kThreads) {
     int id[8];
     load_idx8(D, 8 * i, id);
+#if POETX_ROW_PROBE == 1
+#pragma unroll
+    for (int q = 0; q < 8; ++q) id[q] = (8 * i + q) ^ (id[q] & 0);
+#endif
     for (int r = 0; r < nr; ++r) {
       const __nv_bfloat16* row = gs + r * f;
       float u[8];
