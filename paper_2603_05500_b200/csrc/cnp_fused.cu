@@ -609,7 +609,6 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (k++ % 8 != warp) continue;
             const int i0 = 32 * ta, j0 = 32 * tb, j = j0 + lane;
             const bool trans = off && rank == 1;  // g_ij = -2 P_ji from own row j
-#ifndef POETX_CNP_OUT_OLD
             // 16 rows at a time: every shared load (and, accumulating, every
             // global read) of the group in flight before the stores
 #pragma unroll 1
@@ -647,18 +646,6 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
               }
             }
-#else
-#pragma unroll 4
-            for (int y = 0; y < 32; ++y) {
-              const int i = i0 + y;
-              if (j > i) {
-                const float acc = trans ? -stage[(j - lo) * CF::PITCH + i] : stage[(i - lo) * CF::PITCH + j];
-                const float gv = 2.f * acc;
-                float* dst = out + rowp<B>(i) + j;
-                *dst = accumulate ? *dst + gv : gv;
-              }
-            }
-#endif
           }
         }
       }
