@@ -171,3 +171,27 @@ def test_layer_backward_dg_matches_packed(N):
     for got, want in ((gr, g_ref.q_r), (gp, g_ref.q_p)):
         err = (got - want).abs().max().item()
         assert err <= 2e-2 * max(1.0, want.abs().max().item()), err
+
+
+@pytest.mark.parametrize("K", [64, 192, 256, 320, 448, 512, 640, 2048])
+@pytest.mark.parametrize("ms", [1, 2])
+def test_pair_gemm_k_edges_of_the_tile_head_and_tail(N, K, ms):
+    """512-row pair tiles run the first min(K blocks, stages) K blocks on
+    sub-tile 0 first and the last up to 3 on sub-tile 0 first again
+    (POETX_PAIR_TAIL): K from one 64-wide block (head only) through
+    head + 1, head + tail with no middle, and long middles, against torch
+    fp32; 256-row tiles alongside.  Several tiles per CTA pair (M = 8192 on
+    74 pairs) so the head / tail hand-over between tiles is exercised."""
+    M, Nn = 8192, 1024
+    g = torch.Generator("cuda").manual_seed(K * 7 + ms)
+    a = torch.randn((M, K), device="cuda", generator=g).to(torch.bfloat16)
+    b = torch.randn((K, Nn), device="cuda", generator=g).to(torch.bfloat16)
+    N.lib().poetx_set_gemm_pair_ms(ms)
+    try:
+        c = matmul(N, a, b, 0)
+        torch.cuda.synchronize()
+    finally:
+        N.lib().poetx_set_gemm_pair_ms(0)
+    ref = a.float() @ b.float()
+    err = float((c.float() - ref).abs().max() / ref.abs().max())
+    assert err < 1e-2, err
