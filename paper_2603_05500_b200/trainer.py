@@ -431,6 +431,21 @@ def _swiglu_regather(vg, vu, maps):
     return _swiglu_fwd(vg, vu, maps, torch.empty_like(vg))
 
 
+def cnp_wave_fwd_target(end: int, done: int, wave: int, nb: int) -> int:
+    """Forward CNP prefix after a launch that must cover blocks < ``end``:
+    ``done`` rounded up past ``end`` to whole waves, capped at ``nb``."""
+    if end <= done:
+        return done
+    return min(nb, -(-end // wave) * wave)
+
+
+def cnp_wave_bwd_start(off: int, hi: int, wave: int, last: bool) -> int:
+    """Backward CNP launch [start, hi) once blocks >= ``off`` have their dG:
+    the largest whole number of waves below ``hi`` (everything left on the
+    last launch)."""
+    return off if last else hi - ((hi - off) // wave) * wave
+
+
 class _CnpBackwardHook(torch.autograd.Function):
     """Identity on the residual stream at a decoder block's input.  Its
     backward runs once every layer of the block has produced its dG (they
@@ -452,7 +467,7 @@ class _CnpBackwardHook(torch.autograd.Function):
         # launch ends on a nearly empty wave (154 blocks = 2.08 waves of 74)
         off, _ = model.block_ranges[ctx.i]
         hi = model.cnp_bwd_lo
-        start = off if ctx.i == 0 else hi - ((hi - off) // model.cnp_wave) * model.cnp_wave
+        start = cnp_wave_bwd_start(off, hi, model.cnp_wave, ctx.i == 0)
         if start >= hi:
             return dh, None, None
         cs = model.cnp_stream
@@ -903,10 +918,9 @@ class PoetLlama(torch.nn.Module):
         extend the computed prefix to ``end`` rounded up to whole CNP waves
         (blocks of later decoder blocks computed early are final: the packed
         parameters only change in the optimizer)."""
-        if end <= self.cnp_fwd_done:
+        tgt = cnp_wave_fwd_target(end, self.cnp_fwd_done, self.cnp_wave, self.stack.nb)
+        if tgt <= self.cnp_fwd_done:
             return
-        w = self.cnp_wave
-        tgt = min(self.stack.nb, -(-end // w) * w)
         self.stack.forward_factors_range(self.cnp_fwd_done, tgt - self.cnp_fwd_done)
         self.cnp_fwd_done = tgt
 
